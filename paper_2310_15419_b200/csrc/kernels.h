@@ -1,0 +1,52 @@
+// kernels.h -- internal launcher interface between the C ABI (sketch_api.cu) and the
+// sm_100a kernels (sketch_kernels.cu).  Not part of the public boundary.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "philox.cuh"
+
+namespace sk {
+
+// Threads per CTA of the fused apply kernels: 16 warps.
+constexpr int kWarps = 16;
+constexpr int kThreads = kWarps * 32;
+// Rows of Â owned by one warp.  Rademacher: 32 rows per lane (one 32-bit Philox word per
+// lane per nonzero).  Uniform / Gaussian: 16 rows per lane (8 Philox blocks per nonzero).
+constexpr int kRowsPerWarpRad = 1024;
+constexpr int kRowsPerWarpPair = 512;
+
+// One CTA of work: column `col`, Â rows [row0, row0 + (1 << wd_log2) * rows_per_warp).
+// The CTA's 16 warps are arranged as W_d = 1 << wd_log2 row-warps times
+// W_k = 16 >> wd_log2 slices of the column's nonzero stream.
+struct Item {
+  int32_t col;
+  int32_t row0;
+  int32_t wd_log2;
+  int32_t pad;
+};
+
+struct ApplyArgs {
+  const int64_t* colptr;
+  const int32_t* rowidx;
+  const void* vals;
+  void* out;
+  const Item* items;
+  int64_t n_items;
+  int64_t d;
+  int64_t ld;           // leading dimension of out (== d)
+  int64_t row_offset;
+  PhiloxKeys keys;
+};
+
+// dist: 0 = Rademacher, 1 = uniform, 2 = Gaussian; dtype: 0 = f64, 1 = f32.
+cudaError_t launch_apply(int dist, int dtype, const ApplyArgs& a, cudaStream_t stream);
+
+cudaError_t launch_fill_s(int dist, int dtype, uint64_t seed, int64_t i0, int64_t i1, int64_t j0,
+                          int64_t j1, void* out, int64_t ld, cudaStream_t stream);
+
+// Sets *flag (device int) nonzero if some rowidx is outside [0, m).
+cudaError_t launch_validate_rows(const int32_t* rowidx, int64_t nnz, int64_t m, int* flag,
+                                 cudaStream_t stream);
+
+}  // namespace sk

@@ -1,0 +1,464 @@
+// sketch_api.cu -- the C ABI of libsketch (include/sketch.h): argument checking, the plan
+// (validation + longest-first work schedule) and the launch of the sm_100a kernels.
+//
+// The plan is the GPU analogue of the paper's "format conversion" step (PAPER.md:444-445,
+// 619-641): the kji kernel needs only the CSC structure ("Algorithm 3 only
+// requires standard CSC"), so planning is just validation plus the order in which the
+// (column, Â-row tile) work items of Algorithm 1's outer loops are
+// handed to CTAs -- the parallelised outer loops of PAPER.md:327-332.
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/sketch.h"
+#include "kernels.h"
+#include "philox.cuh"
+
+using sk::Item;
+
+namespace {
+
+thread_local std::string g_detail;
+
+int cuda_fail(cudaError_t e, const char* what) {
+  g_detail = std::string(what) + ": " + cudaGetErrorString(e);
+  return SK_ECUDA;
+}
+
+#define SK_CUDA(call)                                  \
+  do {                                                 \
+    cudaError_t e_ = (call);                           \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+  } while (0)
+
+bool valid_dist(int d) { return d == SK_RADEMACHER || d == SK_UNIFORM || d == SK_GAUSSIAN; }
+bool valid_dtype(int t) { return t == SK_F64 || t == SK_F32; }
+size_t dtype_bytes(int t) { return t == SK_F64 ? 8 : 4; }
+
+constexpr int64_t kMaxD = (int64_t(1) << 31) - 1;
+constexpr int kSMs = 148;
+
+// Work schedule for one row-tiling (Rademacher: 1024 rows per warp; uniform/Gaussian: 512).
+struct Schedule {
+  std::vector<Item> items;
+  int64_t philox_blocks = 0;
+};
+
+// colptr: n+1 absolute offsets (colptr[0] may be nonzero for column sub-ranges).
+Schedule build_schedule(const int64_t* colptr, int64_t n, int64_t d, int rows_per_warp,
+                        int blocks_per_nnz_per_warp) {
+  Schedule S;
+  const int64_t n_rw = (d + rows_per_warp - 1) / rows_per_warp;  // row-warps covering d
+  // W_d (row-warps per CTA) minimising padded row-warps; ties -> larger W_d.
+  int base = 0;
+  int64_t best_waste = INT64_MAX;
+  for (int wdl = 4; wdl >= 0; --wdl) {
+    const int64_t WD = int64_t(1) << wdl;
+    const int64_t waste = ((n_rw + WD - 1) / WD) * WD - n_rw;
+    if (waste < best_waste) { best_waste = waste; base = wdl; }
+  }
+  auto cost_of = [&](int64_t L, int wdl) {
+    const int64_t WK = sk::kWarps >> wdl;
+    return (L + WK - 1) / WK + 2;   // per-warp nonzeros (+ store / reduction overhead)
+  };
+  // Average load per SM slot with the base shape; a column whose CTAs would each exceed a
+  // quarter of it is re-shaped to W_d = 1 (16 warps on its nonzero stream) so the longest
+  // CTAs do not set the makespan (column-length skew, e.g. power-law columns).
+  double total = 0;
+  for (int64_t k = 0; k < n; ++k) {
+    const int64_t L = colptr[k + 1] - colptr[k];
+    const int64_t tiles = (n_rw + (int64_t(1) << base) - 1) >> base;
+    total += (double)cost_of(L, base) * (double)tiles;
+  }
+  const double per_slot = total / kSMs;
+  std::vector<std::pair<int64_t, Item>> tmp;
+  for (int64_t k = 0; k < n; ++k) {
+    const int64_t L = colptr[k + 1] - colptr[k];
+    int wdl = base;
+    if (wdl > 0 && (double)cost_of(L, wdl) > 0.25 * per_slot) wdl = 0;
+    const int64_t WD = int64_t(1) << wdl;
+    const int64_t tiles = (n_rw + WD - 1) / WD;
+    for (int64_t tt = 0; tt < tiles; ++tt) {
+      Item it;
+      it.col = (int32_t)k;
+      it.row0 = (int32_t)(tt * WD * rows_per_warp);
+      it.wd_log2 = wdl;
+      it.pad = 0;
+      tmp.emplace_back(cost_of(L, wdl), it);
+    }
+    S.philox_blocks += L * tiles * WD * blocks_per_nnz_per_warp;
+  }
+  std::stable_sort(tmp.begin(), tmp.end(),
+                   [](const std::pair<int64_t, Item>& a, const std::pair<int64_t, Item>& b) {
+                     return a.first > b.first;
+                   });
+  S.items.reserve(tmp.size());
+  for (auto& pr : tmp) S.items.push_back(pr.second);
+  return S;
+}
+
+}  // namespace
+
+struct sk_plan_s {
+  sk_dtype_t dtype;
+  int64_t d, m, n, nnz, row_offset, max_col;
+  const int64_t* colptr;   // device (caller-owned)
+  const int32_t* rowidx;   // device (caller-owned)
+  Item* d_items = nullptr; // [rad items | pair items]
+  int64_t* owned_colptr = nullptr;  // device copy made by sketch_plan_host
+  int64_t n_rad = 0, n_pair = 0;
+  int64_t philox_rad = 0, philox_pair = 0;
+};
+
+namespace {
+
+int check_dims(sk_dtype_t dtype, int64_t d, int64_t m, int64_t n, int64_t row_offset) {
+  if (!valid_dtype(dtype) || d < 1 || d > kMaxD || m < 0 || m > kMaxD || n < 0 || n > kMaxD ||
+      row_offset < 0)
+    return SK_EINVAL;
+  return SK_OK;
+}
+
+int validate_colptr(const int64_t* h, int64_t n, int64_t nnz, bool require_zero_base) {
+  if (require_zero_base && h[0] != 0) return SK_ECSC;
+  if (h[n] - h[0] != nnz) return SK_ECSC;
+  for (int64_t k = 0; k < n; ++k)
+    if (h[k + 1] < h[k]) return SK_ECSC;
+  return SK_OK;
+}
+
+int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n, int64_t row_offset,
+              const int64_t* h_colptr, const int64_t* d_colptr, const int32_t* rowidx, int64_t nnz,
+              cudaStream_t stream) {
+  sk_plan_s* p = new (std::nothrow) sk_plan_s();
+  if (!p) return SK_ENOMEM;
+  p->dtype = dtype; p->d = d; p->m = m; p->n = n; p->nnz = nnz; p->row_offset = row_offset;
+  p->colptr = d_colptr; p->rowidx = rowidx;
+  p->max_col = 0;
+  for (int64_t k = 0; k < n; ++k) p->max_col = std::max(p->max_col, h_colptr[k + 1] - h_colptr[k]);
+  Schedule rad = build_schedule(h_colptr, n, d, sk::kRowsPerWarpRad, sk::kRowsPerWarpRad / 128);
+  Schedule pair = build_schedule(h_colptr, n, d, sk::kRowsPerWarpPair, sk::kRowsPerWarpPair / 2);
+  p->n_rad = (int64_t)rad.items.size();
+  p->n_pair = (int64_t)pair.items.size();
+  p->philox_rad = rad.philox_blocks;
+  p->philox_pair = pair.philox_blocks;
+  const int64_t total = p->n_rad + p->n_pair;
+  if (total > 0) {
+    cudaError_t e = cudaMalloc(&p->d_items, (size_t)total * sizeof(Item));
+    if (e != cudaSuccess) { delete p; return e == cudaErrorMemoryAllocation ? SK_ENOMEM : cuda_fail(e, "cudaMalloc(items)"); }
+    std::vector<Item> all(rad.items);
+    all.insert(all.end(), pair.items.begin(), pair.items.end());
+    e = cudaMemcpyAsync(p->d_items, all.data(), (size_t)total * sizeof(Item), cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);   // `all` is pageable and local
+    if (e != cudaSuccess) { cudaFree(p->d_items); delete p; return cuda_fail(e, "upload items"); }
+  }
+  *out = p;
+  return SK_OK;
+}
+
+int validate_rows_sync(const int32_t* rowidx, int64_t nnz, int64_t m, cudaStream_t stream) {
+  if (nnz == 0) return SK_OK;
+  int* flag = nullptr;
+  SK_CUDA(cudaMallocAsync(&flag, sizeof(int), stream));
+  int h = 0;
+  cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(int), stream);
+  if (e == cudaSuccess) e = sk::launch_validate_rows(rowidx, nnz, m, flag, stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, stream);
+  cudaFreeAsync(flag, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) return cuda_fail(e, "validate rows");
+  return h ? SK_ECSC : SK_OK;
+}
+
+int apply_items(const sk_plan_s* p, uint64_t seed, sk_dist_t dist, const void* vals, void* out,
+                cudaStream_t stream) {
+  sk::ApplyArgs a;
+  a.colptr = p->colptr;
+  a.rowidx = p->rowidx;
+  a.vals = vals;
+  a.out = out;
+  a.items = dist == SK_RADEMACHER ? p->d_items : p->d_items + p->n_rad;
+  a.n_items = dist == SK_RADEMACHER ? p->n_rad : p->n_pair;
+  a.d = p->d;
+  a.ld = p->d;
+  a.row_offset = p->row_offset;
+  a.keys = sk::make_keys(seed);
+  cudaError_t e = sk::launch_apply((int)dist, (int)p->dtype, a, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "launch apply");
+  return SK_OK;
+}
+
+struct PoolInit {
+  PoolInit() {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
+};
+
+void ensure_pool() {
+  thread_local bool done = false;
+  if (!done) { PoolInit p; (void)p; done = true; }
+}
+
+}  // namespace
+
+extern "C" {
+
+int sketch_plan(sk_plan_t* plan, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
+                int64_t row_offset, const int64_t* colptr, const int32_t* rowidx, int64_t nnz,
+                sk_stream_t stream_) {
+  if (!plan) return SK_EINVAL;
+  *plan = nullptr;
+  int rc = check_dims(dtype, d, m, n, row_offset);
+  if (rc) return rc;
+  if (nnz < 0 || !colptr || (nnz > 0 && !rowidx)) return SK_EINVAL;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  std::vector<int64_t> h((size_t)n + 1);
+  SK_CUDA(cudaMemcpyAsync(h.data(), colptr, (size_t)(n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
+  SK_CUDA(cudaStreamSynchronize(stream));
+  rc = validate_colptr(h.data(), n, nnz, true);
+  if (rc) return rc;
+  rc = validate_rows_sync(rowidx, nnz, m, stream);
+  if (rc) return rc;
+  return make_plan(plan, dtype, d, m, n, row_offset, h.data(), colptr, rowidx, nnz, stream);
+}
+
+int sketch_plan_host(sk_plan_t* plan, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
+                     int64_t row_offset, const int64_t* h_colptr, const int32_t* rowidx,
+                     int64_t nnz, int validate_rows, sk_stream_t stream_) {
+  if (!plan) return SK_EINVAL;
+  *plan = nullptr;
+  int rc = check_dims(dtype, d, m, n, row_offset);
+  if (rc) return rc;
+  if (nnz < 0 || !h_colptr || (nnz > 0 && !rowidx)) return SK_EINVAL;
+  rc = validate_colptr(h_colptr, n, nnz, true);
+  if (rc) return rc;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (validate_rows) {
+    rc = validate_rows_sync(rowidx, nnz, m, stream);
+    if (rc) return rc;
+  }
+  int64_t* dc = nullptr;
+  SK_CUDA(cudaMalloc(&dc, (size_t)(n + 1) * sizeof(int64_t)));
+  cudaError_t e = cudaMemcpyAsync(dc, h_colptr, (size_t)(n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, stream);
+  if (e != cudaSuccess) { cudaFree(dc); return cuda_fail(e, "upload colptr"); }
+  rc = make_plan(plan, dtype, d, m, n, row_offset, h_colptr, dc, rowidx, nnz, stream);
+  if (rc) { cudaFree(dc); return rc; }
+  (*plan)->owned_colptr = dc;
+  return SK_OK;
+}
+
+int sketch_apply(sk_plan_t plan, uint64_t seed, sk_dist_t dist, const void* vals, void* out,
+                 sk_stream_t stream) {
+  if (!plan || !valid_dist(dist) || !out) return SK_EINVAL;
+  if (plan->nnz > 0 && !vals) return SK_EINVAL;
+  if (plan->n == 0) return SK_OK;
+  return apply_items(plan, seed, dist, vals, out, (cudaStream_t)stream);
+}
+
+int sketch_apply_csc(uint64_t seed, sk_dist_t dist, sk_dtype_t dtype, int64_t d, int64_t m,
+                     int64_t n, int64_t row_offset, const int64_t* colptr, const int32_t* rowidx,
+                     int64_t nnz, const void* vals, void* out, sk_stream_t stream) {
+  if (!valid_dist(dist)) return SK_EINVAL;
+  sk_plan_t p = nullptr;
+  int rc = sketch_plan(&p, dtype, d, m, n, row_offset, colptr, rowidx, nnz, stream);
+  if (rc) return rc;
+  rc = sketch_apply(p, seed, dist, vals, out, stream);
+  cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+  int rc2 = sketch_plan_destroy(p);
+  if (rc) return rc;
+  if (e != cudaSuccess) return cuda_fail(e, "sketch_apply_csc sync");
+  return rc2;
+}
+
+int sketch_apply_host(uint64_t seed, sk_dist_t dist, sk_dtype_t dtype, int64_t d, int64_t m,
+                      int64_t n, int64_t row_offset, const int64_t* h_colptr,
+                      const int32_t* h_rowidx, const void* h_vals, void* h_out,
+                      int pipeline_chunks, sk_stream_t stream_) {
+  if (!valid_dist(dist)) return SK_EINVAL;
+  int rc = check_dims(dtype, d, m, n, row_offset);
+  if (rc) return rc;
+  if (!h_colptr || !h_out) return SK_EINVAL;
+  const int64_t nnz = h_colptr[n];
+  if (nnz > 0 && (!h_rowidx || !h_vals)) return SK_EINVAL;
+  rc = validate_colptr(h_colptr, n, nnz, true);
+  if (rc) return rc;
+  ensure_pool();
+  cudaStream_t stream = (cudaStream_t)stream_;
+  const size_t w = dtype_bytes(dtype);
+
+  // Column groups with balanced nnz; group g+1's upload overlaps group g's kernels.
+  int G = pipeline_chunks > 0 ? pipeline_chunks : (int)std::min<int64_t>(8, std::max<int64_t>(1, nnz / (1 << 21)));
+  G = (int)std::max<int64_t>(1, std::min<int64_t>(G, n));
+  std::vector<int64_t> cb((size_t)G + 1, 0);
+  {
+    int64_t k = 0;
+    for (int g = 1; g < G; ++g) {
+      const int64_t target = (nnz * g) / G;
+      while (k < n && h_colptr[k] < target) ++k;
+      cb[g] = std::max(cb[g - 1], k);
+    }
+    cb[G] = n;
+  }
+
+  // Schedules for every group, uploaded once.
+  std::vector<Item> all;
+  std::vector<int64_t> item_off((size_t)G + 1, 0);
+  const bool rad = dist == SK_RADEMACHER;
+  for (int g = 0; g < G; ++g) {
+    Schedule s = rad ? build_schedule(h_colptr + cb[g], cb[g + 1] - cb[g], d, sk::kRowsPerWarpRad, 8)
+                     : build_schedule(h_colptr + cb[g], cb[g + 1] - cb[g], d, sk::kRowsPerWarpPair, 256);
+    item_off[g] = (int64_t)all.size();
+    all.insert(all.end(), s.items.begin(), s.items.end());
+  }
+  item_off[G] = (int64_t)all.size();
+
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  std::vector<cudaEvent_t> ev_in(G), ev_done(G);
+  cudaEvent_t ev_start = nullptr, ev_end = nullptr;
+  int64_t* d_colptr = nullptr;
+  int32_t* d_rowidx = nullptr;
+  void* d_vals = nullptr;
+  void* d_out = nullptr;
+  Item* d_items = nullptr;
+  int* d_flag = nullptr;
+  int h_flag = 0;
+  cudaError_t e = cudaSuccess;
+  const char* what = "";
+#define SK_STEP(call) do { if (e == cudaSuccess) { e = (call); if (e != cudaSuccess) what = #call; } } while (0)
+  SK_STEP(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
+  SK_STEP(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
+  SK_STEP(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
+  SK_STEP(cudaEventCreateWithFlags(&ev_end, cudaEventDisableTiming));
+  for (int g = 0; g < G; ++g) {
+    SK_STEP(cudaEventCreateWithFlags(&ev_in[g], cudaEventDisableTiming));
+    SK_STEP(cudaEventCreateWithFlags(&ev_done[g], cudaEventDisableTiming));
+  }
+  SK_STEP(cudaMallocAsync((void**)&d_colptr, (size_t)(n + 1) * 8, stream));
+  SK_STEP(cudaMallocAsync((void**)&d_rowidx, (size_t)std::max<int64_t>(nnz, 1) * 4, stream));
+  SK_STEP(cudaMallocAsync(&d_vals, (size_t)std::max<int64_t>(nnz, 1) * w, stream));
+  SK_STEP(cudaMallocAsync(&d_out, (size_t)std::max<int64_t>(d * n, 1) * w, stream));
+  SK_STEP(cudaMallocAsync((void**)&d_items, std::max<size_t>(all.size(), 1) * sizeof(Item), stream));
+  SK_STEP(cudaMallocAsync((void**)&d_flag, sizeof(int), stream));
+  SK_STEP(cudaMemsetAsync(d_flag, 0, sizeof(int), stream));
+  if (!all.empty()) SK_STEP(cudaMemcpyAsync(d_items, all.data(), all.size() * sizeof(Item), cudaMemcpyHostToDevice, stream));
+  SK_STEP(cudaEventRecord(ev_start, stream));
+  SK_STEP(cudaStreamWaitEvent(h2d, ev_start, 0));
+  SK_STEP(cudaMemcpyAsync(d_colptr, h_colptr, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, h2d));
+  for (int g = 0; g < G; ++g) {
+    const int64_t p0 = h_colptr[cb[g]], p1 = h_colptr[cb[g + 1]];
+    if (p1 > p0) {
+      SK_STEP(cudaMemcpyAsync(d_rowidx + p0, h_rowidx + p0, (size_t)(p1 - p0) * 4, cudaMemcpyHostToDevice, h2d));
+      SK_STEP(cudaMemcpyAsync((char*)d_vals + p0 * w, (const char*)h_vals + p0 * w, (size_t)(p1 - p0) * w,
+                              cudaMemcpyHostToDevice, h2d));
+    }
+    SK_STEP(cudaEventRecord(ev_in[g], h2d));
+  }
+  const sk::PhiloxKeys keys = sk::make_keys(seed);
+  for (int g = 0; g < G; ++g) {
+    const int64_t c0 = cb[g], c1 = cb[g + 1];
+    const int64_t p0 = h_colptr[c0], p1 = h_colptr[c1];
+    SK_STEP(cudaStreamWaitEvent(stream, ev_in[g], 0));
+    if (p1 > p0 && e == cudaSuccess) e = sk::launch_validate_rows(d_rowidx + p0, p1 - p0, m, d_flag, stream);
+    sk::ApplyArgs a;
+    a.colptr = d_colptr + c0;
+    a.rowidx = d_rowidx;
+    a.vals = d_vals;
+    a.out = (char*)d_out + (size_t)(c0 * d) * w;
+    a.items = d_items + item_off[g];
+    a.n_items = item_off[g + 1] - item_off[g];
+    a.d = d;
+    a.ld = d;
+    a.row_offset = row_offset;
+    a.keys = keys;
+    if (e == cudaSuccess) { e = sk::launch_apply((int)dist, (int)dtype, a, stream); if (e) what = "launch apply"; }
+    SK_STEP(cudaEventRecord(ev_done[g], stream));
+    SK_STEP(cudaStreamWaitEvent(d2h, ev_done[g], 0));
+    if (c1 > c0)
+      SK_STEP(cudaMemcpyAsync((char*)h_out + (size_t)(c0 * d) * w, (char*)d_out + (size_t)(c0 * d) * w,
+                              (size_t)((c1 - c0) * d) * w, cudaMemcpyDeviceToHost, d2h));
+  }
+  SK_STEP(cudaEventRecord(ev_end, d2h));
+  SK_STEP(cudaStreamWaitEvent(stream, ev_end, 0));
+  SK_STEP(cudaMemcpyAsync(&h_flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  if (d_colptr) cudaFreeAsync(d_colptr, stream);
+  if (d_rowidx) cudaFreeAsync(d_rowidx, stream);
+  if (d_vals) cudaFreeAsync(d_vals, stream);
+  if (d_out) cudaFreeAsync(d_out, stream);
+  if (d_items) cudaFreeAsync(d_items, stream);
+  if (d_flag) cudaFreeAsync(d_flag, stream);
+  cudaError_t es = cudaStreamSynchronize(stream);
+  if (e == cudaSuccess && es != cudaSuccess) { e = es; what = "cudaStreamSynchronize"; }
+  for (int g = 0; g < G; ++g) {
+    if (ev_in[g]) cudaEventDestroy(ev_in[g]);
+    if (ev_done[g]) cudaEventDestroy(ev_done[g]);
+  }
+  if (ev_start) cudaEventDestroy(ev_start);
+  if (ev_end) cudaEventDestroy(ev_end);
+  if (h2d) cudaStreamDestroy(h2d);
+  if (d2h) cudaStreamDestroy(d2h);
+#undef SK_STEP
+  if (e != cudaSuccess) return cuda_fail(e, what);
+  return h_flag ? SK_ECSC : SK_OK;
+}
+
+int sketch_fill_s(uint64_t seed, sk_dist_t dist, sk_dtype_t dtype, int64_t i0, int64_t i1,
+                  int64_t j0, int64_t j1, void* out, int64_t ld, sk_stream_t stream) {
+  if (!valid_dist(dist) || !valid_dtype(dtype)) return SK_EINVAL;
+  if (i0 < 0 || i1 < i0 || j0 < 0 || j1 < j0 || i1 > kMaxD || ld < (i1 - i0)) return SK_EINVAL;
+  if ((i1 > i0 && j1 > j0) && !out) return SK_EINVAL;
+  cudaError_t e = sk::launch_fill_s((int)dist, (int)dtype, seed, i0, i1, j0, j1, out, ld, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "launch fill_s");
+  return SK_OK;
+}
+
+int sketch_plan_stats(sk_plan_t plan, sk_stats_t* h) {
+  if (!plan || !h) return SK_EINVAL;
+  h->d = plan->d; h->m = plan->m; h->n = plan->n; h->nnz = plan->nnz;
+  h->row_offset = plan->row_offset;
+  h->max_col_nnz = plan->max_col;
+  h->n_items_rad = plan->n_rad;
+  h->n_items_pair = plan->n_pair;
+  h->philox_blocks_rad = plan->philox_rad;
+  h->philox_blocks_pair = plan->philox_pair;
+  h->plan_bytes = (plan->n_rad + plan->n_pair) * (int64_t)sizeof(Item) +
+                  (plan->owned_colptr ? (plan->n + 1) * 8 : 0);
+  return SK_OK;
+}
+
+int sketch_plan_destroy(sk_plan_t plan) {
+  if (!plan) return SK_OK;
+  cudaError_t e = cudaSuccess;
+  if (plan->d_items) e = cudaFree(plan->d_items);
+  if (plan->owned_colptr) { cudaError_t e2 = cudaFree(plan->owned_colptr); if (e == cudaSuccess) e = e2; }
+  delete plan;
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFree(plan)");
+  return SK_OK;
+}
+
+const char* sketch_error_string(int code) {
+  switch (code) {
+    case SK_OK: return "ok";
+    case SK_EINVAL: return "invalid argument";
+    case SK_ECSC: return "CSC validation failed";
+    case SK_ENOMEM: return "out of memory";
+    case SK_ECUDA: return "CUDA error";
+    case SK_EUNSUPPORTED: return "unsupported";
+    default: return "unknown status";
+  }
+}
+
+const char* sketch_last_error_detail(void) { return g_detail.c_str(); }
+
+const char* sketch_version(void) { return "libsketch 0.1.0 sm_100a"; }
+
+}  // extern "C"

@@ -259,9 +259,9 @@ int sketch_plan_host(sk_plan_t* plan, sk_dtype_t dtype, int64_t d, int64_t m, in
 
 int sketch_apply(sk_plan_t plan, uint64_t seed, sk_dist_t dist, const void* vals, void* out,
                  sk_stream_t stream) {
-  if (!plan || !valid_dist(dist) || !out) return SK_EINVAL;
-  if (plan->nnz > 0 && !vals) return SK_EINVAL;
-  if (plan->n == 0) return SK_OK;
+  if (!plan || !valid_dist(dist)) return SK_EINVAL;
+  if (plan->n == 0) return SK_OK;                  // nothing to write
+  if (!out || (plan->nnz > 0 && !vals)) return SK_EINVAL;
   return apply_items(plan, seed, dist, vals, out, (cudaStream_t)stream);
 }
 

@@ -15,6 +15,7 @@
 // No tensor cores: per column this is a matrix-vector product with a freshly generated
 // matrix, not a dense contraction.
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "kernels.h"
@@ -42,17 +43,31 @@ __device__ __forceinline__ T ldg_val(const void* vals, int64_t p) {
 //         2-word FSEL per element.
 //  fp32:  the "T - 2P" form Â = Σ a - 2 Σ_{bit=1} a: one predicated FADD per element
 //         (acc holds P; the lane-uniform column total T is kept separately).
+template <int SELMODE>
 __device__ __forceinline__ void apply_signs(double (&acc)[32], uint32_t w, double a) {
-  const int lo = __double2loint(a), hi = __double2hiint(a), nhi = hi ^ (int)0x80000000;
+  if constexpr (SELMODE == 0) {
+    // high word of ±a selected per element (SEL, predicate from R2P), shared low word, DADD
+    const int lo = __double2loint(a), hi = __double2hiint(a), nhi = hi ^ (int)0x80000000;
 #pragma unroll
-  for (int b = 0; b < 32; ++b) {
-    int h;
-    asm("{.reg .pred p; .reg .b32 t; and.b32 t, %1, %4; setp.ne.u32 p, t, 0; selp.b32 %0, %2, %3, p;}"
-        : "=r"(h) : "r"(w), "r"(nhi), "r"(hi), "r"(1u << b));
-    acc[b] += __hiloint2double(h, lo);
+    for (int b = 0; b < 32; ++b) {
+      int h;
+      asm("{.reg .pred p; .reg .b32 t; and.b32 t, %1, %4; setp.ne.u32 p, t, 0; selp.b32 %0, %2, %3, p;}"
+          : "=r"(h) : "r"(w), "r"(nhi), "r"(hi), "r"(1u << b));
+      acc[b] += __hiloint2double(h, lo);
+    }
+  } else {
+    // ±1.0 as the register pair (0, h), h = 0xBFF00000 / 0x3FF00000, then one DFMA
+#pragma unroll
+    for (int b = 0; b < 32; ++b) {
+      int h;
+      asm("{.reg .pred p; .reg .b32 t; and.b32 t, %1, %2; setp.ne.u32 p, t, 0; selp.b32 %0, -1074790400, 1072693248, p;}"
+          : "=r"(h) : "r"(w), "r"(1u << b));
+      acc[b] = fma(__hiloint2double(h, 0), a, acc[b]);
+    }
   }
 }
 
+template <int SELMODE>
 __device__ __forceinline__ void apply_signs(float (&acc)[32], uint32_t w, float a) {
 #pragma unroll
   for (int b = 0; b < 32; ++b)
@@ -72,7 +87,7 @@ __device__ __forceinline__ T finish_sign_sum(T acc, T total) {
 // every nonzero, so they split the RNG work: for a group of 4 nonzeros, lane t of the quad
 // generates block q of nonzero 4u + t, and a 4x4 word transpose through shared memory hands
 // every lane its own word of all four blocks.  One Philox call per 128 (row, nonzero) pairs.
-template <typename T>
+template <typename T, int SELMODE>
 __global__ void __launch_bounds__(kThreads, 1) sk_rad_kernel(const ApplyArgs P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const Item it = P.items[blockIdx.x];
@@ -119,7 +134,7 @@ __global__ void __launch_bounds__(kThreads, 1) sk_rad_kernel(const ApplyArgs P) 
       for (int s = 0; s < 4; ++s) {
         const T a = __shfl_sync(kFull, al, 4 * u + s);   // 0 past cnt: adds ±0
         total += a;
-        apply_signs(acc, w[s], a);
+        apply_signs<SELMODE>(acc, w[s], a);
       }
     }
   }
@@ -280,8 +295,15 @@ cudaError_t launch_apply(int dist, int dtype, const ApplyArgs& a, cudaStream_t s
   const size_t rad32 = kXchBytes + (size_t)kWarps * 32 * kRadPad * 4;
   const size_t pair64 = (size_t)kWarps * 32 * kPairPad * 8;
   const size_t pair32 = (size_t)kWarps * 32 * kPairPad * 4;
-  if (dist == 0) return dtype == 0 ? launch_items(sk_rad_kernel<double>, rad64, a, stream)
-                                   : launch_items(sk_rad_kernel<float>, rad32, a, stream);
+  if (dist == 0) {
+    if (dtype == 1) return launch_items(sk_rad_kernel<float, 0>, rad32, a, stream);
+    static const int selmode = [] {
+      const char* v = getenv("SKETCH_RAD_SELMODE");   // tuning knob only; results identical
+      return v ? atoi(v) : 0;
+    }();
+    if (selmode == 1) return launch_items(sk_rad_kernel<double, 1>, rad64, a, stream);
+    return launch_items(sk_rad_kernel<double, 0>, rad64, a, stream);
+  }
   if (dist == 1) return dtype == 0 ? launch_items(sk_pair_kernel<1, double>, pair64, a, stream)
                                    : launch_items(sk_pair_kernel<1, float>, pair32, a, stream);
   return dtype == 0 ? launch_items(sk_pair_kernel<2, double>, pair64, a, stream)

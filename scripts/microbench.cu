@@ -36,6 +36,31 @@ __global__ void philox_kernel(uint32_t* out, int iters, sk::PhiloxKeys K) {
   if (f == 0x12345678u) out[0] = f;
 }
 
+// IMAD.WIDE.U32 vs (IMAD.HI.U32 + IMAD.LO) for the 32x32->64 products of a Philox round.
+template <int MODE>
+__global__ void mul_kernel(uint32_t* out, int iters, uint32_t m) {
+  uint32_t a[8], f = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = threadIdx.x * 7919u + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if constexpr (MODE == 0) {
+        const uint64_t p = (uint64_t)m * a[i];
+        a[i] = (uint32_t)(p >> 32) ^ (uint32_t)p;
+      } else {
+        uint32_t hi, lo;
+        asm volatile("mul.hi.u32 %0, %1, %2;" : "=r"(hi) : "r"(m), "r"(a[i]));
+        asm volatile("mul.lo.u32 %0, %1, %2;" : "=r"(lo) : "r"(m), "r"(a[i]));
+        a[i] = hi ^ lo;
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) f ^= a[i];
+  if (f == 0x12345678u) out[0] = f;
+}
+
 int main() {
   cudaDeviceProp p;
   cudaGetDeviceProperties(&p, 0);
@@ -62,6 +87,10 @@ int main() {
   const int piters = 4000;
   timeit([&] { philox_kernel<<<blocks, threads>>>((uint32_t*)buf, piters, sk::make_keys(7)); },
          (double)blocks * threads * piters, "philox_blocks_per_s");
+  timeit([&] { mul_kernel<0><<<blocks, threads>>>((uint32_t*)buf, 20000, 0xD2511F53u); },
+         (double)blocks * threads * 8 * 20000, "mulwide_per_s");
+  timeit([&] { mul_kernel<1><<<blocks, threads>>>((uint32_t*)buf, 20000, 0xD2511F53u); },
+         (double)blocks * threads * 8 * 20000, "mulhi_lo_per_s");
   printf("}\n");
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) { fprintf(stderr, "%s\n", cudaGetErrorString(e)); return 1; }

@@ -39,6 +39,20 @@ struct ApplyArgs {
   PhiloxKeys keys;
 };
 
+// Work item of the tensor-core ±1 kernel: column `col`, 128-row tiles [tile0, tile0 + ntiles).
+struct TcItem {
+  int32_t col;
+  int32_t tile0;
+  int32_t ntiles;
+  int32_t pad;
+};
+
+// Longest column the tensor-core path accepts (int32 accumulation bound, sketch_tc.cu).
+constexpr int64_t kTcMaxColumn = 131071;
+
+cudaError_t launch_apply_rad_tc(const ApplyArgs& a, const TcItem* items, int64_t n_items, cudaStream_t stream);
+int tc_tiles_per_cta();
+
 // dist: 0 = Rademacher, 1 = uniform, 2 = Gaussian; dtype: 0 = f64, 1 = f32.
 cudaError_t launch_apply(int dist, int dtype, const ApplyArgs& a, cudaStream_t stream);
 

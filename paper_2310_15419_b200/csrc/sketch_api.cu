@@ -8,6 +8,7 @@
 // handed to CTAs -- the parallelised outer loops of PAPER.md:327-332.
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -102,6 +103,38 @@ Schedule build_schedule(const int64_t* colptr, int64_t n, int64_t d, int rows_pe
   return S;
 }
 
+// Tensor-core schedule: per column, ceil(d/128) row tiles in groups of <= 16 per CTA,
+// longest columns first.
+std::vector<sk::TcItem> build_tc_schedule(const int64_t* colptr, int64_t n, int64_t d) {
+  const int64_t tiles = (d + 127) / 128;
+  const int64_t per = sk::tc_tiles_per_cta();
+  const int64_t groups = (tiles + per - 1) / per;
+  const int64_t tpg = (tiles + groups - 1) / groups;
+  std::vector<std::pair<int64_t, sk::TcItem>> tmp;
+  for (int64_t k = 0; k < n; ++k) {
+    const int64_t L = colptr[k + 1] - colptr[k];
+    for (int64_t g = 0; g * tpg < tiles; ++g) {
+      sk::TcItem it;
+      it.col = (int32_t)k;
+      it.tile0 = (int32_t)(g * tpg);
+      it.ntiles = (int32_t)std::min(tpg, tiles - g * tpg);
+      it.pad = 0;
+      tmp.emplace_back(L, it);
+    }
+  }
+  std::stable_sort(tmp.begin(), tmp.end(), [](const std::pair<int64_t, sk::TcItem>& a,
+                                              const std::pair<int64_t, sk::TcItem>& b) { return a.first > b.first; });
+  std::vector<sk::TcItem> out;
+  out.reserve(tmp.size());
+  for (auto& pr : tmp) out.push_back(pr.second);
+  return out;
+}
+
+bool tc_disabled() {
+  static const bool off = [] { const char* v = getenv("SKETCH_DISABLE_TC"); return v && v[0] == '1'; }();
+  return off;
+}
+
 }  // namespace
 
 struct sk_plan_s {
@@ -110,6 +143,8 @@ struct sk_plan_s {
   const int64_t* colptr;   // device (caller-owned)
   const int32_t* rowidx;   // device (caller-owned)
   Item* d_items = nullptr; // [rad items | pair items]
+  sk::TcItem* d_tc = nullptr;       // tensor-core ±1 fp64 schedule (empty if not eligible)
+  int64_t n_tc = 0;
   int64_t* owned_colptr = nullptr;  // device copy made by sketch_plan_host
   int64_t n_rad = 0, n_pair = 0;
   int64_t philox_rad = 0, philox_pair = 0;
@@ -147,6 +182,14 @@ int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
   p->n_pair = (int64_t)pair.items.size();
   p->philox_rad = rad.philox_blocks;
   p->philox_pair = pair.philox_blocks;
+  if (dtype == SK_F64 && p->max_col <= sk::kTcMaxColumn && n > 0) {
+    std::vector<sk::TcItem> tc = build_tc_schedule(h_colptr, n, d);
+    p->n_tc = (int64_t)tc.size();
+    cudaError_t e = cudaMalloc(&p->d_tc, tc.size() * sizeof(sk::TcItem));
+    if (e == cudaSuccess) e = cudaMemcpyAsync(p->d_tc, tc.data(), tc.size() * sizeof(sk::TcItem), cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    if (e != cudaSuccess) { if (p->d_tc) cudaFree(p->d_tc); delete p; return cuda_fail(e, "tc schedule"); }
+  }
   const int64_t total = p->n_rad + p->n_pair;
   if (total > 0) {
     cudaError_t e = cudaMalloc(&p->d_items, (size_t)total * sizeof(Item));
@@ -188,7 +231,11 @@ int apply_items(const sk_plan_s* p, uint64_t seed, sk_dist_t dist, const void* v
   a.ld = p->d;
   a.row_offset = p->row_offset;
   a.keys = sk::make_keys(seed);
-  cudaError_t e = sk::launch_apply((int)dist, (int)p->dtype, a, stream);
+  cudaError_t e;
+  if (dist == SK_RADEMACHER && p->n_tc > 0 && !tc_disabled())
+    e = sk::launch_apply_rad_tc(a, p->d_tc, p->n_tc, stream);
+  else
+    e = sk::launch_apply((int)dist, (int)p->dtype, a, stream);
   if (e != cudaSuccess) return cuda_fail(e, "launch apply");
   return SK_OK;
 }
@@ -440,6 +487,7 @@ int sketch_plan_destroy(sk_plan_t plan) {
   cudaError_t e = cudaSuccess;
   if (plan->d_items) e = cudaFree(plan->d_items);
   if (plan->owned_colptr) { cudaError_t e2 = cudaFree(plan->owned_colptr); if (e == cudaSuccess) e = e2; }
+  if (plan->d_tc) { cudaError_t e2 = cudaFree(plan->d_tc); if (e == cudaSuccess) e = e2; }
   delete plan;
   if (e != cudaSuccess) return cuda_fail(e, "cudaFree(plan)");
   return SK_OK;

@@ -50,8 +50,12 @@ struct TcItem {
 // Longest column the tensor-core path accepts (int32 accumulation bound, sketch_tc.cu).
 constexpr int64_t kTcMaxColumn = 131071;
 
-cudaError_t launch_apply_rad_tc(const ApplyArgs& a, const TcItem* items, int64_t n_items, cudaStream_t stream);
+// smem_staged = 1: S tiles staged in shared memory (variant 1); 0: staged in TMEM (variant 2).
+cudaError_t launch_apply_rad_tc(const ApplyArgs& a, const TcItem* items, int64_t n_items, int smem_staged,
+                                cudaStream_t stream);
 int tc_tiles_per_cta();
+cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const TcItem* items, int64_t n_items, cudaStream_t stream);
+int f4_tiles_per_cta();
 
 // dist: 0 = Rademacher, 1 = uniform, 2 = Gaussian; dtype: 0 = f64, 1 = f32.
 cudaError_t launch_apply(int dist, int dtype, const ApplyArgs& a, cudaStream_t stream);

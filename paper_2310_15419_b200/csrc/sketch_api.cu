@@ -7,6 +7,7 @@
 // (column, Â-row tile) work items of Algorithm 1's outer loops are
 // handed to CTAs -- the parallelised outer loops of PAPER.md:327-332.
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cstdlib>
 #include <cstdio>
@@ -105,9 +106,8 @@ Schedule build_schedule(const int64_t* colptr, int64_t n, int64_t d, int rows_pe
 
 // Tensor-core schedule: per column, ceil(d/128) row tiles in groups of <= 16 per CTA,
 // longest columns first.
-std::vector<sk::TcItem> build_tc_schedule(const int64_t* colptr, int64_t n, int64_t d) {
+std::vector<sk::TcItem> build_tc_schedule(const int64_t* colptr, int64_t n, int64_t d, int64_t per) {
   const int64_t tiles = (d + 127) / 128;
-  const int64_t per = sk::tc_tiles_per_cta();
   const int64_t groups = (tiles + per - 1) / per;
   const int64_t tpg = (tiles + groups - 1) / groups;
   std::vector<std::pair<int64_t, sk::TcItem>> tmp;
@@ -130,10 +130,25 @@ std::vector<sk::TcItem> build_tc_schedule(const int64_t* colptr, int64_t n, int6
   return out;
 }
 
-bool tc_disabled() {
-  static const bool off = [] { const char* v = getenv("SKETCH_DISABLE_TC"); return v && v[0] == '1'; }();
-  return off;
+// Kernel used for ±1 with fp64 values (process-wide; results agree within the parity bound):
+// SK_PATH_TC_FP4 (default), SK_PATH_TC_INT8_SMEM, SK_PATH_TC_INT8_TMEM, SK_PATH_SIMT.
+// Initialised from SKETCH_RAD_F64_PATH = fp4 | int8smem | int8tmem | simt, else fp4.
+std::atomic<int> g_rad_f64_path{-1};
+
+int rad_f64_path() {
+  int v = g_rad_f64_path.load(std::memory_order_relaxed);
+  if (v >= 0) return v;
+  v = SK_PATH_TC_FP4;
+  if (const char* e = getenv("SKETCH_RAD_F64_PATH")) {
+    if (!strcmp(e, "int8smem")) v = SK_PATH_TC_INT8_SMEM;
+    else if (!strcmp(e, "int8tmem")) v = SK_PATH_TC_INT8_TMEM;
+    else if (!strcmp(e, "simt")) v = SK_PATH_SIMT;
+  }
+  g_rad_f64_path.store(v, std::memory_order_relaxed);
+  return v;
 }
+
+const char* kernel_name(const sk_plan_s* p, int dist);
 
 }  // namespace
 
@@ -143,8 +158,9 @@ struct sk_plan_s {
   const int64_t* colptr;   // device (caller-owned)
   const int32_t* rowidx;   // device (caller-owned)
   Item* d_items = nullptr; // [rad items | pair items]
-  sk::TcItem* d_tc = nullptr;       // tensor-core ±1 fp64 schedule (empty if not eligible)
-  int64_t n_tc = 0;
+  sk::TcItem* d_tc = nullptr;       // tensor-core ±1 fp64 schedules (empty if not eligible):
+  int64_t n_tc = 0;                 //   [int8 items (16 tiles) | fp4 items (6 tiles)]
+  int64_t n_f4 = 0;
   int64_t* owned_colptr = nullptr;  // device copy made by sketch_plan_host
   int64_t n_rad = 0, n_pair = 0;
   int64_t philox_rad = 0, philox_pair = 0;
@@ -183,8 +199,11 @@ int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
   p->philox_rad = rad.philox_blocks;
   p->philox_pair = pair.philox_blocks;
   if (dtype == SK_F64 && p->max_col <= sk::kTcMaxColumn && n > 0) {
-    std::vector<sk::TcItem> tc = build_tc_schedule(h_colptr, n, d);
+    std::vector<sk::TcItem> tc = build_tc_schedule(h_colptr, n, d, sk::tc_tiles_per_cta());
+    std::vector<sk::TcItem> f4 = build_tc_schedule(h_colptr, n, d, sk::f4_tiles_per_cta());
     p->n_tc = (int64_t)tc.size();
+    p->n_f4 = (int64_t)f4.size();
+    tc.insert(tc.end(), f4.begin(), f4.end());
     cudaError_t e = cudaMalloc(&p->d_tc, tc.size() * sizeof(sk::TcItem));
     if (e == cudaSuccess) e = cudaMemcpyAsync(p->d_tc, tc.data(), tc.size() * sizeof(sk::TcItem), cudaMemcpyHostToDevice, stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
@@ -232,9 +251,11 @@ int apply_items(const sk_plan_s* p, uint64_t seed, sk_dist_t dist, const void* v
   a.row_offset = p->row_offset;
   a.keys = sk::make_keys(seed);
   cudaError_t e;
-  if (dist == SK_RADEMACHER && p->n_tc > 0 && !tc_disabled())
-    e = sk::launch_apply_rad_tc(a, p->d_tc, p->n_tc, stream);
-  else
+  const int path = rad_f64_path();
+  if (dist == SK_RADEMACHER && p->n_tc > 0 && path != SK_PATH_SIMT) {
+    if (path == SK_PATH_TC_FP4) e = sk::launch_apply_rad_f4(a, p->d_tc + p->n_tc, p->n_f4, stream);
+    else e = sk::launch_apply_rad_tc(a, p->d_tc, p->n_tc, path == SK_PATH_TC_INT8_SMEM ? 1 : 0, stream);
+  } else
     e = sk::launch_apply((int)dist, (int)p->dtype, a, stream);
   if (e != cudaSuccess) return cuda_fail(e, "launch apply");
   return SK_OK;
@@ -254,6 +275,25 @@ struct PoolInit {
 void ensure_pool() {
   thread_local bool done = false;
   if (!done) { PoolInit p; (void)p; done = true; }
+}
+
+
+const char* kernel_name(const sk_plan_s* p, int dist) {
+  if (dist == SK_RADEMACHER) {
+    if (p->dtype == SK_F32) return "sk_rad_kernel<float>";
+    if (p->n_tc > 0) {
+      switch (rad_f64_path()) {
+        case SK_PATH_TC_FP4: return "sk_rad_f4_kernel (tcgen05 kind::mxf4)";
+        case SK_PATH_TC_INT8_SMEM: return "sk_rad_tc_kernel (tcgen05 kind::i8, S in smem)";
+        case SK_PATH_TC_INT8_TMEM: return "sk_rad_tm_kernel (tcgen05 kind::i8, S in TMEM)";
+        default: break;
+      }
+    }
+    return "sk_rad_kernel<double>";
+  }
+  const bool f64 = p->dtype == SK_F64;
+  if (dist == SK_UNIFORM) return f64 ? "sk_pair_kernel<uniform, double>" : "sk_pair_kernel<uniform, float>";
+  return f64 ? "sk_pair_kernel<gaussian, double>" : "sk_pair_kernel<gaussian, float>";
 }
 
 }  // namespace
@@ -357,18 +397,6 @@ int sketch_apply_host(uint64_t seed, sk_dist_t dist, sk_dtype_t dtype, int64_t d
     cb[G] = n;
   }
 
-  // Schedules for every group, uploaded once.
-  std::vector<Item> all;
-  std::vector<int64_t> item_off((size_t)G + 1, 0);
-  const bool rad = dist == SK_RADEMACHER;
-  for (int g = 0; g < G; ++g) {
-    Schedule s = rad ? build_schedule(h_colptr + cb[g], cb[g + 1] - cb[g], d, sk::kRowsPerWarpRad, 8)
-                     : build_schedule(h_colptr + cb[g], cb[g + 1] - cb[g], d, sk::kRowsPerWarpPair, 256);
-    item_off[g] = (int64_t)all.size();
-    all.insert(all.end(), s.items.begin(), s.items.end());
-  }
-  item_off[G] = (int64_t)all.size();
-
   cudaStream_t h2d = nullptr, d2h = nullptr;
   std::vector<cudaEvent_t> ev_in(G), ev_done(G);
   cudaEvent_t ev_start = nullptr, ev_end = nullptr;
@@ -376,7 +404,6 @@ int sketch_apply_host(uint64_t seed, sk_dist_t dist, sk_dtype_t dtype, int64_t d
   int32_t* d_rowidx = nullptr;
   void* d_vals = nullptr;
   void* d_out = nullptr;
-  Item* d_items = nullptr;
   int* d_flag = nullptr;
   int h_flag = 0;
   cudaError_t e = cudaSuccess;
@@ -394,10 +421,17 @@ int sketch_apply_host(uint64_t seed, sk_dist_t dist, sk_dtype_t dtype, int64_t d
   SK_STEP(cudaMallocAsync((void**)&d_rowidx, (size_t)std::max<int64_t>(nnz, 1) * 4, stream));
   SK_STEP(cudaMallocAsync(&d_vals, (size_t)std::max<int64_t>(nnz, 1) * w, stream));
   SK_STEP(cudaMallocAsync(&d_out, (size_t)std::max<int64_t>(d * n, 1) * w, stream));
-  SK_STEP(cudaMallocAsync((void**)&d_items, std::max<size_t>(all.size(), 1) * sizeof(Item), stream));
   SK_STEP(cudaMallocAsync((void**)&d_flag, sizeof(int), stream));
   SK_STEP(cudaMemsetAsync(d_flag, 0, sizeof(int), stream));
-  if (!all.empty()) SK_STEP(cudaMemcpyAsync(d_items, all.data(), all.size() * sizeof(Item), cudaMemcpyHostToDevice, stream));
+  // One plan per column group (same kernels and schedules as sketch_apply); built before any
+  // copy is in flight.  Group plans reference d_colptr + c0 (absolute offsets) and d_rowidx.
+  std::vector<sk_plan_t> plans((size_t)G, nullptr);
+  for (int g = 0; g < G && e == cudaSuccess; ++g) {
+    const int64_t c0 = cb[g], c1 = cb[g + 1];
+    const int rcp = make_plan(&plans[g], dtype, d, m, c1 - c0, row_offset, h_colptr + c0, d_colptr + c0,
+                              d_rowidx, h_colptr[c1] - h_colptr[c0], stream);
+    if (rcp != SK_OK) { e = cudaErrorUnknown; what = "make_plan(group)"; }
+  }
   SK_STEP(cudaEventRecord(ev_start, stream));
   SK_STEP(cudaStreamWaitEvent(h2d, ev_start, 0));
   SK_STEP(cudaMemcpyAsync(d_colptr, h_colptr, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, h2d));
@@ -410,24 +444,15 @@ int sketch_apply_host(uint64_t seed, sk_dist_t dist, sk_dtype_t dtype, int64_t d
     }
     SK_STEP(cudaEventRecord(ev_in[g], h2d));
   }
-  const sk::PhiloxKeys keys = sk::make_keys(seed);
   for (int g = 0; g < G; ++g) {
     const int64_t c0 = cb[g], c1 = cb[g + 1];
     const int64_t p0 = h_colptr[c0], p1 = h_colptr[c1];
     SK_STEP(cudaStreamWaitEvent(stream, ev_in[g], 0));
     if (p1 > p0 && e == cudaSuccess) e = sk::launch_validate_rows(d_rowidx + p0, p1 - p0, m, d_flag, stream);
-    sk::ApplyArgs a;
-    a.colptr = d_colptr + c0;
-    a.rowidx = d_rowidx;
-    a.vals = d_vals;
-    a.out = (char*)d_out + (size_t)(c0 * d) * w;
-    a.items = d_items + item_off[g];
-    a.n_items = item_off[g + 1] - item_off[g];
-    a.d = d;
-    a.ld = d;
-    a.row_offset = row_offset;
-    a.keys = keys;
-    if (e == cudaSuccess) { e = sk::launch_apply((int)dist, (int)dtype, a, stream); if (e) what = "launch apply"; }
+    if (e == cudaSuccess && c1 > c0) {
+      const int rca = apply_items(plans[g], seed, dist, d_vals, (char*)d_out + (size_t)(c0 * d) * w, stream);
+      if (rca != SK_OK) { e = cudaErrorLaunchFailure; what = "launch apply"; }
+    }
     SK_STEP(cudaEventRecord(ev_done[g], stream));
     SK_STEP(cudaStreamWaitEvent(d2h, ev_done[g], 0));
     if (c1 > c0)
@@ -441,7 +466,6 @@ int sketch_apply_host(uint64_t seed, sk_dist_t dist, sk_dtype_t dtype, int64_t d
   if (d_rowidx) cudaFreeAsync(d_rowidx, stream);
   if (d_vals) cudaFreeAsync(d_vals, stream);
   if (d_out) cudaFreeAsync(d_out, stream);
-  if (d_items) cudaFreeAsync(d_items, stream);
   if (d_flag) cudaFreeAsync(d_flag, stream);
   cudaError_t es = cudaStreamSynchronize(stream);
   if (e == cudaSuccess && es != cudaSuccess) { e = es; what = "cudaStreamSynchronize"; }
@@ -449,6 +473,7 @@ int sketch_apply_host(uint64_t seed, sk_dist_t dist, sk_dtype_t dtype, int64_t d
     if (ev_in[g]) cudaEventDestroy(ev_in[g]);
     if (ev_done[g]) cudaEventDestroy(ev_done[g]);
   }
+  for (auto pl : plans) sketch_plan_destroy(pl);
   if (ev_start) cudaEventDestroy(ev_start);
   if (ev_end) cudaEventDestroy(ev_end);
   if (h2d) cudaStreamDestroy(h2d);
@@ -507,6 +532,17 @@ const char* sketch_error_string(int code) {
 
 const char* sketch_last_error_detail(void) { return g_detail.c_str(); }
 
-const char* sketch_version(void) { return "libsketch 0.1.0 sm_100a"; }
+const char* sketch_version(void) { return "libsketch 0.2.0 sm_100a"; }
+
+int sketch_set_rad_f64_path(int path) {
+  if (path < SK_PATH_TC_FP4 || path > SK_PATH_SIMT) return SK_EINVAL;
+  g_rad_f64_path.store(path, std::memory_order_relaxed);
+  return SK_OK;
+}
+
+const char* sketch_apply_kernel_name(sk_plan_t plan, sk_dist_t dist) {
+  if (!plan || !valid_dist(dist)) return "";
+  return kernel_name(plan, (int)dist);
+}
 
 }  // extern "C"

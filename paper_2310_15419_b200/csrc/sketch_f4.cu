@@ -1,0 +1,410 @@
+// sketch_f4.cu -- ±1 sketch of fp64 values on the 5th-gen tensor cores with packed fp4 operands
+// (tcgen05.mma kind::mxf4, block-scaled e2m1, f32 accumulation in TMEM), sm_100a.
+//
+// Per column k, Â[:, k] = S[:, J_k] · a_k (Algorithm 3's inner loops) is computed
+// EXACTLY on the tensor cores:
+//  * signs -> fp4.  S[i, p] = ±1 is the e2m1 nibble 0x2 (+1.0) / 0xA (-1.0): the sign bit of the
+//    nibble IS the Philox bit (bit 1 -> -1, include/sketch.h).  Operand A = S tile, M = 128 rows
+//    x K = 64 nonzeros, K-major, packed 2 per byte (0.5 byte per (row, nonzero)).
+//  * values -> binary signed digits.  With E = frexp exponent of max_p |a_p| of the column,
+//    A_p = rint(a_p 2^(61-E)) (|A_p| <= 2^61, rounding is the only approximation: <= 2^-62 L max|a|)
+//    and U_p = A_p + 2^63 (mod 2^64), the digits d_{p,s} = 2 bit_s(U_p) - 1 in {±1} satisfy
+//    Σ_s d_{p,s} 2^s = 2 A_p + 1.  Operand B = 72 x 64 fp4: rows s < 64 hold d_{.,s}, row 64 is all
+//    +1 (gives Σ_p S[i,p]), rows 65..71 are 0.
+//  * D[i, s] = Σ_p S[i,p] d_{p,s} are integers with |D| <= L < 2^24: exact in f32.
+//    Â[i] = 2^(E-62) (Σ_s 2^s D[i,s] - D[i,64]), formed with two exact int64 partial sums.
+//  * both operands are produced by the same path: a Philox4x32-10 block (one nonzero x 128 rows)
+//    or a value's 64-bit U, 32 x 32 bit-transposed across the warp (5 shuffle stages), expanded to
+//    nibbles ((y << (3-c)) & 0x88888888) | 0x22222222 and stored with STS.128 into the canonical
+//    K-major no-swizzle layout (8-row x 16-byte core matrices).  Inside each 32-nonzero K chunk,
+//    word c nibble n holds nonzero 4n + c for both A and B.
+//  * CTA = up to 12 A-producer warps (tile = w % T, nonzero half = w / T) + 2 B-producer warps +
+//    1 MMA warp; 4-stage smem ring (A: T x 4 KB, B: 2.3 KB per stage) with mbarrier full/empty;
+//    block scale factors (ue8m0 = 1.0) live in TMEM columns [448, 512).
+// Measured (scripts/microbench_mxf4.cu): one M=128,K=64 mxf4 MMA reads its 4 KB A tile at
+// ~44.5 B/clk -> ~89 entries/clk/SM, vs ~62 for int8 and 64 lanes/clk/SM for FP64 DFMA.
+#include <cstdint>
+#include <cstdlib>
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+#include "philox.cuh"
+
+namespace sk {
+namespace {
+
+constexpr int kF4Tiles = 6;                       // 128-row tiles per CTA (max)
+constexpr int kF4AWarps = 2 * kF4Tiles;           // A producers: (tile, nonzero half)
+constexpr int kF4BWarps = 2;                      // B producers: nonzero half
+constexpr int kF4Producers = kF4AWarps + kF4BWarps;
+constexpr int kF4LoaderWarp = kF4Producers;       // streams rowidx / vals into a smem ring
+constexpr int kF4MmaWarp = kF4Producers + 1;
+constexpr int kF4Threads = (kF4Producers + 2) * 32;
+constexpr int kF4Slots = 8;                       // nonzero-stream ring (K-steps of 64)
+constexpr int kF4N = 72;                          // 64 digit rows + ones row + 7 zero rows
+constexpr int kF4Stages = 4;
+constexpr int kF4ATile = 128 * 32;                // 128 rows x 64 fp4 = 4 KB
+constexpr int kF4BTile = (kF4N / 8) * 256;        // 9 row groups x 256 B = 2304 B
+constexpr int kF4Stage = kF4Tiles * kF4ATile + 3072;
+constexpr uint32_t kF4SfCol = 448;                // scale factors: TMEM columns [448, 512)
+
+struct F4Shared {
+  uint64_t full[kF4Stages];
+  uint64_t empty[kF4Stages];
+  uint64_t jfull[kF4Slots];
+  uint64_t jempty[kF4Slots];
+  uint64_t done;
+  uint32_t js[kF4Slots][64];
+  double vs[kF4Slots][64];
+  uint32_t tmem_base;
+  unsigned long long maxabs_bits;
+  int32_t E;
+  int32_t nonfinite;
+};
+
+__device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void f4_mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(s_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void f4_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(s_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void f4_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}"
+      :: "r"(s_u32(bar)), "r"(parity) : "memory");
+}
+
+// K-major, no-swizzle smem descriptor: core matrix = 8 rows x 16 B; LBO = stride between the two
+// 16-byte K chunks (128 B), SBO = stride between 8-row groups (256 B); version 1 (sm_100).
+__device__ __forceinline__ uint64_t f4_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)(128u >> 4) << 16;
+  d |= (uint64_t)(256u >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  return d;
+}
+
+// Block-scaled instruction descriptor: A = B = E2M1 (MXF4 format 1), K-major, D = F32,
+// scale format E8M0, M = 128, N = 72, K = 64.
+__host__ __device__ constexpr uint32_t f4_idesc() {
+  return (1u << 7) | (1u << 10) | ((uint32_t)(kF4N >> 3) << 17) | (1u << 23) | ((128u >> 4) << 24);
+}
+
+// One transpose stage on one word: t = rotate(partner word), x = keep ? x : t (bit select).
+__device__ __forceinline__ uint32_t f4_stage(uint32_t x, uint32_t y, uint32_t sh, uint32_t keep) {
+  uint32_t t, r;
+  asm("shf.l.wrap.b32 %0, %1, %1, %2;" : "=r"(t) : "r"(y), "r"(sh));
+  asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(r) : "r"(x), "r"(t), "r"(keep));   // (x & keep) | (t & ~keep)
+  return r;
+}
+
+template <int NW>
+__device__ __forceinline__ void f4_transpose(uint32_t (&x)[NW], int lane) {
+#pragma unroll
+  for (int j = 16; j > 0; j >>= 1) {
+    const uint32_t m = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu : j == 4 ? 0x0F0F0F0Fu
+                     : j == 2 ? 0x33333333u : 0x55555555u;
+    const bool hi = (lane & j) != 0;
+    const uint32_t keep = hi ? ~m : m;
+    const uint32_t sh = hi ? (32 - j) : j;
+    uint32_t y[NW];
+#pragma unroll
+    for (int k = 0; k < NW; ++k) y[k] = __shfl_xor_sync(0xFFFFFFFFu, x[k], j);
+#pragma unroll
+    for (int k = 0; k < NW; ++k) x[k] = f4_stage(x[k], y[k], sh, keep);
+  }
+}
+
+// 32 sign bits (bit l = nonzero l of the chunk; 1 -> -1.0) -> 16 bytes of e2m1 nibbles; word c
+// nibble n holds nonzero 4n + c.
+__device__ __forceinline__ uint32_t f4_valid_mask(int c, int nvalid) {
+  // nibbles n with 4n + c < nvalid
+  const int cnt = nvalid > c ? (nvalid - c + 3) >> 2 : 0;   // number of valid nibbles (0..8)
+  return cnt >= 8 ? 0xFFFFFFFFu : ((1u << (4 * cnt)) - 1u);
+}
+
+__device__ __forceinline__ uint32_t f4_nib(uint32_t t) {   // (t & 0x88888888) | 0x22222222
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(t), "r"(0x88888888u), "r"(0x22222222u));
+  return r;
+}
+
+__device__ __forceinline__ void f4_store_row(uint32_t addr, uint32_t y) {
+  const uint32_t w0 = f4_nib(y << 3), w1 = f4_nib(y << 2), w2 = f4_nib(y << 1), w3 = f4_nib(y);
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" :: "r"(addr), "r"(w0), "r"(w1), "r"(w2), "r"(w3) : "memory");
+}
+
+// B rows: as f4_store_row, with nibbles of nonzeros >= nvalid (padding past the column end)
+// forced to 0.0 so padded K positions contribute nothing whatever the S nibbles are.
+__device__ __forceinline__ void f4_store_row_masked(uint32_t addr, uint32_t y, int nvalid) {
+  uint32_t w0 = f4_nib(y << 3), w1 = f4_nib(y << 2), w2 = f4_nib(y << 1), w3 = f4_nib(y);
+  if (nvalid < 32) {
+    w0 &= f4_valid_mask(0, nvalid);
+    w1 &= f4_valid_mask(1, nvalid);
+    w2 &= f4_valid_mask(2, nvalid);
+    w3 &= f4_valid_mask(3, nvalid);
+  }
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" :: "r"(addr), "r"(w0), "r"(w1), "r"(w2), "r"(w3) : "memory");
+}
+
+// byte offset of row m, K chunk h inside a K-major no-swizzle tile (core matrices 8 x 16 B)
+__device__ __forceinline__ uint32_t f4_off(int m, int h) {
+  return (uint32_t)((m >> 3) * 256 + h * 128 + (m & 7) * 16);
+}
+
+// dbg (tuning only, results invalid when nonzero): 1 = A producers skip generation, 2 = no MMAs,
+// 3 = no proxy fences, 4 = B producers skip their work, 5 = 2 + 4.
+__global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArgs P, const TcItem* items, int dbg) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* stages = smem_raw + ((1024u - (s_u32(smem_raw) & 1023u)) & 1023u);
+  F4Shared& sh = *reinterpret_cast<F4Shared*>(stages + kF4Stages * kF4Stage);
+  const TcItem it = items[blockIdx.x];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t pb = P.colptr[it.col], pe = P.colptr[it.col + 1];
+  const int64_t L = pe - pb;
+  const int nsteps = (int)((L + 63) >> 6);
+  const int T = it.ntiles;                         // <= kF4Tiles
+  const double* vals = reinterpret_cast<const double*>(P.vals);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kF4Stages; ++s) { f4_mbar_init(&sh.full[s], 2 * T + kF4BWarps); f4_mbar_init(&sh.empty[s], 1); }
+    for (int s = 0; s < kF4Slots; ++s) { f4_mbar_init(&sh.jfull[s], 32); f4_mbar_init(&sh.jempty[s], (2 * T + kF4BWarps) * 32); }
+    f4_mbar_init(&sh.done, 1);
+    sh.maxabs_bits = 0ull;
+    sh.nonfinite = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kF4MmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 :: "r"(s_u32(&sh.tmem_base)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  // B rows 64..71 of every stage are constant: row 64 = +1.0 (0x2), rows 65..71 = 0
+  for (int i = threadIdx.x; i < kF4Stages * 8 * 2; i += blockDim.x) {
+    const int s = i / 16, row = 64 + (i % 16) / 2, h = i & 1;
+    const uint32_t v = row == 64 ? 0x22222222u : 0u;
+    const uint32_t a = s_u32(stages + s * kF4Stage + kF4Tiles * kF4ATile) + f4_off(row, h);
+    asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" :: "r"(a), "r"(v) : "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  const uint32_t tmem = sh.tmem_base;
+
+  // scale factors = 1.0 (ue8m0 0x7F) in TMEM columns [448, 512), all 128 lanes
+  if (warp < 4) {
+    const uint32_t taddr = tmem + ((uint32_t)(32 * warp) << 16) + kF4SfCol;
+    const uint32_t v = 0x7F7F7F7Fu;
+#pragma unroll
+    for (int c = 0; c < 64; c += 8)
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1};"
+                   :: "r"(taddr + c), "r"(v) : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  }
+  // column scale E (all producers)
+  if (warp < kF4Producers) {
+    double mx = 0.0;
+    for (int64_t p = pb + threadIdx.x; p < pe; p += kF4Producers * 32) mx = fmax(mx, fabs(__ldg(vals + p)));
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+    if (lane == 0) atomicMax(&sh.maxabs_bits, (unsigned long long)__double_as_longlong(mx));
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double m = __longlong_as_double((long long)sh.maxabs_bits);
+    int e = 0;
+    if (isfinite(m)) frexp(m, &e); else sh.nonfinite = 1;
+    sh.E = e;
+  }
+  __syncthreads();
+  const int E = sh.E;
+
+  if (warp < 2 * T) {
+    // ===================== A producers: S tile (w % T), nonzero half (w / T) =====================
+    const int t = warp % T, h = warp / T;
+    const uint32_t q = (uint32_t)(it.tile0 + t);
+    const uint32_t tile_off = (uint32_t)(t * kF4ATile) + f4_off(lane, h);
+    // Philox of K-step ks+1 is computed while K-step ks is transposed (two independent chains)
+    auto gen = [&](int ks) -> uint4 {
+      const int slot = ks % kF4Slots;
+      f4_wait(&sh.jfull[slot], (ks / kF4Slots) & 1);
+      const uint32_t j = sh.js[slot][32 * h + lane];
+      f4_arrive(&sh.jempty[slot]);
+      return s_block(q, (uint64_t)P.row_offset + j, P.keys);   // padded nonzeros: j = 0, B = 0
+    };
+    uint4 xb = nsteps > 0 ? gen(0) : make_uint4(0, 0, 0, 0);
+    for (int ks = 0; ks < nsteps; ++ks) {
+      uint32_t x[4] = {xb.x, xb.y, xb.z, xb.w};
+      const int stage = ks % kF4Stages, use = ks / kF4Stages;
+      if (dbg == 1) {
+        if (ks + 1 < nsteps) { const int slot = (ks + 1) % kF4Slots; f4_wait(&sh.jfull[slot], ((ks + 1) / kF4Slots) & 1); f4_arrive(&sh.jempty[slot]); }
+        if (use > 0) f4_wait(&sh.empty[stage], (use - 1) & 1);
+      } else {
+        if (ks + 1 < nsteps) xb = gen(ks + 1);
+        f4_transpose<4>(x, lane);                   // lane r: row 32qq + r over the 32 nonzeros
+        if (use > 0) f4_wait(&sh.empty[stage], (use - 1) & 1);
+        const uint32_t tile = s_u32(stages + stage * kF4Stage) + tile_off;
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) f4_store_row(tile + (uint32_t)(qq * 4 * 256), x[qq]);   // row 32qq + lane
+      }
+      if (dbg != 3) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) f4_arrive(&sh.full[stage]);
+    }
+  } else if (warp >= kF4AWarps && warp < kF4Producers) {
+    // ===================== B producers: digits of nonzero half h =====================
+    const int h = warp - kF4AWarps;
+    // 2^(61-E) as two exact power-of-two factors (each within the double range)
+    const int e1 = 61 - E > 1000 ? 1000 : (61 - E < -1000 ? -1000 : 61 - E);
+    const double sc1 = ldexp(1.0, e1), sc2 = ldexp(1.0, 61 - E - e1);
+    for (int ks = 0; ks < nsteps; ++ks) {
+      const int slot = ks % kF4Slots;
+      f4_wait(&sh.jfull[slot], (ks / kF4Slots) & 1);
+      const double v0 = sh.vs[slot][32 * h + lane];
+      f4_arrive(&sh.jempty[slot]);
+      const int stage = ks % kF4Stages, use = ks / kF4Stages;
+      if (dbg == 4 || dbg == 5) {
+        if (use > 0) f4_wait(&sh.empty[stage], (use - 1) & 1);
+        __syncwarp();
+        if (lane == 0) f4_arrive(&sh.full[stage]);
+        continue;
+      }
+      const int64_t p = pb + (int64_t)ks * 64 + 32 * h + lane;
+      // U = A + 2^63 (mod 2^64); digit s = +1 iff bit s of U; nibble sign = NOT bit.  Padding
+      // nonzeros past the column end contribute nothing: their B nibbles are 0.0 (masked below).
+      unsigned long long U = 0ull;
+      if (p < pe) {
+        const long long A = __double2ll_rn((v0 * sc1) * sc2);
+        U = (unsigned long long)A ^ 0x8000000000000000ull;
+      }
+      uint32_t x[2] = {~(uint32_t)U, ~(uint32_t)(U >> 32)};   // sign bits of the digit nibbles
+      f4_transpose<2>(x, lane);                                // lane s: digit s (and 32 + s)
+      if (use > 0) f4_wait(&sh.empty[stage], (use - 1) & 1);
+      const uint32_t bt = s_u32(stages + stage * kF4Stage + kF4Tiles * kF4ATile);
+      const int64_t c0 = pb + (int64_t)ks * 64 + 32 * h;
+      const int nvalid = (int)(pe - c0 < 0 ? 0 : (pe - c0 > 32 ? 32 : pe - c0));
+      f4_store_row_masked(bt + f4_off(lane, h), x[0], nvalid);
+      f4_store_row_masked(bt + f4_off(32 + lane, h), x[1], nvalid);
+      if (nvalid < 32 && lane == 0) {   // last, partial K chunk: the ones row gets zeros too
+        const uint32_t z = 0u;         // (+1 digit signs are 0 bits: y = 0 -> nibbles 0x2)
+        f4_store_row_masked(bt + f4_off(64, h), z, nvalid);
+      }
+      if (dbg != 3) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) f4_arrive(&sh.full[stage]);
+    }
+  } else if (warp == kF4LoaderWarp) {
+    // ===================== loader: rowidx / vals -> smem ring with cp.async ====================
+    // Non-blocking: each lane issues its copies (zero-filled past the column end) and a
+    // cp.async.mbarrier.arrive.noinc that fires when they land; it only blocks on ring space.
+    for (int ks = 0; ks < nsteps; ++ks) {
+      const int slot = ks % kF4Slots, use = ks / kF4Slots;
+      if (use > 0) f4_wait(&sh.jempty[slot], (use - 1) & 1);
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int64_t p = pb + (int64_t)ks * 64 + 32 * half + lane;
+        const bool ok = p < pe;
+        const int64_t ps = ok ? p : pb;                 // any valid address; 0 bytes read if !ok
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;"
+                     :: "r"(s_u32(&sh.js[slot][32 * half + lane])), "l"(P.rowidx + ps), "r"(ok ? 4 : 0) : "memory");
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;"
+                     :: "r"(s_u32(&sh.vs[slot][32 * half + lane])), "l"(vals + ps), "r"(ok ? 8 : 0) : "memory");
+      }
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" :: "r"(s_u32(&sh.jfull[slot])) : "memory");
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  } else if (warp == kF4MmaWarp) {
+    // ===================== MMA issuer =====================
+    if (lane == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t idesc = f4_idesc();
+      for (int ks = 0; ks < nsteps; ++ks) {
+        const int stage = ks % kF4Stages;
+        f4_wait(&sh.full[stage], (ks / kF4Stages) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t sb = s_u32(stages + stage * kF4Stage);
+        const uint64_t bdesc = f4_desc(sb + kF4Tiles * kF4ATile);
+        for (int tt = 0; tt < T && dbg != 2 && dbg != 5; ++tt) {
+          const uint64_t adesc = f4_desc(sb + tt * kF4ATile);
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}"
+              :: "r"(tmem + (uint32_t)(tt * kF4N)), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(ks > 0 ? 1u : 0u),
+                 "r"(tmem + kF4SfCol), "r"(tmem + kF4SfCol + 32u));
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                     :: "r"(s_u32(&sh.empty[stage])) : "memory");
+      }
+      if (nsteps > 0)
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                     :: "r"(s_u32(&sh.done)) : "memory");
+    }
+    __syncwarp();
+  }
+
+  // ===================== epilogue: warps 0..11 read D (lane quarter = warp % 4) =====================
+  if (warp < kF4Producers) {
+    if (nsteps > 0) {
+      f4_wait(&sh.done, 0);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+    const int qw = warp & 3;
+    double* outc = reinterpret_cast<double*>(P.out) + (int64_t)it.col * P.ld;
+    const double nan = __longlong_as_double(0x7FF8000000000000ll);
+    for (int tt = warp >> 2; warp < 12 && tt < T; tt += 3) {
+      long long lo = 0, hi = 0, ones = 0;
+      if (nsteps > 0) {
+        const uint32_t base = tmem + ((uint32_t)(32 * qw) << 16) + (uint32_t)(tt * kF4N);
+#pragma unroll
+        for (int c = 0; c < 72; c += 8) {
+          uint32_t D[8];
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                       : "=r"(D[0]), "=r"(D[1]), "=r"(D[2]), "=r"(D[3]), "=r"(D[4]), "=r"(D[5]), "=r"(D[6]), "=r"(D[7])
+                       : "r"(base + (uint32_t)c));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const long long dv = (long long)__float2ll_rn(__uint_as_float(D[u]));
+            const int s = c + u;
+            if (s < 32) lo += dv << s;
+            else if (s < 64) hi += dv << (s - 32);
+            else if (s == 64) ones = dv;
+          }
+        }
+      }
+      const int64_t row = (int64_t)(it.tile0 + tt) * 128 + 32 * qw + lane;
+      if (row < P.d) {
+        // Σ_s 2^s D_s - D_64 = hi 2^32 + (lo - ones), both parts exact in fp64; one rounding
+        const double v = scalbn((double)hi * 4294967296.0 + (double)(lo - ones), E - 62);
+        outc[row] = sh.nonfinite ? nan : v;
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == kF4MmaWarp) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(512));
+  }
+}
+
+}  // namespace
+
+int f4_tiles_per_cta() { return kF4Tiles; }
+
+cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const TcItem* items, int64_t n_items, cudaStream_t stream) {
+  if (n_items == 0) return cudaSuccess;
+  const size_t smem = (size_t)kF4Stages * kF4Stage + sizeof(F4Shared) + 1024;
+  cudaError_t e = cudaFuncSetAttribute(sk_rad_f4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  static const int dbg = [] { const char* v = getenv("SKETCH_F4_DEBUG"); return v ? atoi(v) : 0; }();
+  sk_rad_f4_kernel<<<(unsigned)n_items, kF4Threads, smem, stream>>>(a, items, dbg);
+  return cudaGetLastError();
+}
+
+}  // namespace sk

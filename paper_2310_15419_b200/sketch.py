@@ -27,7 +27,11 @@ SK_OK, SK_EINVAL, SK_ECSC, SK_ENOMEM, SK_ECUDA, SK_EUNSUPPORTED = 0, -1, -2, -3,
 
 EXPORTS = ["sketch_plan", "sketch_plan_host", "sketch_apply", "sketch_apply_csc",
            "sketch_apply_host", "sketch_fill_s", "sketch_plan_stats", "sketch_plan_destroy",
-           "sketch_error_string", "sketch_last_error_detail", "sketch_version"]
+           "sketch_error_string", "sketch_last_error_detail", "sketch_version",
+           "sketch_set_rad_f64_path", "sketch_apply_kernel_name"]
+RAD_F64_PATHS = {"fp4": 0, "int8smem": 1, "int8tmem": 2, "simt": 3}
+_STRING_RESULTS = ("sketch_error_string", "sketch_last_error_detail", "sketch_version",
+                   "sketch_apply_kernel_name")
 
 
 class SketchError(RuntimeError):
@@ -76,8 +80,11 @@ def load_library(path: str = LIB_PATH):
         lib.sketch_last_error_detail.restype = ctypes.c_char_p
         lib.sketch_version.argtypes = []
         lib.sketch_version.restype = ctypes.c_char_p
+        lib.sketch_set_rad_f64_path.argtypes = [i32]
+        lib.sketch_apply_kernel_name.argtypes = [vp, i32]
+        lib.sketch_apply_kernel_name.restype = ctypes.c_char_p
         for name in EXPORTS:
-            if name not in ("sketch_error_string", "sketch_last_error_detail", "sketch_version"):
+            if name not in _STRING_RESULTS:
                 getattr(lib, name).restype = ctypes.c_int
         _lib = lib
         return lib
@@ -163,6 +170,10 @@ class Plan:
                "sketch_apply")
         return out
 
+    def kernel_name(self, dist) -> str:
+        """Name of the kernel ``apply`` launches for ``dist``."""
+        return load_library().sketch_apply_kernel_name(self._h, _dist(dist)).decode()
+
     def close(self):
         if getattr(self, "_h", None):
             _check(load_library().sketch_plan_destroy(self._h), "sketch_plan_destroy")
@@ -234,6 +245,13 @@ def sketch_fill_s(seed, dist, i0, i1, j0, j1, dtype="f64", device="cuda", stream
                                         int(j0), int(j1), ctypes.c_void_p(out.data_ptr()),
                                         int(i1) - int(i0), _stream_ptr(stream)), "sketch_fill_s")
     return out
+
+
+def set_rad_f64_path(path) -> None:
+    """Select the kernel for ±1 sketches of fp64 values: "fp4" (tensor cores, default),
+    "int8smem", "int8tmem" or "simt" (process-wide)."""
+    p = RAD_F64_PATHS[path] if isinstance(path, str) else int(path)
+    _check(load_library().sketch_set_rad_f64_path(p), "sketch_set_rad_f64_path")
 
 
 def version() -> str:

@@ -1,0 +1,130 @@
+// microbench_mxf4.cu -- tcgen05.mma kind::mxf4 (block-scaled packed e2m1) throughput on sm_100a:
+// A = 128 x 64 fp4 (4 KB, K-major no swizzle), B = N x 64 fp4 (K-major), scale factors (ue8m0 = 1.0)
+// in TMEM, f32 accumulators.  Also a correctness probe: A = B = all +1.0 (nibble 0x2), so every
+// accumulator element must equal 64 * iters.
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)(layout & 7u) << 61;
+  return d;
+}
+
+template <int N, int LAY>
+__global__ void __launch_bounds__(128, 1) k(int iters, unsigned long long* cyc, float* probe) {
+  extern __shared__ __align__(1024) unsigned char raw[];
+  unsigned char* sm = raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
+  __shared__ uint64_t bar[4];
+  __shared__ uint32_t tbase;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // A: 4 tiles x 4 KB, B: N x 32 B; all nibbles 0x2 (+1.0)
+  for (int i = threadIdx.x; i < 4 * 16384 + N * 32; i += blockDim.x) sm[i] = 0x22;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 4; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(&bar[i])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" :: "r"(smem_u32(&tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  const uint32_t tb = tbase;
+  // scale factors: columns [448, 512) of every lane = 0x7F (ue8m0 1.0)
+  {
+    const uint32_t taddr = tb + ((uint32_t)(32 * (warp & 3)) << 16) + 448u;
+    uint32_t v = 0x7F7F7F7Fu;
+    for (int c = 0; c < 64; c += 8)
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1};"
+                   :: "r"(taddr + c), "r"(v) : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  }
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t idesc = (0u << 4) | (1u << 7) | (1u << 10) | (0u << 15) | (0u << 16) |
+                         ((uint32_t)(N >> 3) << 17) | (1u << 23) | ((128u >> 4) << 24);
+  const int nacc = 448 / N < 4 ? 448 / N : 4;
+  if (threadIdx.x == 0) {
+    const uint32_t a0 = smem_u32(sm);
+    const uint32_t b0 = smem_u32(sm + 4 * 16384);
+    const uint64_t bdesc = make_desc(b0, 128u, 256u, 0u);     // K core-matrix stride 128 B, N 8-row groups 256 B
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      const int bi = it & 3;
+      if (it >= 4)
+        asm volatile("{\n\t.reg .pred P1;\n\tWAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t@!P1 bra WAIT_%=;\n\t}"
+                     :: "r"(smem_u32(&bar[bi])), "r"((uint32_t)(((it >> 2) - 1) & 1)) : "memory");
+      for (int t = 0; t < 4; ++t) {
+        // LAY 0: K-major no swizzle (core 8x16B, LBO=128 K, SBO=256 M); LAY 6: SWIZZLE_32B (8 rows x 32 B atoms,
+        // SBO=256); LAY 2: SWIZZLE_128B (8 rows x 128 B atoms, SBO=1024, K slice = first 32 B of each row)
+        const uint64_t adesc = LAY == 0 ? make_desc(a0 + t * 4096, 128u, 256u, 0u)
+                             : LAY == 6 ? make_desc(a0 + t * 4096, 16u, 256u, 6u)
+                                        : make_desc(a0 + t * 16384 / 4, 16u, 1024u, 2u);
+        const uint32_t d = tb + (uint32_t)((t % nacc) * N);
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                     "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}"
+                     :: "r"(d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(it > 0 ? 1u : 0u),
+                        "r"(tb + 448u), "r"(tb + 480u));
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                   :: "r"(smem_u32(&bar[bi])) : "memory");
+    }
+    for (int it = (iters > 4 ? iters - 4 : 0); it < iters; ++it)
+      asm volatile("{\n\t.reg .pred P1;\n\tWAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t@!P1 bra WAIT_%=;\n\t}"
+                   :: "r"(smem_u32(&bar[it & 3])), "r"((uint32_t)((it >> 2) & 1)) : "memory");
+    long long t1 = clock64();
+    if (blockIdx.x == 0) *cyc = (unsigned long long)(t1 - t0);
+  }
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (blockIdx.x == 0) {
+    uint32_t v[8];
+    const uint32_t taddr = tb + ((uint32_t)(32 * (warp & 3)) << 16);
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    probe[threadIdx.x] = __uint_as_float(v[0]);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" :: "r"(tb));
+}
+
+template <int N, int LAY>
+void run() {
+  unsigned long long* d;
+  float* probe;
+  cudaMalloc(&d, 8);
+  cudaMalloc(&probe, 128 * 4);
+  const int smem = 4 * 16384 + 256 * 32 + 1024;
+  cudaFuncSetAttribute(k<N, LAY>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int iters = 400;
+  k<N, LAY><<<148, 128, smem>>>(iters, d, probe);
+  cudaError_t e = cudaDeviceSynchronize();
+  unsigned long long c = 0;
+  float h[128];
+  cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
+  cudaMemcpy(h, probe, sizeof(h), cudaMemcpyDeviceToHost);
+  const double per = (double)c / (iters * 4.0);
+  printf("layout %d mxf4 M=128 N=%3d K=64: %.1f cycles/MMA, %.1f A-bytes/clk, %.1f entries/clk; probe D[0]=%.1f D[127]=%.1f (expect %d) %s\n",
+         LAY, N, per, 4096.0 / per, 8192.0 / per, h[0], h[127], 64 * iters, e == cudaSuccess ? "ok" : cudaGetErrorString(e));
+  cudaFree(d);
+  cudaFree(probe);
+}
+
+int main() {
+  run<64, 0>();
+  run<64, 6>();
+  run<64, 2>();
+  return 0;
+}

@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(544, 1) k(int iters, unsigned long long* cyc, 
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
-  const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)AMAJOR << 15) | (1u << 16) |
+  const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(AMAJOR == 1) << 15) | (1u << 16) |
                          ((uint32_t)(N >> 3) << 17) | ((128u >> 4) << 24);
   const int ncols = N < 32 ? 32 : N;   // accumulator stride (columns)
   const int nacc = 512 / ncols < 16 ? 512 / ncols : 16;
@@ -66,12 +66,20 @@ __global__ void __launch_bounds__(544, 1) k(int iters, unsigned long long* cyc, 
                      :: "r"(smem_u32(&bar[bi])), "r"((uint32_t)(((it >> 2) - 1) & 1)) : "memory");
       }
       for (int t = 0; t < 16; ++t) {
+        if constexpr (AMAJOR == 2) {
+          const uint32_t d = tbase + (uint32_t)(t * 16);
+          const uint32_t at = tbase + 256u + (uint32_t)(t * 8);
+          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                       "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}"
+                       :: "r"(d), "r"(at), "l"(bdesc), "r"(idesc), "r"(it > 0 ? 1u : 0u));
+        } else {
         const uint64_t adesc = AMAJOR ? make_desc(a0 + t * 4096, 4096u, 1024u, 2u)
                                       : make_desc(a0 + t * 4096, 16u, 1024u, 2u);
         const uint32_t d = tbase + (uint32_t)((t % nacc) * ncols);
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
                      :: "r"(d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(it > 0 ? 1u : 0u));
+        }
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
                    :: "r"(smem_u32(&bar[bi])) : "memory");
@@ -115,6 +123,8 @@ void run(const char* name) {
 }
 
 int main() {
+  run<16, 2, 0>("A TMEM K-major (TS)");
+  run<16, 2, 1>("A TMEM K-major (TS) + STS");
   run<16, 1, 0>("A MN-major SW128");
   run<16, 1, 1>("A MN-major SW128 + STS stress");
   run<64, 1, 0>("A MN-major SW128");

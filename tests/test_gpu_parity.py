@@ -152,6 +152,44 @@ def test_sketch_matches_oracle_small(sk, dist, case):
     _check(got, ref, B, TOL["f64"])
 
 
+@pytest.mark.parametrize("path", ["fp4", "int8smem", "int8tmem", "simt"])
+def test_rad_f64_kernel_paths(sk, path):
+    # every ±1 fp64 kernel (tensor-core fp4 / int8-smem / int8-TMEM, SIMT) meets the fp64 bar on
+    # the edge cases: ragged d and tiles, empty and single-nonzero columns, a column that is long
+    # relative to the rest, unsorted rows with duplicates, explicit zeros and huge / tiny values
+    try:
+        sk.set_rad_f64_path(path)
+        cases = [workloads.random_csc(5000, 40, 33, seed=2),
+                 workloads.random_csc(3000, 12, [0, 5, 0, 0, 64, 1, 0, 33, 0, 2, 0, 100], seed=5),
+                 workloads.random_csc(200000, 24, [20000] + [10] * 23, seed=6),
+                 workloads.random_csc(500, 10, 40, seed=7, sorted_rows=False, duplicates=True)]
+        wide = workloads.random_csc(4000, 6, 70, seed=17)
+        wide.vals = wide.vals * np.logspace(-200, 200, wide.nnz)       # dynamic range per column
+        wide.vals[::7] = 0.0
+        cases.append(wide)
+        for A, d in zip(cases, [1000, 300, 1100, 129, 2050]):
+            plan_kernel = None
+            got = _gpu_sketch(sk, A, d, "rademacher", 31)
+            ref, B = oracle.sketch(31, "rademacher", d, A.m, A.n, A.colptr, A.rowidx, A.vals, threads=8)
+            _check(got, ref, B, TOL["f64"])
+            del plan_kernel
+    finally:
+        sk.set_rad_f64_path("fp4")
+
+
+def test_kernel_names_report_the_path(sk):
+    A = workloads.random_csc(1000, 4, 10, seed=1)
+    plan = sk.Plan(_dev(A.colptr), _dev(A.rowidx), 300, A.m, "f64")
+    try:
+        for path, tag in (("fp4", "mxf4"), ("int8smem", "smem"), ("int8tmem", "TMEM"), ("simt", "sk_rad_kernel")):
+            sk.set_rad_f64_path(path)
+            assert tag in plan.kernel_name("rademacher")
+        assert "uniform" in plan.kernel_name("uniform") and "gaussian" in plan.kernel_name("gaussian")
+    finally:
+        sk.set_rad_f64_path("fp4")
+        plan.close()
+
+
 @pytest.mark.parametrize("dist", ["rademacher", "uniform", "gaussian"])
 def test_sketch_f32_matches_oracle(sk, dist):
     A = workloads.random_csc(20000, 25, 120, seed=10, dtype=np.float32)

@@ -168,11 +168,9 @@ def test_rad_f64_kernel_paths(sk, path):
         wide.vals[::7] = 0.0
         cases.append(wide)
         for A, d in zip(cases, [1000, 300, 1100, 129, 2050]):
-            plan_kernel = None
             got = _gpu_sketch(sk, A, d, "rademacher", 31)
             ref, B = oracle.sketch(31, "rademacher", d, A.m, A.n, A.colptr, A.rowidx, A.vals, threads=8)
             _check(got, ref, B, TOL["f64"])
-            del plan_kernel
     finally:
         sk.set_rad_f64_path("fp4")
 

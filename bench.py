@@ -103,14 +103,21 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def load_profile_traffic(config: str):
-    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+def load_profile_traffic(config: str, kernel: str):
+    """dram bytes (read + write) per launch of `kernel` on `config` from the committed
+    `ncu --set full` capture (profiles/traffic.json), or None."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(path) as f:
-            return json.load(f).get(config)
+            entry = json.load(f).get(config)
     except Exception:
         return None
+    if isinstance(entry, dict):
+        for k, v in entry.items():
+            if k in kernel or kernel.startswith(k):
+                return v
+        return None
+    return entry
 
 
 def cpu_baseline(cfg, A, max_wall_s: float = 8.0):
@@ -342,15 +349,22 @@ def main():
     achieved_tf = 2.0 * cfg.d * nnz_local / (t_kern / 1e3) / 1e12
     peak_tf = alu_peak_tflops(cfg.dtype, sm_mhz)
     stats = plan.stats()
+    kname = plan.kernel_name(cfg.dist)
     roofline = {"bound": "alu", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
-                "frac": achieved_tf / peak_tf, "traffic": load_profile_traffic(cfg.name),
-                "kernel": "sk_rad_kernel<double>" if cfg.dist == "rademacher" and cfg.dtype == "f64"
-                else f"sk_{'rad' if cfg.dist == 'rademacher' else 'pair'}_kernel",
-                "peak_source": f"{cfg.dtype} vector pipe: 148 SMs x {64 if cfg.dtype == 'f64' else 128} "
-                               f"lanes x 2 flop x {sm_mhz:.0f} MHz (sm_max_mhz of {peak_src} peaks)",
+                "frac": achieved_tf / peak_tf, "traffic": load_profile_traffic(cfg.name, kname),
+                "kernel": kname,
+                "peak_source": f"{cfg.dtype} vector pipe (the SpMM's FMA roofline): 148 SMs x "
+                               f"{64 if cfg.dtype == 'f64' else 128} lanes x 2 flop x {sm_mhz:.0f} MHz "
+                               f"(sm_max_mhz of {peak_src} peaks)",
                 "kernel_ms": t_kern,
                 "hbm_frac": (in_bytes / (t_kern / 1e3) / 1e9) / float(peaks.get("hbm_gbs", 6650.0)),
                 "algorithmic_bytes": int(in_bytes)}
+    if "mxf4" in kname:
+        # the tensor-core path's own ceiling: one M=128,K=64 mxf4 MMA per 92 cycles
+        # (scripts/microbench_mxf4.cu) = 89 (row, nonzero) entries/clk/SM
+        tc_peak = 2 * 89.0 * 148 * sm_mhz * 1e6 / 1e12
+        roofline["tensor_feed_peak"] = tc_peak
+        roofline["tensor_feed_frac"] = achieved_tf / tc_peak
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -16,13 +16,13 @@ constexpr int kThreads = kWarps * 32;
 constexpr int kRowsPerWarpRad = 1024;
 constexpr int kRowsPerWarpPair = 512;
 
-// One CTA of work: column `col`, Â rows [row0, row0 + (1 << wd_log2) * rows_per_warp).
-// The CTA's 16 warps are arranged as W_d = 1 << wd_log2 row-warps times
-// W_k = 16 >> wd_log2 slices of the column's nonzero stream.
+// One CTA of work: column `col`, Â rows [row0, row0 + wd * rows_per_warp).
+// The CTA's 16 warps are arranged as W_d = wd row-warps times W_k = 16 / wd slices of the
+// column's nonzero stream (16 - W_d W_k warps idle when W_d does not divide 16).
 struct Item {
   int32_t col;
   int32_t row0;
-  int32_t wd_log2;
+  int32_t wd;
   int32_t pad;
 };
 
@@ -56,6 +56,10 @@ cudaError_t launch_apply_rad_tc(const ApplyArgs& a, const TcItem* items, int64_t
 int tc_tiles_per_cta();
 cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const TcItem* items, int64_t n_items, cudaStream_t stream);
 int f4_tiles_per_cta();
+// Tensor cores + FP64 SIMT in one persistent kernel; items = int8 schedule (<= 16 tiles each);
+// counter = one device int (work queue head), reset by the launcher.
+cudaError_t launch_apply_rad_hybrid(const ApplyArgs& a, const TcItem* items, int64_t n_items, int* counter,
+                                    cudaStream_t stream);
 
 // dist: 0 = Rademacher, 1 = uniform, 2 = Gaussian; dtype: 0 = f64, 1 = f32.
 cudaError_t launch_apply(int dist, int dtype, const ApplyArgs& a, cudaStream_t stream);

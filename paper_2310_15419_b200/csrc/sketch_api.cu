@@ -56,42 +56,38 @@ Schedule build_schedule(const int64_t* colptr, int64_t n, int64_t d, int rows_pe
                         int blocks_per_nnz_per_warp) {
   Schedule S;
   const int64_t n_rw = (d + rows_per_warp - 1) / rows_per_warp;  // row-warps covering d
-  // W_d (row-warps per CTA) minimising padded row-warps; ties -> larger W_d.
-  int base = 0;
-  int64_t best_waste = INT64_MAX;
-  for (int wdl = 4; wdl >= 0; --wdl) {
-    const int64_t WD = int64_t(1) << wdl;
-    const int64_t waste = ((n_rw + WD - 1) / WD) * WD - n_rw;
-    if (waste < best_waste) { best_waste = waste; base = wdl; }
-  }
-  auto cost_of = [&](int64_t L, int wdl) {
-    const int64_t WK = sk::kWarps >> wdl;
-    return (L + WK - 1) / WK + 2;   // per-warp nonzeros (+ store / reduction overhead)
+  // Cost of one CTA (warps run in parallel): its per-warp nonzero slice plus a fixed overhead
+  // (prologue, reduction, store) of about 30 nonzero-equivalents.  W_d (row-warps per CTA,
+  // 1..16) minimises Σ_columns tiles × cost for the matrix as a whole.
+  auto cost_of = [&](int64_t L, int64_t WD) {
+    const int64_t WK = sk::kWarps / WD;
+    return (L + WK - 1) / WK + 30;
   };
+  int64_t base = 1;
+  double best = 1e300;
+  for (int64_t WD = 1; WD <= std::min<int64_t>(16, n_rw); ++WD) {
+    const int64_t tiles = (n_rw + WD - 1) / WD;
+    double tot = 0;
+    for (int64_t k = 0; k < n; ++k) tot += (double)tiles * (double)cost_of(colptr[k + 1] - colptr[k], WD);
+    if (tot < best * 0.999) { best = tot; base = WD; }
+  }
   // Average load per SM slot with the base shape; a column whose CTAs would each exceed a
   // quarter of it is re-shaped to W_d = 1 (16 warps on its nonzero stream) so the longest
   // CTAs do not set the makespan (column-length skew, e.g. power-law columns).
-  double total = 0;
-  for (int64_t k = 0; k < n; ++k) {
-    const int64_t L = colptr[k + 1] - colptr[k];
-    const int64_t tiles = (n_rw + (int64_t(1) << base) - 1) >> base;
-    total += (double)cost_of(L, base) * (double)tiles;
-  }
-  const double per_slot = total / kSMs;
+  const double per_slot = best / kSMs;
   std::vector<std::pair<int64_t, Item>> tmp;
   for (int64_t k = 0; k < n; ++k) {
     const int64_t L = colptr[k + 1] - colptr[k];
-    int wdl = base;
-    if (wdl > 0 && (double)cost_of(L, wdl) > 0.25 * per_slot) wdl = 0;
-    const int64_t WD = int64_t(1) << wdl;
+    int64_t WD = base;
+    if (WD > 1 && (double)cost_of(L, WD) > 0.25 * per_slot) WD = 1;
     const int64_t tiles = (n_rw + WD - 1) / WD;
     for (int64_t tt = 0; tt < tiles; ++tt) {
       Item it;
       it.col = (int32_t)k;
       it.row0 = (int32_t)(tt * WD * rows_per_warp);
-      it.wd_log2 = wdl;
+      it.wd = (int32_t)WD;
       it.pad = 0;
-      tmp.emplace_back(cost_of(L, wdl), it);
+      tmp.emplace_back(cost_of(L, WD), it);
     }
     S.philox_blocks += L * tiles * WD * blocks_per_nnz_per_warp;
   }
@@ -140,7 +136,8 @@ int rad_f64_path() {
   if (v >= 0) return v;
   v = SK_PATH_TC_FP4;
   if (const char* e = getenv("SKETCH_RAD_F64_PATH")) {
-    if (!strcmp(e, "int8smem")) v = SK_PATH_TC_INT8_SMEM;
+    if (!strcmp(e, "hybrid")) v = SK_PATH_HYBRID;
+    else if (!strcmp(e, "int8smem")) v = SK_PATH_TC_INT8_SMEM;
     else if (!strcmp(e, "int8tmem")) v = SK_PATH_TC_INT8_TMEM;
     else if (!strcmp(e, "simt")) v = SK_PATH_SIMT;
   }
@@ -198,7 +195,9 @@ int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
   p->n_pair = (int64_t)pair.items.size();
   p->philox_rad = rad.philox_blocks;
   p->philox_pair = pair.philox_blocks;
-  if (dtype == SK_F64 && p->max_col <= sk::kTcMaxColumn && n > 0) {
+  // Tensor-core ±1 paths: every column within the exact-accumulation bound, and columns long
+  // enough on average (>= 256 nonzeros) to amortise a CTA's TMEM / barrier / scale prologue.
+  if (dtype == SK_F64 && p->max_col <= sk::kTcMaxColumn && n > 0 && nnz >= 256 * n) {
     std::vector<sk::TcItem> tc = build_tc_schedule(h_colptr, n, d, sk::tc_tiles_per_cta());
     std::vector<sk::TcItem> f4 = build_tc_schedule(h_colptr, n, d, sk::f4_tiles_per_cta());
     p->n_tc = (int64_t)tc.size();
@@ -253,7 +252,12 @@ int apply_items(const sk_plan_s* p, uint64_t seed, sk_dist_t dist, const void* v
   cudaError_t e;
   const int path = rad_f64_path();
   if (dist == SK_RADEMACHER && p->n_tc > 0 && path != SK_PATH_SIMT) {
-    if (path == SK_PATH_TC_FP4) e = sk::launch_apply_rad_f4(a, p->d_tc + p->n_tc, p->n_f4, stream);
+    if (path == SK_PATH_HYBRID) {
+      int* counter = nullptr;
+      e = cudaMallocAsync((void**)&counter, sizeof(int), stream);
+      if (e == cudaSuccess) e = sk::launch_apply_rad_hybrid(a, p->d_tc, p->n_tc, counter, stream);
+      if (counter) cudaFreeAsync(counter, stream);
+    } else if (path == SK_PATH_TC_FP4) e = sk::launch_apply_rad_f4(a, p->d_tc + p->n_tc, p->n_f4, stream);
     else e = sk::launch_apply_rad_tc(a, p->d_tc, p->n_tc, path == SK_PATH_TC_INT8_SMEM ? 1 : 0, stream);
   } else
     e = sk::launch_apply((int)dist, (int)p->dtype, a, stream);
@@ -284,6 +288,7 @@ const char* kernel_name(const sk_plan_s* p, int dist) {
     if (p->n_tc > 0) {
       switch (rad_f64_path()) {
         case SK_PATH_TC_FP4: return "sk_rad_f4_kernel (tcgen05 kind::mxf4)";
+        case SK_PATH_HYBRID: return "sk_rad_hybrid_kernel (tcgen05 kind::i8 + FP64 SIMT)";
         case SK_PATH_TC_INT8_SMEM: return "sk_rad_tc_kernel (tcgen05 kind::i8, S in smem)";
         case SK_PATH_TC_INT8_TMEM: return "sk_rad_tm_kernel (tcgen05 kind::i8, S in TMEM)";
         default: break;
@@ -535,7 +540,7 @@ const char* sketch_last_error_detail(void) { return g_detail.c_str(); }
 const char* sketch_version(void) { return "libsketch 0.2.0 sm_100a"; }
 
 int sketch_set_rad_f64_path(int path) {
-  if (path < SK_PATH_TC_FP4 || path > SK_PATH_SIMT) return SK_EINVAL;
+  if (path < SK_PATH_TC_FP4 || path > SK_PATH_HYBRID) return SK_EINVAL;
   g_rad_f64_path.store(path, std::memory_order_relaxed);
   return SK_OK;
 }

@@ -87,17 +87,18 @@ __device__ __forceinline__ T finish_sign_sum(T acc, T total) {
 // every nonzero, so they split the RNG work: for a group of 4 nonzeros, lane t of the quad
 // generates block q of nonzero 4u + t, and a 4x4 word transpose through shared memory hands
 // every lane its own word of all four blocks.  One Philox call per 128 (row, nonzero) pairs.
+// fp32 needs 32 accumulator registers, so two CTAs fit per SM (one CTA's prologue / reduction /
+// store overlaps the other's main loop); fp64 needs 64 and runs one CTA per SM.
 template <typename T, int SELMODE>
-__global__ void __launch_bounds__(kThreads, 1) sk_rad_kernel(const ApplyArgs P) {
+__global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 2 : 1) sk_rad_kernel(const ApplyArgs P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const Item it = P.items[blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wdl = it.wd_log2;
-  const int WD = 1 << wdl, WK = kWarps >> wdl;
-  const int wd = warp & (WD - 1), wk = warp >> wdl;
+  const int WD = it.wd, WK = kWarps / WD;              // warps >= WD*WK get an empty slice
+  const int wd = warp % WD, wk = warp / WD;
   const int64_t pb = P.colptr[it.col], pe = P.colptr[it.col + 1];
   const int64_t L = pe - pb;
-  const int64_t s0 = pb + (L * wk) / WK, s1 = pb + (L * (wk + 1)) / WK;
+  const int64_t s0 = wk < WK ? pb + (L * wk) / WK : pe, s1 = wk < WK ? pb + (L * (wk + 1)) / WK : pe;
   const int64_t warp_row0 = (int64_t)it.row0 + (int64_t)wd * kRowsPerWarpRad;
   const uint32_t q = (uint32_t)(warp_row0 >> 7) + (uint32_t)(lane >> 2);
   const int t = lane & 3, g = lane >> 2;
@@ -153,7 +154,7 @@ __global__ void __launch_bounds__(kThreads, 1) sk_rad_kernel(const ApplyArgs P) 
     const int rwd = r >> 10, rr = r & 1023;
     const int off = (rr >> 5) * kRadPad + (rr & 31);
     T s = red[rwd * (32 * kRadPad) + off];
-    for (int kk = 1; kk < WK; ++kk) s += red[((kk << wdl) + rwd) * (32 * kRadPad) + off];
+    for (int kk = 1; kk < WK; ++kk) s += red[(kk * WD + rwd) * (32 * kRadPad) + off];
     outc[row] = s;
   }
 }
@@ -182,12 +183,11 @@ __global__ void __launch_bounds__(kThreads, 1) sk_pair_kernel(const ApplyArgs P)
   extern __shared__ __align__(16) unsigned char smem[];
   const Item it = P.items[blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wdl = it.wd_log2;
-  const int WD = 1 << wdl, WK = kWarps >> wdl;
-  const int wd = warp & (WD - 1), wk = warp >> wdl;
+  const int WD = it.wd, WK = kWarps / WD;              // warps >= WD*WK get an empty slice
+  const int wd = warp % WD, wk = warp / WD;
   const int64_t pb = P.colptr[it.col], pe = P.colptr[it.col + 1];
   const int64_t L = pe - pb;
-  const int64_t s0 = pb + (L * wk) / WK, s1 = pb + (L * (wk + 1)) / WK;
+  const int64_t s0 = wk < WK ? pb + (L * wk) / WK : pe, s1 = wk < WK ? pb + (L * (wk + 1)) / WK : pe;
   const int64_t lane_row0 = (int64_t)it.row0 + (int64_t)wd * kRowsPerWarpPair + 16 * lane;
   const uint32_t q0 = (uint32_t)(lane_row0 >> 1);
   // Lanes whose rows all lie past d skip generation (their results are never stored).
@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(kThreads, 1) sk_pair_kernel(const ApplyArgs P)
     const int rwd = r >> 9, rr = r & 511;
     const int off = (rr >> 4) * kPairPad + (rr & 15);
     T s = red[rwd * (32 * kPairPad) + off];
-    for (int kk = 1; kk < WK; ++kk) s += red[((kk << wdl) + rwd) * (32 * kPairPad) + off];
+    for (int kk = 1; kk < WK; ++kk) s += red[(kk * WD + rwd) * (32 * kPairPad) + off];
     outc[row] = s;
   }
 }

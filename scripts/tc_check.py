@@ -1,7 +1,6 @@
-"""Quick GPU check of the tensor-core ±1 path against the oracle on small cases, then timing."""
+"""Quick GPU check of every ±1 fp64 kernel path against the oracle on small cases."""
 import os
 import sys
-import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -12,19 +11,20 @@ import oracle  # noqa: E402
 import workloads  # noqa: E402
 from paper_2310_15419_b200 import sketch as sk  # noqa: E402
 
-
-def run(A, d, seed):
-    dev = torch.device("cuda:0")
-    plan = sk.Plan(torch.from_numpy(A.colptr).to(dev), torch.from_numpy(A.rowidx).to(dev), d, A.m, "f64",
-                   row_offset=A.row_offset)
-    out = plan.apply(torch.from_numpy(A.vals).to(dev), seed, "rademacher")
-    torch.cuda.synchronize()
-    return out.T.cpu().numpy()
-
-
-for (m, n, L, d) in [(300, 3, 5, 128), (1000, 4, 40, 300), (5000, 7, 100, 2000), (20000, 5, 3000, 700)]:
-    A = workloads.random_csc(m, n, L, seed=1)
-    got = run(A, d, 7)
-    ref, B = oracle.sketch(7, "rademacher", d, A.m, A.n, A.colptr, A.rowidx, A.vals)
-    rel = np.abs(got - ref) / np.maximum(B, 1e-300)
-    print(f"m={m} n={n} L={L} d={d}: max rel err {rel.max():.3e}", flush=True)
+paths = sys.argv[1:] or ["fp4", "hybrid", "int8smem", "int8tmem", "simt"]
+dev = torch.device("cuda:0")
+for path in paths:
+    sk.set_rad_f64_path(path)
+    worst = 0.0
+    for (m, n, L, d) in [(3000, 3, 500, 128), (10000, 4, 400, 300), (50000, 7, 1000, 2000), (20000, 5, 3000, 700),
+                         (90000, 300, 260, 2000)]:
+        A = workloads.random_csc(m, n, L, seed=1)
+        plan = sk.Plan(torch.from_numpy(A.colptr).to(dev), torch.from_numpy(A.rowidx).to(dev), d, A.m, "f64")
+        out = plan.apply(torch.from_numpy(A.vals).to(dev), 7, "rademacher")
+        torch.cuda.synchronize()
+        got = out.T.cpu().numpy()
+        kname = plan.kernel_name("rademacher")
+        plan.close()
+        ref, B = oracle.sketch(7, "rademacher", d, A.m, A.n, A.colptr, A.rowidx, A.vals, threads=8)
+        worst = max(worst, float((np.abs(got - ref) / np.maximum(B, 1e-300)).max()))
+    print(f"{path:9s} {kname}: max rel err {worst:.3e}", flush=True)

@@ -152,18 +152,19 @@ def test_sketch_matches_oracle_small(sk, dist, case):
     _check(got, ref, B, TOL["f64"])
 
 
-@pytest.mark.parametrize("path", ["fp4", "int8smem", "int8tmem", "simt"])
+@pytest.mark.parametrize("path", ["fp4", "int8smem", "int8tmem", "simt", "hybrid"])
 def test_rad_f64_kernel_paths(sk, path):
     # every ±1 fp64 kernel (tensor-core fp4 / int8-smem / int8-TMEM, SIMT) meets the fp64 bar on
     # the edge cases: ragged d and tiles, empty and single-nonzero columns, a column that is long
     # relative to the rest, unsorted rows with duplicates, explicit zeros and huge / tiny values
     try:
         sk.set_rad_f64_path(path)
-        cases = [workloads.random_csc(5000, 40, 33, seed=2),
-                 workloads.random_csc(3000, 12, [0, 5, 0, 0, 64, 1, 0, 33, 0, 2, 0, 100], seed=5),
+        # (averages >= 256 nonzeros per column, so the tensor-core paths are eligible)
+        cases = [workloads.random_csc(50000, 40, 300, seed=2),
+                 workloads.random_csc(30000, 12, [0, 500, 0, 0, 640, 1, 0, 3300, 0, 2, 0, 100], seed=5),
                  workloads.random_csc(200000, 24, [20000] + [10] * 23, seed=6),
-                 workloads.random_csc(500, 10, 40, seed=7, sorted_rows=False, duplicates=True)]
-        wide = workloads.random_csc(4000, 6, 70, seed=17)
+                 workloads.random_csc(5000, 10, 400, seed=7, sorted_rows=False, duplicates=True)]
+        wide = workloads.random_csc(40000, 6, 700, seed=17)
         wide.vals = wide.vals * np.logspace(-200, 200, wide.nnz)       # dynamic range per column
         wide.vals[::7] = 0.0
         cases.append(wide)
@@ -176,10 +177,11 @@ def test_rad_f64_kernel_paths(sk, path):
 
 
 def test_kernel_names_report_the_path(sk):
-    A = workloads.random_csc(1000, 4, 10, seed=1)
+    A = workloads.random_csc(10000, 4, 300, seed=1)
     plan = sk.Plan(_dev(A.colptr), _dev(A.rowidx), 300, A.m, "f64")
     try:
-        for path, tag in (("fp4", "mxf4"), ("int8smem", "smem"), ("int8tmem", "TMEM"), ("simt", "sk_rad_kernel")):
+        for path, tag in (("fp4", "mxf4"), ("int8smem", "smem"), ("int8tmem", "TMEM"), ("simt", "sk_rad_kernel"),
+                          ("hybrid", "hybrid")):
             sk.set_rad_f64_path(path)
             assert tag in plan.kernel_name("rademacher")
         assert "uniform" in plan.kernel_name("uniform") and "gaussian" in plan.kernel_name("gaussian")

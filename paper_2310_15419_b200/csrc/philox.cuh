@@ -63,10 +63,19 @@ __device__ __forceinline__ uint4 s_block(uint32_t q, uint64_t j, const PhiloxKey
 // ---------------------------------------------------------------- transforms
 
 // Uniform (-1, 1) on the odd 2^-53 grid: k = (xa:xb) >> 11, S = (2k + 1 - 2^53) 2^-53.
-// Computed without an int->double conversion: with b = bit 52 of k and r = k mod 2^52,
-// |S| = r'·2^-52 + 2^-53 where r' = b ? r : (2^52 - 1 - r); M = 1 + r'·2^-52 is built
-// from bits and |S| = M - (1 - 2^-53) is exact (Sterbenz).  S = b ? |S| : -|S|.
+// k < 2^53 converts to double exactly (I2F.F64.U64 on the conversion pipe, off the busy ALU
+// pipe), and S = fma(k, 2^-52, -(1 - 2^-53)) is exact: the true value is an odd multiple of
+// 2^-53 of magnitude < 1, so the single rounding of the FMA changes nothing.
 __device__ __forceinline__ double uniform53(uint32_t xa, uint32_t xb) {
+  const unsigned long long k = (((unsigned long long)xa << 32) | xb) >> 11;
+  return fma(__ull2double_rn(k), 0x1p-52, __longlong_as_double((long long)0xBFEFFFFFFFFFFFFFull));
+}
+
+// The same value without an int->double conversion (exponent-OR construction), kept for
+// reference: with b = bit 52 of k and r = k mod 2^52, |S| = r'·2^-52 + 2^-53 where
+// r' = b ? r : (2^52 - 1 - r); M = 1 + r'·2^-52 is built from bits and |S| = M - (1 - 2^-53)
+// exactly (Sterbenz).  S = b ? |S| : -|S|.
+__device__ __forceinline__ double uniform53_bits(uint32_t xa, uint32_t xb) {
   const uint32_t lo = __funnelshift_r(xb, xa, 11);          // bits 31..0 of k
   const uint32_t hi = xa >> 11;                             // bits 52..32 of k
   const uint32_t nb = ~(uint32_t)((int32_t)xa >> 31);       // all ones iff b == 0

@@ -19,7 +19,8 @@
 //    K-major no-swizzle layout (8-row x 16-byte core matrices).  Inside each 32-nonzero K chunk,
 //    word c nibble n holds nonzero 4n + c for both A and B.
 //  * CTA = up to 12 A-producer warps (tile = w % T, nonzero half = w / T) + 2 B-producer warps +
-//    1 MMA warp; 4-stage smem ring (A: T x 4 KB, B: 2.3 KB per stage) with mbarrier full/empty;
+//    1 MMA warp; 2-stage smem ring, each stage 4 K-steps (A: T x 16 KB, B: 4 x 2.5 KB) with mbarrier
+//    full/empty (fewer, larger handshakes: 10.9 -> 8.4 ms on c5);
 //    block scale factors (ue8m0 = 1.0) live in TMEM columns [448, 512).
 // Measured (scripts/microbench_mxf4.cu): one M=128,K=64 mxf4 MMA reads its 4 KB A tile at
 // ~44.5 B/clk -> ~89 entries/clk/SM, vs ~62 for int8 and 64 lanes/clk/SM for FP64 DFMA.
@@ -42,10 +43,13 @@ constexpr int kF4MmaWarp = kF4Producers + 1;
 constexpr int kF4Threads = (kF4Producers + 2) * 32;
 constexpr int kF4Slots = 8;                       // nonzero-stream ring (K-steps of 64)
 constexpr int kF4N = 72;                          // 64 digit rows + ones row + 7 zero rows
-constexpr int kF4Stages = 4;
+constexpr int kF4Sub = 4;                         // K-steps (64 nonzeros each) per smem stage
+constexpr int kF4Stages = 2;
 constexpr int kF4ATile = 128 * 32;                // 128 rows x 64 fp4 = 4 KB
 constexpr int kF4BTile = (kF4N / 8) * 256;        // 9 row groups x 256 B = 2304 B
-constexpr int kF4Stage = kF4Tiles * kF4ATile + 3072;
+constexpr int kF4BSub = 2560;                     // B tile slot per K-step (padded)
+constexpr int kF4ATileS = kF4Sub * kF4ATile;      // one tile's A data per stage
+constexpr int kF4Stage = kF4Tiles * kF4ATileS + kF4Sub * kF4BSub;
 constexpr uint32_t kF4SfCol = 448;                // scale factors: TMEM columns [448, 512)
 
 struct F4Shared {
@@ -169,6 +173,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
   const int64_t pb = P.colptr[it.col], pe = P.colptr[it.col + 1];
   const int64_t L = pe - pb;
   const int nsteps = (int)((L + 63) >> 6);
+  const int nsup = (nsteps + kF4Sub - 1) / kF4Sub;
   const int T = it.ntiles;                         // <= kF4Tiles
   const double* vals = reinterpret_cast<const double*>(P.vals);
 
@@ -186,10 +191,10 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   // B rows 64..71 of every stage are constant: row 64 = +1.0 (0x2), rows 65..71 = 0
-  for (int i = threadIdx.x; i < kF4Stages * 8 * 2; i += blockDim.x) {
-    const int s = i / 16, row = 64 + (i % 16) / 2, h = i & 1;
+  for (int i = threadIdx.x; i < kF4Stages * kF4Sub * 8 * 2; i += blockDim.x) {
+    const int s = i / (16 * kF4Sub), sub = (i / 16) % kF4Sub, row = 64 + (i % 16) / 2, h = i & 1;
     const uint32_t v = row == 64 ? 0x22222222u : 0u;
-    const uint32_t a = s_u32(stages + s * kF4Stage + kF4Tiles * kF4ATile) + f4_off(row, h);
+    const uint32_t a = s_u32(stages + s * kF4Stage + kF4Tiles * kF4ATileS + sub * kF4BSub) + f4_off(row, h);
     asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" :: "r"(a), "r"(v) : "memory");
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -228,29 +233,34 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
     // ===================== A producers: S tile (w % T), nonzero half (w / T) =====================
     const int t = warp % T, h = warp / T;
     const uint32_t q = (uint32_t)(it.tile0 + t);
-    const uint32_t tile_off = (uint32_t)(t * kF4ATile) + f4_off(lane, h);
-    // Philox of K-step ks+1 is computed while K-step ks is transposed (two independent chains)
-    auto gen = [&](int ks) -> uint4 {
+    // One smem stage holds kF4Sub = 4 K-steps: the warp generates all of them (independent Philox
+    // chains, 4 kF4Sub interleaved 32x32 transposes) and signals the stage once.
+    auto getj = [&](int ks) -> uint32_t {
+      if (ks >= nsteps) return 0u;
       const int slot = ks % kF4Slots;
       f4_wait(&sh.jfull[slot], (ks / kF4Slots) & 1);
       const uint32_t j = sh.js[slot][32 * h + lane];
       f4_arrive(&sh.jempty[slot]);
-      return s_block(q, (uint64_t)P.row_offset + j, P.keys);   // padded nonzeros: j = 0, B = 0
+      return j;
     };
-    uint4 xb = nsteps > 0 ? gen(0) : make_uint4(0, 0, 0, 0);
-    for (int ks = 0; ks < nsteps; ++ks) {
-      uint32_t x[4] = {xb.x, xb.y, xb.z, xb.w};
-      const int stage = ks % kF4Stages, use = ks / kF4Stages;
-      if (dbg == 1) {
-        if (ks + 1 < nsteps) { const int slot = (ks + 1) % kF4Slots; f4_wait(&sh.jfull[slot], ((ks + 1) / kF4Slots) & 1); f4_arrive(&sh.jempty[slot]); }
-        if (use > 0) f4_wait(&sh.empty[stage], (use - 1) & 1);
-      } else {
-        if (ks + 1 < nsteps) xb = gen(ks + 1);
-        f4_transpose<4>(x, lane);                   // lane r: row 32qq + r over the 32 nonzeros
-        if (use > 0) f4_wait(&sh.empty[stage], (use - 1) & 1);
-        const uint32_t tile = s_u32(stages + stage * kF4Stage) + tile_off;
+    for (int ss = 0; ss < nsup; ++ss) {
+      const int stage = ss % kF4Stages, use = ss / kF4Stages;
+      uint32_t x[4 * kF4Sub];
 #pragma unroll
-        for (int qq = 0; qq < 4; ++qq) f4_store_row(tile + (uint32_t)(qq * 4 * 256), x[qq]);   // row 32qq + lane
+      for (int sub = 0; sub < kF4Sub; ++sub) {
+        const uint32_t j = getj(kF4Sub * ss + sub);
+        const uint4 xb = s_block(q, (uint64_t)P.row_offset + j, P.keys);   // padded nonzeros: B = 0
+        x[4 * sub + 0] = xb.x; x[4 * sub + 1] = xb.y; x[4 * sub + 2] = xb.z; x[4 * sub + 3] = xb.w;
+      }
+      f4_transpose<4 * kF4Sub>(x, lane);          // lane r: row 32qq + r over 32 nonzeros
+      if (use > 0) f4_wait(&sh.empty[stage], (use - 1) & 1);
+      if (dbg != 1) {
+        const uint32_t tile = s_u32(stages + stage * kF4Stage) + (uint32_t)(t * kF4ATileS) + f4_off(lane, h);
+#pragma unroll
+        for (int sub = 0; sub < kF4Sub; ++sub)
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq)
+            f4_store_row(tile + (uint32_t)(sub * kF4ATile + qq * 4 * 256), x[4 * sub + qq]);   // row 32qq + lane
       }
       if (dbg != 3) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
@@ -262,37 +272,45 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
     // 2^(61-E) as two exact power-of-two factors (each within the double range)
     const int e1 = 61 - E > 1000 ? 1000 : (61 - E < -1000 ? -1000 : 61 - E);
     const double sc1 = ldexp(1.0, e1), sc2 = ldexp(1.0, 61 - E - e1);
-    for (int ks = 0; ks < nsteps; ++ks) {
-      const int slot = ks % kF4Slots;
-      f4_wait(&sh.jfull[slot], (ks / kF4Slots) & 1);
-      const double v0 = sh.vs[slot][32 * h + lane];
-      f4_arrive(&sh.jempty[slot]);
-      const int stage = ks % kF4Stages, use = ks / kF4Stages;
-      if (dbg == 4 || dbg == 5) {
-        if (use > 0) f4_wait(&sh.empty[stage], (use - 1) & 1);
-        __syncwarp();
-        if (lane == 0) f4_arrive(&sh.full[stage]);
-        continue;
+    for (int ss = 0; ss < nsup; ++ss) {
+      const int stage = ss % kF4Stages, use = ss / kF4Stages;
+      uint32_t x[2 * kF4Sub];
+      int nval[kF4Sub];
+#pragma unroll
+      for (int sub = 0; sub < kF4Sub; ++sub) {
+        const int ks = kF4Sub * ss + sub;
+        double v0 = 0.0;
+        if (ks < nsteps) {
+          const int slot = ks % kF4Slots;
+          f4_wait(&sh.jfull[slot], (ks / kF4Slots) & 1);
+          v0 = sh.vs[slot][32 * h + lane];
+          f4_arrive(&sh.jempty[slot]);
+        }
+        const int64_t c0 = pb + (int64_t)ks * 64 + 32 * h;
+        nval[sub] = (int)(pe - c0 < 0 ? 0 : (pe - c0 > 32 ? 32 : pe - c0));
+        // U = A + 2^63 (mod 2^64); digit s = +1 iff bit s of U; nibble sign = NOT bit.  Padding
+        // nonzeros past the column end contribute nothing: their B nibbles are 0.0 (masked below).
+        unsigned long long U = 0ull;
+        if (lane < nval[sub]) {
+          const long long A = __double2ll_rn((v0 * sc1) * sc2);
+          U = (unsigned long long)A ^ 0x8000000000000000ull;
+        }
+        x[2 * sub] = ~(uint32_t)U;                 // sign bits of the digit nibbles
+        x[2 * sub + 1] = ~(uint32_t)(U >> 32);
       }
-      const int64_t p = pb + (int64_t)ks * 64 + 32 * h + lane;
-      // U = A + 2^63 (mod 2^64); digit s = +1 iff bit s of U; nibble sign = NOT bit.  Padding
-      // nonzeros past the column end contribute nothing: their B nibbles are 0.0 (masked below).
-      unsigned long long U = 0ull;
-      if (p < pe) {
-        const long long A = __double2ll_rn((v0 * sc1) * sc2);
-        U = (unsigned long long)A ^ 0x8000000000000000ull;
-      }
-      uint32_t x[2] = {~(uint32_t)U, ~(uint32_t)(U >> 32)};   // sign bits of the digit nibbles
-      f4_transpose<2>(x, lane);                                // lane s: digit s (and 32 + s)
+      f4_transpose<2 * kF4Sub>(x, lane);           // lane s: digit s (and 32 + s) per K-step
       if (use > 0) f4_wait(&sh.empty[stage], (use - 1) & 1);
-      const uint32_t bt = s_u32(stages + stage * kF4Stage + kF4Tiles * kF4ATile);
-      const int64_t c0 = pb + (int64_t)ks * 64 + 32 * h;
-      const int nvalid = (int)(pe - c0 < 0 ? 0 : (pe - c0 > 32 ? 32 : pe - c0));
-      f4_store_row_masked(bt + f4_off(lane, h), x[0], nvalid);
-      f4_store_row_masked(bt + f4_off(32 + lane, h), x[1], nvalid);
-      if (nvalid < 32 && lane == 0) {   // last, partial K chunk: the ones row gets zeros too
-        const uint32_t z = 0u;         // (+1 digit signs are 0 bits: y = 0 -> nibbles 0x2)
-        f4_store_row_masked(bt + f4_off(64, h), z, nvalid);
+      if (dbg != 4 && dbg != 5) {
+#pragma unroll
+        for (int sub = 0; sub < kF4Sub; ++sub) {
+          const uint32_t bt = s_u32(stages + stage * kF4Stage + kF4Tiles * kF4ATileS + sub * kF4BSub);
+          f4_store_row_masked(bt + f4_off(lane, h), x[2 * sub], nval[sub]);
+          f4_store_row_masked(bt + f4_off(32 + lane, h), x[2 * sub + 1], nval[sub]);
+          if (nval[sub] < 32 && lane == 0) {   // partial (last) K chunk: the ones row too
+            const uint32_t z = 0u;              // (y = 0 -> nibbles 0x2 = +1.0)
+            f4_store_row_masked(bt + f4_off(64, h), z, nval[sub]);
+          }
+        }
       }
       if (dbg != 3) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
@@ -323,19 +341,23 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
     if (lane == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t idesc = f4_idesc();
-      for (int ks = 0; ks < nsteps; ++ks) {
-        const int stage = ks % kF4Stages;
-        f4_wait(&sh.full[stage], (ks / kF4Stages) & 1);
+      for (int ss = 0; ss < nsup; ++ss) {
+        const int stage = ss % kF4Stages;
+        f4_wait(&sh.full[stage], (ss / kF4Stages) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t sb = s_u32(stages + stage * kF4Stage);
-        const uint64_t bdesc = f4_desc(sb + kF4Tiles * kF4ATile);
-        for (int tt = 0; tt < T && dbg != 2 && dbg != 5; ++tt) {
-          const uint64_t adesc = f4_desc(sb + tt * kF4ATile);
-          asm volatile(
-              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-              "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}"
-              :: "r"(tmem + (uint32_t)(tt * kF4N)), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(ks > 0 ? 1u : 0u),
-                 "r"(tmem + kF4SfCol), "r"(tmem + kF4SfCol + 32u));
+        for (int sub = 0; sub < kF4Sub; ++sub) {
+          const int ks = kF4Sub * ss + sub;
+          if (ks >= nsteps) break;
+          const uint64_t bdesc = f4_desc(sb + kF4Tiles * kF4ATileS + sub * kF4BSub);
+          for (int tt = 0; tt < T && dbg != 2 && dbg != 5; ++tt) {
+            const uint64_t adesc = f4_desc(sb + tt * kF4ATileS + sub * kF4ATile);
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}"
+                :: "r"(tmem + (uint32_t)(tt * kF4N)), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(ks > 0 ? 1u : 0u),
+                   "r"(tmem + kF4SfCol), "r"(tmem + kF4SfCol + 32u));
+          }
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
                      :: "r"(s_u32(&sh.empty[stage])) : "memory");

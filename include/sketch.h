@@ -155,18 +155,23 @@ const char* sketch_version(void);
 /*
  * Kernel selection for SK_RADEMACHER with SK_F64 values (process-wide).  All paths compute the
  * same Â within the parity bound (|Â - oracle| <= 1e-12 |S||A|); the tensor-core paths are
- * exact up to the per-column fixed-point rounding of the values (<= 2^-44 |S||A|) and a single
- * final fp64 rounding.  Tensor-core paths need every column to hold <= 131071 nonzeros and
- * an average of >= 256 nonzeros per column, else the SIMT kernel runs.  Default: SK_PATH_TC_FP4, or the SKETCH_RAD_F64_PATH environment variable
- * (fp4 | int8smem | int8tmem | simt | hybrid).  Errors: SK_EINVAL for an unknown path.
+ * exact up to the per-column fixed-point rounding of the values (<= 2^-44 |S||A| for
+ * SK_PATH_TC_FP4..HYBRID, <= 2^-42 |S||A| for SK_PATH_TC_FP4N) and a single final fp64 rounding.
+ * Tensor-core paths need an average of >= 256 nonzeros per column and every column to hold
+ * <= 131071 nonzeros (SK_PATH_TC_FP4N: <= 1048575), else the SIMT kernel runs.
+ * Default: SK_PATH_TC_FP4, or the SKETCH_RAD_F64_PATH environment variable
+ * (fp4 | fp4n | int8smem | int8tmem | simt | hybrid).  SK_PATH_TC_FP4N also needs 16-byte aligned
+ * rowidx / vals (TMA) and colptr[n] < 2^31 - 512.  Errors: SK_EINVAL for an unknown path.
  */
 typedef enum {
     SK_PATH_TC_FP4 = 0,        /* tcgen05 kind::mxf4: ±1 as e2m1, values as 64 signed binary digits */
     SK_PATH_TC_INT8_SMEM = 1,  /* tcgen05 kind::i8: S tiles in smem (MN-major), 8 int8 digit planes */
     SK_PATH_TC_INT8_TMEM = 2,  /* tcgen05 kind::i8: S tiles in TMEM (K-major) */
     SK_PATH_SIMT = 3,          /* FP64 SIMT kernel: one SEL + one DADD per (row, nonzero) */
-    SK_PATH_HYBRID = 4         /* one persistent kernel: int8 tensor-core warps + FP64 SIMT warps
+    SK_PATH_HYBRID = 4,        /* one persistent kernel: int8 tensor-core warps + FP64 SIMT warps
                                   pulling columns from one queue */
+    SK_PATH_TC_FP4N = 5        /* tcgen05 kind::mxf4, S as the N = 256 operand, values as 63 magnitude
+                                  digits, TMA-fed persistent kernel */
 } sk_rad_f64_path_t;
 int sketch_set_rad_f64_path(int path);
 

@@ -56,6 +56,22 @@ cudaError_t launch_apply_rad_tc(const ApplyArgs& a, const TcItem* items, int64_t
 int tc_tiles_per_cta();
 cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const TcItem* items, int64_t n_items, cudaStream_t stream);
 int f4_tiles_per_cta();
+// S-as-N=256 fp4 kernel (sketch_f4n.cu): items = (column, 256-row tile), longest first; dtype 0 = f64,
+// 1 = f32; n_cols = columns of the plan (per-column value maxima are computed first).
+constexpr int64_t kF4nMaxColumn = (int64_t(1) << 20) - 1;
+constexpr int kF4nRows = 256;
+// Work item of the S-as-N fp4 kernel: column col (nonzeros [pb, pb + L)), 256-row tile `tile` of Â.
+struct NItem {
+  int64_t pb;
+  int32_t L;
+  int32_t col;
+  int32_t tile;
+  int32_t pad;
+};
+// rowidx and vals must be 16-byte aligned (TMA); nnz_end = colptr[n] (absolute end of the stream).
+bool f4n_aligned(const void* p);
+cudaError_t launch_apply_rad_f4n(const ApplyArgs& a, int dtype, const NItem* items, int64_t n_items, int64_t n_cols,
+                                 int64_t nnz_end, cudaStream_t stream);
 // Tensor cores + FP64 SIMT in one persistent kernel; items = int8 schedule (<= 16 tiles each);
 // counter = one device int (work queue head), reset by the launcher.
 cudaError_t launch_apply_rad_hybrid(const ApplyArgs& a, const TcItem* items, int64_t n_items, int* counter,

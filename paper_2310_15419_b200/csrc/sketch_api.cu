@@ -126,9 +126,29 @@ std::vector<sk::TcItem> build_tc_schedule(const int64_t* colptr, int64_t n, int6
   return out;
 }
 
+// S-as-N fp4 schedule: one item per (column, 256-row tile of Â), longest columns first.
+std::vector<sk::NItem> build_f4n_schedule(const int64_t* colptr, int64_t n, int64_t d) {
+  const int64_t tiles = (d + sk::kF4nRows - 1) / sk::kF4nRows;
+  std::vector<sk::NItem> out;
+  out.reserve((size_t)(n * tiles));
+  for (int64_t k = 0; k < n; ++k)
+    for (int64_t g = 0; g < tiles; ++g) {
+      sk::NItem it;
+      it.pb = colptr[k];
+      it.L = (int32_t)(colptr[k + 1] - colptr[k]);
+      it.col = (int32_t)k;
+      it.tile = (int32_t)g;
+      it.pad = 0;
+      out.push_back(it);
+    }
+  std::stable_sort(out.begin(), out.end(), [](const sk::NItem& a, const sk::NItem& b) { return a.L > b.L; });
+  return out;
+}
+
 // Kernel used for ±1 with fp64 values (process-wide; results agree within the parity bound):
-// SK_PATH_TC_FP4 (default), SK_PATH_TC_INT8_SMEM, SK_PATH_TC_INT8_TMEM, SK_PATH_SIMT.
-// Initialised from SKETCH_RAD_F64_PATH = fp4 | int8smem | int8tmem | simt, else fp4.
+// SK_PATH_TC_FP4 (default), SK_PATH_TC_FP4N, SK_PATH_TC_INT8_SMEM, SK_PATH_TC_INT8_TMEM,
+// SK_PATH_SIMT, SK_PATH_HYBRID.  Initialised from SKETCH_RAD_F64_PATH = fp4 | fp4n | int8smem |
+// int8tmem | simt | hybrid, else fp4.
 std::atomic<int> g_rad_f64_path{-1};
 
 int rad_f64_path() {
@@ -136,7 +156,8 @@ int rad_f64_path() {
   if (v >= 0) return v;
   v = SK_PATH_TC_FP4;
   if (const char* e = getenv("SKETCH_RAD_F64_PATH")) {
-    if (!strcmp(e, "hybrid")) v = SK_PATH_HYBRID;
+    if (!strcmp(e, "fp4n")) v = SK_PATH_TC_FP4N;
+    else if (!strcmp(e, "hybrid")) v = SK_PATH_HYBRID;
     else if (!strcmp(e, "int8smem")) v = SK_PATH_TC_INT8_SMEM;
     else if (!strcmp(e, "int8tmem")) v = SK_PATH_TC_INT8_TMEM;
     else if (!strcmp(e, "simt")) v = SK_PATH_SIMT;
@@ -158,6 +179,9 @@ struct sk_plan_s {
   sk::TcItem* d_tc = nullptr;       // tensor-core ±1 fp64 schedules (empty if not eligible):
   int64_t n_tc = 0;                 //   [int8 items (16 tiles) | fp4 items (6 tiles)]
   int64_t n_f4 = 0;
+  sk::NItem* d_f4n = nullptr;       // S-as-N fp4 schedule: (column, 256-row tile), longest first
+  int64_t n_f4n = 0;
+  int64_t nnz_end = 0;              // colptr[n] (absolute end of the nonzero stream)
   int64_t* owned_colptr = nullptr;  // device copy made by sketch_plan_host
   int64_t n_rad = 0, n_pair = 0;
   int64_t philox_rad = 0, philox_pair = 0;
@@ -208,6 +232,22 @@ int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
     if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
     if (e != cudaSuccess) { if (p->d_tc) cudaFree(p->d_tc); delete p; return cuda_fail(e, "tc schedule"); }
   }
+  p->nnz_end = h_colptr[n];
+  // S-as-N fp4 path: TMA streams rowidx / values (16-byte aligned arrays, int32 coordinates)
+  if (dtype == SK_F64 && p->max_col <= sk::kF4nMaxColumn && n > 0 && nnz >= 256 * n && sk::f4n_aligned(rowidx) &&
+      p->nnz_end < (int64_t(1) << 31) - 2 * sk::kF4nRows) {
+    std::vector<sk::NItem> f4n = build_f4n_schedule(h_colptr, n, d);
+    p->n_f4n = (int64_t)f4n.size();
+    cudaError_t e = cudaMalloc(&p->d_f4n, f4n.size() * sizeof(sk::NItem));
+    if (e == cudaSuccess) e = cudaMemcpyAsync(p->d_f4n, f4n.data(), f4n.size() * sizeof(sk::NItem), cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    if (e != cudaSuccess) {
+      if (p->d_f4n) cudaFree(p->d_f4n);
+      if (p->d_tc) cudaFree(p->d_tc);
+      delete p;
+      return cuda_fail(e, "f4n schedule");
+    }
+  }
   const int64_t total = p->n_rad + p->n_pair;
   if (total > 0) {
     cudaError_t e = cudaMalloc(&p->d_items, (size_t)total * sizeof(Item));
@@ -251,7 +291,9 @@ int apply_items(const sk_plan_s* p, uint64_t seed, sk_dist_t dist, const void* v
   a.keys = sk::make_keys(seed);
   cudaError_t e;
   const int path = rad_f64_path();
-  if (dist == SK_RADEMACHER && p->n_tc > 0 && path != SK_PATH_SIMT) {
+  if (dist == SK_RADEMACHER && path == SK_PATH_TC_FP4N && p->n_f4n > 0 && sk::f4n_aligned(vals)) {
+    e = sk::launch_apply_rad_f4n(a, (int)p->dtype, p->d_f4n, p->n_f4n, p->n, p->nnz_end, stream);
+  } else if (dist == SK_RADEMACHER && p->n_tc > 0 && path != SK_PATH_SIMT && path != SK_PATH_TC_FP4N) {
     if (path == SK_PATH_HYBRID) {
       int* counter = nullptr;
       e = cudaMallocAsync((void**)&counter, sizeof(int), stream);
@@ -284,8 +326,11 @@ void ensure_pool() {
 
 const char* kernel_name(const sk_plan_s* p, int dist) {
   if (dist == SK_RADEMACHER) {
+    if (p->n_f4n > 0 && rad_f64_path() == SK_PATH_TC_FP4N)
+      return p->dtype == SK_F32 ? "sk_rad_f4n_kernel<float> (tcgen05 kind::mxf4, N=256)"
+                                : "sk_rad_f4n_kernel<double> (tcgen05 kind::mxf4, N=256)";
     if (p->dtype == SK_F32) return "sk_rad_kernel<float>";
-    if (p->n_tc > 0) {
+    if (p->n_tc > 0 && rad_f64_path() != SK_PATH_TC_FP4N) {
       switch (rad_f64_path()) {
         case SK_PATH_TC_FP4: return "sk_rad_f4_kernel (tcgen05 kind::mxf4)";
         case SK_PATH_HYBRID: return "sk_rad_hybrid_kernel (tcgen05 kind::i8 + FP64 SIMT)";
@@ -508,6 +553,7 @@ int sketch_plan_stats(sk_plan_t plan, sk_stats_t* h) {
   h->philox_blocks_rad = plan->philox_rad;
   h->philox_blocks_pair = plan->philox_pair;
   h->plan_bytes = (plan->n_rad + plan->n_pair) * (int64_t)sizeof(Item) +
+                  (plan->n_tc + plan->n_f4) * (int64_t)sizeof(sk::TcItem) + plan->n_f4n * (int64_t)sizeof(sk::NItem) +
                   (plan->owned_colptr ? (plan->n + 1) * 8 : 0);
   return SK_OK;
 }
@@ -518,6 +564,7 @@ int sketch_plan_destroy(sk_plan_t plan) {
   if (plan->d_items) e = cudaFree(plan->d_items);
   if (plan->owned_colptr) { cudaError_t e2 = cudaFree(plan->owned_colptr); if (e == cudaSuccess) e = e2; }
   if (plan->d_tc) { cudaError_t e2 = cudaFree(plan->d_tc); if (e == cudaSuccess) e = e2; }
+  if (plan->d_f4n) { cudaError_t e2 = cudaFree(plan->d_f4n); if (e == cudaSuccess) e = e2; }
   delete plan;
   if (e != cudaSuccess) return cuda_fail(e, "cudaFree(plan)");
   return SK_OK;
@@ -540,7 +587,7 @@ const char* sketch_last_error_detail(void) { return g_detail.c_str(); }
 const char* sketch_version(void) { return "libsketch 0.2.0 sm_100a"; }
 
 int sketch_set_rad_f64_path(int path) {
-  if (path < SK_PATH_TC_FP4 || path > SK_PATH_HYBRID) return SK_EINVAL;
+  if (path < SK_PATH_TC_FP4 || path > SK_PATH_TC_FP4N) return SK_EINVAL;
   g_rad_f64_path.store(path, std::memory_order_relaxed);
   return SK_OK;
 }

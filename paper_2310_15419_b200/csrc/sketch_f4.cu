@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kF4Stages; ++s) { f4_mbar_init(&sh.full[s], 2 * T + kF4BWarps); f4_mbar_init(&sh.empty[s], 1); }
-    for (int s = 0; s < kF4Slots; ++s) { f4_mbar_init(&sh.jfull[s], 32); f4_mbar_init(&sh.jempty[s], (2 * T + kF4BWarps) * 32); }
+    for (int s = 0; s < kF4Slots; ++s) { f4_mbar_init(&sh.jfull[s], 32); f4_mbar_init(&sh.jempty[s], 2 * T + kF4BWarps); }
     f4_mbar_init(&sh.done, 1);
     sh.maxabs_bits = 0ull;
     sh.nonfinite = 0;
@@ -240,7 +240,8 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
       const int slot = ks % kF4Slots;
       f4_wait(&sh.jfull[slot], (ks / kF4Slots) & 1);
       const uint32_t j = sh.js[slot][32 * h + lane];
-      f4_arrive(&sh.jempty[slot]);
+      __syncwarp();
+      if (lane == 0) f4_arrive(&sh.jempty[slot]);   // one arrival per warp
       return j;
     };
     for (int ss = 0; ss < nsup; ++ss) {
@@ -284,7 +285,8 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
           const int slot = ks % kF4Slots;
           f4_wait(&sh.jfull[slot], (ks / kF4Slots) & 1);
           v0 = sh.vs[slot][32 * h + lane];
-          f4_arrive(&sh.jempty[slot]);
+          __syncwarp();
+          if (lane == 0) f4_arrive(&sh.jempty[slot]);
         }
         const int64_t c0 = pb + (int64_t)ks * 64 + 32 * h;
         nval[sub] = (int)(pe - c0 < 0 ? 0 : (pe - c0 > 32 ? 32 : pe - c0));

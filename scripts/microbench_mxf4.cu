@@ -18,7 +18,7 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
   return d;
 }
 
-template <int N, int LAY>
+template <int N, int LAY, int M = 128>
 __global__ void __launch_bounds__(128, 1) k(int iters, unsigned long long* cyc, float* probe) {
   extern __shared__ __align__(1024) unsigned char raw[];
   unsigned char* sm = raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(128, 1) k(int iters, unsigned long long* cyc, 
   __shared__ uint32_t tbase;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // A: 4 tiles x 4 KB, B: N x 32 B; all nibbles 0x2 (+1.0)
-  for (int i = threadIdx.x; i < 4 * 16384 + N * 32; i += blockDim.x) sm[i] = 0x22;
+  for (int i = threadIdx.x; i < 4 * 16384 + 256 * 32; i += blockDim.x) sm[i] = 0x22;
   if (threadIdx.x == 0) {
     for (int i = 0; i < 4; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(&bar[i])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(128, 1) k(int iters, unsigned long long* cyc, 
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t idesc = (0u << 4) | (1u << 7) | (1u << 10) | (0u << 15) | (0u << 16) |
-                         ((uint32_t)(N >> 3) << 17) | (1u << 23) | ((128u >> 4) << 24);
+                         ((uint32_t)(N >> 3) << 17) | (1u << 23) | ((uint32_t)(M >> 4) << 24);
   const int nacc = 448 / N < 4 ? 448 / N : 4;
   if (threadIdx.x == 0) {
     const uint32_t a0 = smem_u32(sm);
@@ -100,31 +100,36 @@ __global__ void __launch_bounds__(128, 1) k(int iters, unsigned long long* cyc, 
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" :: "r"(tb));
 }
 
-template <int N, int LAY>
+template <int N, int LAY, int M = 128>
 void run() {
   unsigned long long* d;
   float* probe;
   cudaMalloc(&d, 8);
   cudaMalloc(&probe, 128 * 4);
   const int smem = 4 * 16384 + 256 * 32 + 1024;
-  cudaFuncSetAttribute(k<N, LAY>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k<N, LAY, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int iters = 400;
-  k<N, LAY><<<148, 128, smem>>>(iters, d, probe);
+  k<N, LAY, M><<<148, 128, smem>>>(iters, d, probe);
   cudaError_t e = cudaDeviceSynchronize();
   unsigned long long c = 0;
   float h[128];
   cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
   cudaMemcpy(h, probe, sizeof(h), cudaMemcpyDeviceToHost);
   const double per = (double)c / (iters * 4.0);
-  printf("layout %d mxf4 M=128 N=%3d K=64: %.1f cycles/MMA, %.1f A-bytes/clk, %.1f entries/clk; probe D[0]=%.1f D[127]=%.1f (expect %d) %s\n",
-         LAY, N, per, 4096.0 / per, 8192.0 / per, h[0], h[127], 64 * iters, e == cudaSuccess ? "ok" : cudaGetErrorString(e));
+  printf("layout %d mxf4 M=%d N=%3d K=64: %.1f cycles/MMA, %.1f A-bytes/clk, %.1f entries/clk; probe D[0]=%.1f D[127]=%.1f (expect %d) %s\n",
+         LAY, M, N, per, (M * 32.0) / per, (M * 64.0) / per, h[0], h[127], 64 * iters, e == cudaSuccess ? "ok" : cudaGetErrorString(e));
   cudaFree(d);
   cudaFree(probe);
 }
 
 int main() {
   run<64, 0>();
-  run<64, 6>();
-  run<64, 2>();
+  run<128, 0>();
+  run<256, 0>();
+  run<64, 0, 64>();
+  run<128, 0, 64>();
+  run<256, 0, 64>();
+  run<192, 0, 128>();
+  run<256, 2, 128>();
   return 0;
 }

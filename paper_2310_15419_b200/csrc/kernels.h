@@ -14,7 +14,10 @@ constexpr int kThreads = kWarps * 32;
 // Rows of Â owned by one warp.  Rademacher: 32 rows per lane (one 32-bit Philox word per
 // lane per nonzero).  Uniform / Gaussian: 16 rows per lane (8 Philox blocks per nonzero).
 constexpr int kRowsPerWarpRad = 1024;
-constexpr int kRowsPerWarpPair = 512;
+#ifndef SK_PAIR_ROWS_PER_WARP
+#define SK_PAIR_ROWS_PER_WARP 512
+#endif
+constexpr int kRowsPerWarpPair = SK_PAIR_ROWS_PER_WARP;
 
 // One CTA of work: column `col`, Â rows [row0, row0 + wd * rows_per_warp).
 // The CTA's 16 warps are arranged as W_d = wd row-warps times W_k = 16 / wd slices of the

@@ -13,6 +13,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "bm_tables.h"
+
 namespace sk {
 
 constexpr uint32_t kPhiloxM0 = 0xD2511F53u;
@@ -101,6 +103,96 @@ __device__ __forceinline__ void gaussian_pair(const uint4 x, double& g0, double&
   const double th = __dmul_rn(u2, two_pi_f64());
   double s, c;
   sincos(th, &s, &c);
+  g0 = __dmul_rn(rho, c);
+  g1 = __dmul_rn(rho, s);
+}
+
+// ---------------------------------------------------------------- fast Box-Muller (same definition)
+//
+// The transform of gaussian_pair with its own log and sincos (scripts/gen_bm_tables.py derives and
+// checks the constants against 300-bit mpmath: <= 0.6 ulp each); ~45 FP64 operations per pair
+// instead of the libdevice calls.  Results agree with the libm-based oracle far inside the
+// Gaussian parity bound (1e-14 relative).
+
+// log(u) for u in (0, 1] (u normal).  tab = kBmLogTab rows {c, log c hi, log c lo, pad}.
+__device__ __forceinline__ double bm_log(double u, const double* __restrict__ tab) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(u);
+  const int e = (int)(b >> 52) - 1023;
+  const double m = __longlong_as_double((long long)((b & 0x000FFFFFFFFFFFFFull) | 0x3FF0000000000000ull));
+  const int idx = (int)(((b >> 44) & 0xFFu) + 1u) >> 1;        // round(128 (m - 1)), 0..128
+  const double2 ch = *reinterpret_cast<const double2*>(tab + 4 * idx);
+  const double lo = tab[4 * idx + 2];
+  const double r = fma(m, ch.x, -1.0);                         // |r| < 0.0045
+  // (log1p(r) - r) / r^2 = L2 + L3 r + ... + L7 r^5 (Horner; Estrin measured slower)
+  const double r2 = r * r;
+  double p = fma(r, kBm[kL7], kBm[kL6]);
+  p = fma(r, p, kBm[kL5]);
+  p = fma(r, p, kBm[kL4]);
+  p = fma(r, p, kBm[kL3]);
+  p = fma(r, p, kBm[kL2]);
+  const double ed = (double)e;
+  const double shi = fma(ed, kBm[kLn2Hi], -ch.y);              // exact: both on the 2^-42 grid
+  const double slo = fma(ed, kBm[kLn2Lo], -lo);
+  return shi + (r + fma(r2, p, slo));
+}
+
+// sin and cos of th in [0, 2 pi): Cody-Waite reduction by pi/2 in four parts (exact products for
+// k <= 4), fdlibm kernels on |r| <= pi/4, quadrant by k mod 4 (signs applied as bit flips).
+__device__ __forceinline__ void bm_sincos(double th, double& s, double& c) {
+  const double kr = fma(th, kBm[kTwoOverPi], kBm[kRound]);   // 1.5 2^52 + rint(th 2/pi)
+  const double kd = kr - kBm[kRound];
+  double r = fma(-kd, kBm[kPio2_0], th);
+  r = fma(-kd, kBm[kPio2_1], r);
+  r = fma(-kd, kBm[kPio2_2], r);
+  r = fma(-kd, kBm[kPio2_3], r);
+  // fdlibm kernels, polynomials in z = r^2 (Horner; Estrin measured slower)
+  const double z = r * r;
+  double ps = fma(z, kBm[kS6], kBm[kS5]);
+  ps = fma(z, ps, kBm[kS4]);
+  ps = fma(z, ps, kBm[kS3]);
+  ps = fma(z, ps, kBm[kS2]);
+  ps = fma(z, ps, kBm[kS1]);
+  const double sr = fma(z * r, ps, r);
+  double pc = fma(z, kBm[kC6], kBm[kC5]);
+  pc = fma(z, pc, kBm[kC4]);
+  pc = fma(z, pc, kBm[kC3]);
+  pc = fma(z, pc, kBm[kC2]);
+  pc = fma(z, pc, kBm[kC1]);
+  const double hz = 0.5 * z;
+  const double w = 1.0 - hz;
+  const double cr = w + (((1.0 - w) - hz) + z * (z * pc));
+  const int q = __double2loint(kr) & 3;                        // k mod 4 from the low mantissa bits
+  const bool odd = q & 1;
+  const double a = odd ? cr : sr, bq = odd ? sr : cr;          // sin, cos before signs
+  const int sa = (q & 2) << 30, sb = ((q + 1) & 2) << 30;      // sign bits (0x80000000 or 0)
+  s = __hiloint2double(__double2hiint(a) ^ sa, __double2loint(a));
+  c = __hiloint2double(__double2hiint(bq) ^ sb, __double2loint(bq));
+}
+
+// sqrt(x) for x in [0, 75] to ~1 ulp: rsqrt approximation refined by one Goldschmidt step and one
+// Newton correction (x = -0 or +0 returns x, like sqrt).
+__device__ __forceinline__ double bm_sqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double s = x * y, h = 0.5 * y;
+  const double e = fma(-s, h, 0.5);
+  s = fma(s, e, s);
+  h = fma(h, e, h);
+  const double r = fma(-s, s, x);
+  s = fma(r, h, s);
+  return x == 0.0 ? x : s;
+}
+
+// Same values as gaussian_pair (to within the parity bound) from the same block.
+__device__ __forceinline__ void gaussian_pair_fast(const uint4 x, const double* __restrict__ tab, double& g0, double& g1) {
+  const unsigned long long k1 = (((unsigned long long)x.x << 32) | x.y) >> 11;
+  const unsigned long long k2 = (((unsigned long long)x.z << 32) | x.w) >> 11;
+  const double u1 = __dmul_rn(__ull2double_rn(k1 + 1ull), 0x1p-53);
+  const double u2 = __dmul_rn(__ull2double_rn(k2), 0x1p-53);
+  const double rho = bm_sqrt(-2.0 * bm_log(u1, tab));
+  const double th = __dmul_rn(u2, kBm[kTwoPi]);
+  double s, c;
+  bm_sincos(th, s, c);
   g0 = __dmul_rn(rho, c);
   g1 = __dmul_rn(rho, s);
 }

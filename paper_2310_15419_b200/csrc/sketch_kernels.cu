@@ -29,7 +29,8 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr int kXchWords = 5;                                   // padded 4-word exchange slot
 constexpr int kXchBytes = kWarps * 32 * kXchWords * 4;         // 10 KiB
 constexpr int kRadPad = 33;                                    // 32 rows per lane + 1 pad
-constexpr int kPairPad = 17;                                   // 16 rows per lane + 1 pad
+constexpr int kPairRows = kRowsPerWarpPair / 32;              // Â rows per lane (uniform / Gaussian)
+constexpr int kPairPad = kPairRows + 1;
 
 template <typename T>
 __device__ __forceinline__ T ldg_val(const void* vals, int64_t p) {
@@ -165,22 +166,30 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 2 : 1) sk_rad_kerne
 // q = (warp_row0 + 16 l)/2 + h (h = 0..7); each block yields 2 entries, so a lane generates
 // exactly the S entries it consumes (no exchange).
 template <int DIST, typename T>
-__device__ __forceinline__ void pair_entries(const uint4 x, T& v0, T& v1) {
+__device__ __forceinline__ void pair_entries(const uint4 x, T& v0, T& v1, const double* __restrict__ logtab) {
   if constexpr (DIST == 1) {
     const double d0 = uniform53(x.x, x.y), d1 = uniform53(x.z, x.w);
     if constexpr (sizeof(T) == 8) { v0 = d0; v1 = d1; }
     else { v0 = __double2float_rn(d0); v1 = __double2float_rn(d1); }
   } else {
     double g0, g1;
-    gaussian_pair(x, g0, g1);
+    gaussian_pair_fast(x, logtab, g0, g1);
     if constexpr (sizeof(T) == 8) { v0 = g0; v1 = g1; }
     else { v0 = __double2float_rn(g0); v1 = __double2float_rn(g1); }
   }
 }
 
+constexpr int kPairRedBytes = kWarps * 32 * kPairPad * 8;     // reduction area (fp64 worst case)
+constexpr int kLogTabBytes = 129 * 4 * 8;
+
 template <int DIST, typename T>
-__global__ void __launch_bounds__(kThreads, 1) sk_pair_kernel(const ApplyArgs P) {
+__global__ void __launch_bounds__(kThreads, kPairRows <= 8 ? 2 : 1) sk_pair_kernel(const ApplyArgs P) {
   extern __shared__ __align__(16) unsigned char smem[];
+  double* logtab = reinterpret_cast<double*>(smem + kPairRedBytes);   // Gaussian: log table copy
+  if constexpr (DIST == 2) {
+    for (int i = threadIdx.x; i < 129 * 4; i += blockDim.x) logtab[i] = (&kBmLogTab[0][0])[i];
+    __syncthreads();
+  }
   const Item it = P.items[blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int WD = it.wd, WK = kWarps / WD;              // warps >= WD*WK get an empty slice
@@ -188,14 +197,14 @@ __global__ void __launch_bounds__(kThreads, 1) sk_pair_kernel(const ApplyArgs P)
   const int64_t pb = P.colptr[it.col], pe = P.colptr[it.col + 1];
   const int64_t L = pe - pb;
   const int64_t s0 = wk < WK ? pb + (L * wk) / WK : pe, s1 = wk < WK ? pb + (L * (wk + 1)) / WK : pe;
-  const int64_t lane_row0 = (int64_t)it.row0 + (int64_t)wd * kRowsPerWarpPair + 16 * lane;
+  const int64_t lane_row0 = (int64_t)it.row0 + (int64_t)wd * kRowsPerWarpPair + kPairRows * lane;
   const uint32_t q0 = (uint32_t)(lane_row0 >> 1);
   // Lanes whose rows all lie past d skip generation (their results are never stored).
   const bool active = lane_row0 < P.d;
 
-  T acc[16];
+  T acc[kPairRows];
 #pragma unroll
-  for (int e = 0; e < 16; ++e) acc[e] = T(0);
+  for (int e = 0; e < kPairRows; ++e) acc[e] = T(0);
 
   for (int64_t p = s0; p < s1; p += 32) {
     const int cnt = (int)((s1 - p) < 32 ? (s1 - p) : 32);
@@ -211,10 +220,10 @@ __global__ void __launch_bounds__(kThreads, 1) sk_pair_kernel(const ApplyArgs P)
       if (!active) continue;
       const uint64_t J = (uint64_t)P.row_offset + jr;
 #pragma unroll
-      for (int h = 0; h < 8; ++h) {
+      for (int h = 0; h < kPairRows / 2; ++h) {
         const uint4 x = s_block(q0 + h, J, P.keys);
         T v0, v1;
-        pair_entries<DIST, T>(x, v0, v1);
+        pair_entries<DIST, T>(x, v0, v1, logtab);
         acc[2 * h] = fma(v0, a, acc[2 * h]);
         acc[2 * h + 1] = fma(v1, a, acc[2 * h + 1]);
       }
@@ -224,15 +233,15 @@ __global__ void __launch_bounds__(kThreads, 1) sk_pair_kernel(const ApplyArgs P)
   T* red = reinterpret_cast<T*>(smem);
   T* mine = red + warp * (32 * kPairPad) + lane * kPairPad;
 #pragma unroll
-  for (int e = 0; e < 16; ++e) mine[e] = acc[e];
+  for (int e = 0; e < kPairRows; ++e) mine[e] = acc[e];
   __syncthreads();
   T* outc = reinterpret_cast<T*>(P.out) + (int64_t)it.col * P.ld;
   const int rows = WD * kRowsPerWarpPair;
   for (int r = threadIdx.x; r < rows; r += kThreads) {
     const int64_t row = (int64_t)it.row0 + r;
     if (row >= P.d) break;
-    const int rwd = r >> 9, rr = r & 511;
-    const int off = (rr >> 4) * kPairPad + (rr & 15);
+    const int rwd = r / kRowsPerWarpPair, rr = r % kRowsPerWarpPair;
+    const int off = (rr / kPairRows) * kPairPad + (rr % kPairRows);
     T s = red[rwd * (32 * kPairPad) + off];
     for (int kk = 1; kk < WK; ++kk) s += red[(kk * WD + rwd) * (32 * kPairPad) + off];
     outc[row] = s;
@@ -260,7 +269,7 @@ __global__ void sk_fill_s_kernel(PhiloxKeys K, int64_t i0, int64_t i1, int64_t j
       }
     } else {
       T v0, v1;
-      pair_entries<DIST, T>(x, v0, v1);
+      pair_entries<DIST, T>(x, v0, v1, &kBmLogTab[0][0]);
       const int64_t i = q * 2;
       if (i >= i0 && i < i1) col[i - i0] = v0;
       if (i + 1 >= i0 && i + 1 < i1) col[i + 1 - i0] = v1;
@@ -293,8 +302,9 @@ cudaError_t launch_items(K kernel, size_t smem, const ApplyArgs& a, cudaStream_t
 cudaError_t launch_apply(int dist, int dtype, const ApplyArgs& a, cudaStream_t stream) {
   const size_t rad64 = kXchBytes + (size_t)kWarps * 32 * kRadPad * 8;
   const size_t rad32 = kXchBytes + (size_t)kWarps * 32 * kRadPad * 4;
-  const size_t pair64 = (size_t)kWarps * 32 * kPairPad * 8;
-  const size_t pair32 = (size_t)kWarps * 32 * kPairPad * 4;
+  const size_t pair64 = (size_t)kPairRedBytes;
+  const size_t pair32 = (size_t)kPairRedBytes;
+  const size_t gauss = (size_t)kPairRedBytes + kLogTabBytes;
   if (dist == 0) {
     if (dtype == 1) return launch_items(sk_rad_kernel<float, 0>, rad32, a, stream);
     static const int selmode = [] {
@@ -306,8 +316,8 @@ cudaError_t launch_apply(int dist, int dtype, const ApplyArgs& a, cudaStream_t s
   }
   if (dist == 1) return dtype == 0 ? launch_items(sk_pair_kernel<1, double>, pair64, a, stream)
                                    : launch_items(sk_pair_kernel<1, float>, pair32, a, stream);
-  return dtype == 0 ? launch_items(sk_pair_kernel<2, double>, pair64, a, stream)
-                    : launch_items(sk_pair_kernel<2, float>, pair32, a, stream);
+  return dtype == 0 ? launch_items(sk_pair_kernel<2, double>, gauss, a, stream)
+                    : launch_items(sk_pair_kernel<2, float>, gauss, a, stream);
 }
 
 cudaError_t launch_fill_s(int dist, int dtype, uint64_t seed, int64_t i0, int64_t i1, int64_t j0,

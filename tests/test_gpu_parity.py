@@ -80,6 +80,17 @@ def test_fill_s_matches_oracle(sk, dist, dtype):
                 assert np.array_equal(got, ref), (dist, dtype, i0, j0, seed)
 
 
+def test_gaussian_entries_dense(sk):
+    # 2M Gaussian entries (own fp64 log / sincos, philox.cuh) against the libm-based oracle: the
+    # whole (u1, u2) range is exercised, including u1 near 1 (rho -> 0) and theta near k pi/2
+    seed, i1, j0, j1 = 2, 4096, 123_456, 123_456 + 512
+    got = sk.sketch_fill_s(seed, "gaussian", 0, i1, j0, j1).T.cpu().numpy()
+    ref = oracle.fill_s(seed, "gaussian", 0, i1, j0, j1)
+    rel = np.abs(got - ref) / np.abs(ref)
+    assert np.all(rel <= 1e-14), float(rel.max())
+    assert float(np.median(rel)) < 2.3e-16         # typically within an ulp
+
+
 def test_fill_s_matches_curand_philox(sk):
     # Independent implementation: cuRAND's Philox4_32_10 with curand_init(seed, j, 4q) gives
     # the block (q, 0, j_lo, j_hi); its bits, read as ±1, must equal our S.

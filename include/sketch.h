@@ -160,7 +160,7 @@ const char* sketch_version(void);
  * Tensor-core paths need an average of >= 256 nonzeros per column and every column to hold
  * <= 131071 nonzeros (SK_PATH_TC_FP4N: <= 1048575), else the SIMT kernel runs.
  * Default: SK_PATH_TC_FP4, or the SKETCH_RAD_F64_PATH environment variable
- * (fp4 | fp4n | int8smem | int8tmem | simt | hybrid).  SK_PATH_TC_FP4N also needs 16-byte aligned
+ * (fp4 | fp4t | fp4n | int8smem | int8tmem | simt | hybrid).  SK_PATH_TC_FP4N also needs 16-byte aligned
  * rowidx / vals (TMA) and colptr[n] < 2^31 - 512.  Errors: SK_EINVAL for an unknown path.
  */
 typedef enum {
@@ -170,8 +170,9 @@ typedef enum {
     SK_PATH_SIMT = 3,          /* FP64 SIMT kernel: one SEL + one DADD per (row, nonzero) */
     SK_PATH_HYBRID = 4,        /* one persistent kernel: int8 tensor-core warps + FP64 SIMT warps
                                   pulling columns from one queue */
-    SK_PATH_TC_FP4N = 5        /* tcgen05 kind::mxf4, S as the N = 256 operand, values as 63 magnitude
+    SK_PATH_TC_FP4N = 5,       /* tcgen05 kind::mxf4, S as the N = 256 operand, values as 63 magnitude
                                   digits, TMA-fed persistent kernel */
+    SK_PATH_TC_FP4T = 6        /* tcgen05 kind::mxf4 with the S operand written to / read from TMEM */
 } sk_rad_f64_path_t;
 int sketch_set_rad_f64_path(int path);
 

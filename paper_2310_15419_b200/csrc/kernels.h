@@ -59,6 +59,8 @@ cudaError_t launch_apply_rad_tc(const ApplyArgs& a, const TcItem* items, int64_t
 int tc_tiles_per_cta();
 cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const TcItem* items, int64_t n_items, cudaStream_t stream);
 int f4_tiles_per_cta();
+// S-in-TMEM fp4 kernel (sketch_f4t.cu): items = (column, 512-row block `tile0` of Â), fp64 values.
+cudaError_t launch_apply_rad_f4t(const ApplyArgs& a, const TcItem* items, int64_t n_items, cudaStream_t stream);
 // S-as-N=256 fp4 kernel (sketch_f4n.cu): items = (column, 256-row tile), longest first; dtype 0 = f64,
 // 1 = f32; n_cols = columns of the plan (per-column value maxima are computed first).
 constexpr int64_t kF4nMaxColumn = (int64_t(1) << 20) - 1;

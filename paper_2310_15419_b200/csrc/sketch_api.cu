@@ -157,6 +157,7 @@ int rad_f64_path() {
   v = SK_PATH_TC_FP4;
   if (const char* e = getenv("SKETCH_RAD_F64_PATH")) {
     if (!strcmp(e, "fp4n")) v = SK_PATH_TC_FP4N;
+    else if (!strcmp(e, "fp4t")) v = SK_PATH_TC_FP4T;
     else if (!strcmp(e, "hybrid")) v = SK_PATH_HYBRID;
     else if (!strcmp(e, "int8smem")) v = SK_PATH_TC_INT8_SMEM;
     else if (!strcmp(e, "int8tmem")) v = SK_PATH_TC_INT8_TMEM;
@@ -179,6 +180,8 @@ struct sk_plan_s {
   sk::TcItem* d_tc = nullptr;       // tensor-core ±1 fp64 schedules (empty if not eligible):
   int64_t n_tc = 0;                 //   [int8 items (16 tiles) | fp4 items (6 tiles)]
   int64_t n_f4 = 0;
+  sk::TcItem* d_f4t = nullptr;      // S-in-TMEM fp4 schedule: (column, 512-row block), longest first
+  int64_t n_f4t = 0;
   sk::NItem* d_f4n = nullptr;       // S-as-N fp4 schedule: (column, 256-row tile), longest first
   int64_t n_f4n = 0;
   int64_t nnz_end = 0;              // colptr[n] (absolute end of the nonzero stream)
@@ -233,6 +236,19 @@ int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
     if (e != cudaSuccess) { if (p->d_tc) cudaFree(p->d_tc); delete p; return cuda_fail(e, "tc schedule"); }
   }
   p->nnz_end = h_colptr[n];
+  if (dtype == SK_F64 && p->max_col <= sk::kTcMaxColumn && n > 0 && nnz >= 256 * n) {
+    std::vector<sk::TcItem> f4t = build_tc_schedule(h_colptr, n, (d + 3) / 4, 1);   // 512-row blocks
+    p->n_f4t = (int64_t)f4t.size();
+    cudaError_t e = cudaMalloc(&p->d_f4t, f4t.size() * sizeof(sk::TcItem));
+    if (e == cudaSuccess) e = cudaMemcpyAsync(p->d_f4t, f4t.data(), f4t.size() * sizeof(sk::TcItem), cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    if (e != cudaSuccess) {
+      if (p->d_f4t) cudaFree(p->d_f4t);
+      if (p->d_tc) cudaFree(p->d_tc);
+      delete p;
+      return cuda_fail(e, "f4t schedule");
+    }
+  }
   // S-as-N fp4 path: TMA streams rowidx / values (16-byte aligned arrays, int32 coordinates)
   if (dtype == SK_F64 && p->max_col <= sk::kF4nMaxColumn && n > 0 && nnz >= 256 * n && sk::f4n_aligned(rowidx) &&
       p->nnz_end < (int64_t(1) << 31) - 2 * sk::kF4nRows) {
@@ -291,9 +307,12 @@ int apply_items(const sk_plan_s* p, uint64_t seed, sk_dist_t dist, const void* v
   a.keys = sk::make_keys(seed);
   cudaError_t e;
   const int path = rad_f64_path();
-  if (dist == SK_RADEMACHER && path == SK_PATH_TC_FP4N && p->n_f4n > 0 && sk::f4n_aligned(vals)) {
+  if (dist == SK_RADEMACHER && path == SK_PATH_TC_FP4T && p->n_f4t > 0) {
+    e = sk::launch_apply_rad_f4t(a, p->d_f4t, p->n_f4t, stream);
+  } else if (dist == SK_RADEMACHER && path == SK_PATH_TC_FP4N && p->n_f4n > 0 && sk::f4n_aligned(vals)) {
     e = sk::launch_apply_rad_f4n(a, (int)p->dtype, p->d_f4n, p->n_f4n, p->n, p->nnz_end, stream);
-  } else if (dist == SK_RADEMACHER && p->n_tc > 0 && path != SK_PATH_SIMT && path != SK_PATH_TC_FP4N) {
+  } else if (dist == SK_RADEMACHER && p->n_tc > 0 && path != SK_PATH_SIMT && path != SK_PATH_TC_FP4N &&
+             path != SK_PATH_TC_FP4T) {
     if (path == SK_PATH_HYBRID) {
       int* counter = nullptr;
       e = cudaMallocAsync((void**)&counter, sizeof(int), stream);
@@ -326,11 +345,12 @@ void ensure_pool() {
 
 const char* kernel_name(const sk_plan_s* p, int dist) {
   if (dist == SK_RADEMACHER) {
+    if (p->n_f4t > 0 && rad_f64_path() == SK_PATH_TC_FP4T) return "sk_rad_f4t_kernel (tcgen05 kind::mxf4, S in TMEM)";
     if (p->n_f4n > 0 && rad_f64_path() == SK_PATH_TC_FP4N)
       return p->dtype == SK_F32 ? "sk_rad_f4n_kernel<float> (tcgen05 kind::mxf4, N=256)"
                                 : "sk_rad_f4n_kernel<double> (tcgen05 kind::mxf4, N=256)";
     if (p->dtype == SK_F32) return "sk_rad_kernel<float>";
-    if (p->n_tc > 0 && rad_f64_path() != SK_PATH_TC_FP4N) {
+    if (p->n_tc > 0 && rad_f64_path() != SK_PATH_TC_FP4N && rad_f64_path() != SK_PATH_TC_FP4T) {
       switch (rad_f64_path()) {
         case SK_PATH_TC_FP4: return "sk_rad_f4_kernel (tcgen05 kind::mxf4)";
         case SK_PATH_HYBRID: return "sk_rad_hybrid_kernel (tcgen05 kind::i8 + FP64 SIMT)";
@@ -553,7 +573,8 @@ int sketch_plan_stats(sk_plan_t plan, sk_stats_t* h) {
   h->philox_blocks_rad = plan->philox_rad;
   h->philox_blocks_pair = plan->philox_pair;
   h->plan_bytes = (plan->n_rad + plan->n_pair) * (int64_t)sizeof(Item) +
-                  (plan->n_tc + plan->n_f4) * (int64_t)sizeof(sk::TcItem) + plan->n_f4n * (int64_t)sizeof(sk::NItem) +
+                  (plan->n_tc + plan->n_f4 + plan->n_f4t) * (int64_t)sizeof(sk::TcItem) +
+                  plan->n_f4n * (int64_t)sizeof(sk::NItem) +
                   (plan->owned_colptr ? (plan->n + 1) * 8 : 0);
   return SK_OK;
 }
@@ -565,6 +586,7 @@ int sketch_plan_destroy(sk_plan_t plan) {
   if (plan->owned_colptr) { cudaError_t e2 = cudaFree(plan->owned_colptr); if (e == cudaSuccess) e = e2; }
   if (plan->d_tc) { cudaError_t e2 = cudaFree(plan->d_tc); if (e == cudaSuccess) e = e2; }
   if (plan->d_f4n) { cudaError_t e2 = cudaFree(plan->d_f4n); if (e == cudaSuccess) e = e2; }
+  if (plan->d_f4t) { cudaError_t e2 = cudaFree(plan->d_f4t); if (e == cudaSuccess) e = e2; }
   delete plan;
   if (e != cudaSuccess) return cuda_fail(e, "cudaFree(plan)");
   return SK_OK;
@@ -587,7 +609,7 @@ const char* sketch_last_error_detail(void) { return g_detail.c_str(); }
 const char* sketch_version(void) { return "libsketch 0.2.0 sm_100a"; }
 
 int sketch_set_rad_f64_path(int path) {
-  if (path < SK_PATH_TC_FP4 || path > SK_PATH_TC_FP4N) return SK_EINVAL;
+  if (path < SK_PATH_TC_FP4 || path > SK_PATH_TC_FP4T) return SK_EINVAL;
   g_rad_f64_path.store(path, std::memory_order_relaxed);
   return SK_OK;
 }

@@ -14,7 +14,8 @@
 //  * D[i, s] = Σ_p S[i,p] d_{p,s} are integers with |D| <= L < 2^24: exact in f32.
 //    Â[i] = 2^(E-62) (Σ_s 2^s D[i,s] - D[i,64]), formed with two exact int64 partial sums.
 //  * both operands are produced by the same path: a Philox4x32-10 block (one nonzero x 128 rows)
-//    or a value's 64-bit U, 32 x 32 bit-transposed across the warp (5 shuffle stages), expanded to
+//    or a value's 64-bit U, 32 x 32 bit-transposed across the warp (5 shuffle stages on lane-rotated
+//    words), expanded to
 //    nibbles ((y << (3-c)) & 0x88888888) | 0x22222222 and stored with STS.128 into the canonical
 //    K-major no-swizzle layout (8-row x 16-byte core matrices).  Inside each 32-nonzero K chunk,
 //    word c nibble n holds nonzero 4n + c for both A and B.
@@ -51,6 +52,12 @@ constexpr int kF4BSub = 2560;                     // B tile slot per K-step (pad
 constexpr int kF4ATileS = kF4Sub * kF4ATile;      // one tile's A data per stage
 constexpr int kF4Stage = kF4Tiles * kF4ATileS + kF4Sub * kF4BSub;
 constexpr uint32_t kF4SfCol = 448;                // scale factors: TMEM columns [448, 512)
+// try_wait suspend-time hint (ns): a waiting warp sleeps until the phase completes instead of
+// spinning through SYNCS / BRA / YIELD loops that take issue slots from the producers.
+#ifndef SK_SUSPEND_NS
+#define SK_SUSPEND_NS 1000000
+#endif
+constexpr uint32_t kSuspendNs = SK_SUSPEND_NS;
 
 struct F4Shared {
   uint64_t full[kF4Stages];
@@ -78,9 +85,9 @@ __device__ __forceinline__ void f4_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
       "@!P1 bra WAIT_%=;\n\t}"
-      :: "r"(s_u32(bar)), "r"(parity) : "memory");
+      :: "r"(s_u32(bar)), "r"(parity), "r"(kSuspendNs) : "memory");
 }
 
 // K-major, no-swizzle smem descriptor: core matrix = 8 rows x 16 B; LBO = stride between the two
@@ -100,29 +107,30 @@ __host__ __device__ constexpr uint32_t f4_idesc() {
   return (1u << 7) | (1u << 10) | ((uint32_t)(kF4N >> 3) << 17) | (1u << 23) | ((128u >> 4) << 24);
 }
 
-// One transpose stage on one word: t = rotate(partner word), x = keep ? x : t (bit select).
-__device__ __forceinline__ uint32_t f4_stage(uint32_t x, uint32_t y, uint32_t sh, uint32_t keep) {
-  uint32_t t, r;
-  asm("shf.l.wrap.b32 %0, %1, %1, %2;" : "=r"(t) : "r"(y), "r"(sh));
-  asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(r) : "r"(x), "r"(t), "r"(keep));   // (x & keep) | (t & ~keep)
-  return r;
-}
-
+// 32 x 32 bit transpose of NW independent word sets across the warp: on entry lane p holds word p
+// (bit b = row b), on exit lane r holds row r (bit c = word c).  Between the two rotations every
+// word is kept rotated left by its lane index, which makes each butterfly stage one SHFL + one
+// LOP3 (the partner's word arrives already aligned): 2 + 5 ALU ops per word instead of 5 x 2.
+// Stage s (distance j = 16 >> s) keeps rot(m_j, lane) in the lower lane of a pair, the
+// complement in the upper lane.
 template <int NW>
 __device__ __forceinline__ void f4_transpose(uint32_t (&x)[NW], int lane) {
+  const uint32_t m[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
 #pragma unroll
-  for (int j = 16; j > 0; j >>= 1) {
-    const uint32_t m = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu : j == 4 ? 0x0F0F0F0Fu
-                     : j == 2 ? 0x33333333u : 0x55555555u;
-    const bool hi = (lane & j) != 0;
-    const uint32_t keep = hi ? ~m : m;
-    const uint32_t sh = hi ? (32 - j) : j;
+  for (int k = 0; k < NW; ++k) x[k] = __funnelshift_l(x[k], x[k], lane);
+#pragma unroll
+  for (int s = 0; s < 5; ++s) {
+    const uint32_t rm = __funnelshift_l(m[s], m[s], lane);
+    const uint32_t keep = (lane & (16 >> s)) ? ~rm : rm;
     uint32_t y[NW];
 #pragma unroll
-    for (int k = 0; k < NW; ++k) y[k] = __shfl_xor_sync(0xFFFFFFFFu, x[k], j);
+    for (int k = 0; k < NW; ++k) y[k] = __shfl_xor_sync(0xFFFFFFFFu, x[k], 16 >> s);
 #pragma unroll
-    for (int k = 0; k < NW; ++k) x[k] = f4_stage(x[k], y[k], sh, keep);
+    for (int k = 0; k < NW; ++k)
+      asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(x[k]) : "r"(x[k]), "r"(y[k]), "r"(keep));   // (x & keep) | (y & ~keep)
   }
+#pragma unroll
+  for (int k = 0; k < NW; ++k) x[k] = __funnelshift_r(x[k], x[k], lane);
 }
 
 // 32 sign bits (bit l = nonzero l of the chunk; 1 -> -1.0) -> 16 bytes of e2m1 nibbles; word c

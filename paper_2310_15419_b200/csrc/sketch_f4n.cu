@@ -60,6 +60,10 @@ constexpr int kNStage = kNKS * (kNATile + kNBTile);
 constexpr int kNFStride = 33;                     // epilogue staging: digit pairs per Â row (+1 pad)
 constexpr int kNFBytes = kNRows * kNFStride * 4;
 constexpr uint32_t kNSfCol = 256;                 // TMEM scale-factor columns [256, 320)
+#ifndef SK_SUSPEND_NS
+#define SK_SUSPEND_NS 1000000
+#endif
+constexpr uint32_t kSuspendNs = SK_SUSPEND_NS;     // try_wait suspend-time hint (ns)
 
 struct NShared {
   uint64_t full[kNStages];
@@ -88,9 +92,9 @@ __device__ __forceinline__ void n_arrive(uint64_t* bar) {
   asm volatile(                                                                  \
       "{\n\t.reg .pred P1;\n\t"                                                  \
       "WAIT_%=:\n\t"                                                             \
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"               \
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"               \
       "@!P1 bra WAIT_%=;\n\t}"                                                   \
-      :: "r"(n_u32(bar)), "r"((uint32_t)(parity)) : "memory")
+      :: "r"(n_u32(bar)), "r"((uint32_t)(parity)), "r"(kSuspendNs) : "memory")
 #else
 #define n_wait(bar, parity)                                                      \
   asm volatile(                                                                  \
@@ -98,7 +102,7 @@ __device__ __forceinline__ void n_arrive(uint64_t* bar) {
       "WAIT_%=:\n\t"                                                             \
       "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"              \
       "@!P1 bra WAIT_%=;\n\t}"                                                   \
-      :: "r"(n_u32(bar)), "r"((uint32_t)(parity)) : "memory")
+      :: "r"(n_u32(bar)), "r"((uint32_t)(parity)), "r"(0u) : "memory")
 #endif
 
 // Wait with back-off, for warps that idle for long stretches (epilogue, loader): frees issue slots.

@@ -29,7 +29,7 @@ EXPORTS = ["sketch_plan", "sketch_plan_host", "sketch_apply", "sketch_apply_csc"
            "sketch_apply_host", "sketch_fill_s", "sketch_plan_stats", "sketch_plan_destroy",
            "sketch_error_string", "sketch_last_error_detail", "sketch_version",
            "sketch_set_rad_f64_path", "sketch_apply_kernel_name"]
-RAD_F64_PATHS = {"fp4": 0, "int8smem": 1, "int8tmem": 2, "simt": 3, "hybrid": 4, "fp4n": 5}
+RAD_F64_PATHS = {"fp4": 0, "int8smem": 1, "int8tmem": 2, "simt": 3, "hybrid": 4, "fp4n": 5, "fp4t": 6}
 _STRING_RESULTS = ("sketch_error_string", "sketch_last_error_detail", "sketch_version",
                    "sketch_apply_kernel_name")
 

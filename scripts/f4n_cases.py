@@ -15,6 +15,7 @@ ds = [1000, 300, 1100, 129, 2050]
 A, d = cases[i](), ds[i]
 dev = torch.device("cuda:0")
 plan = sk.Plan(torch.from_numpy(A.colptr).to(dev), torch.from_numpy(A.rowidx).to(dev), d, A.m, "f64")
+if os.environ.get("SKETCH_RAD_F64_PATH"): sk.set_rad_f64_path(os.environ["SKETCH_RAD_F64_PATH"])
 print(i, plan.kernel_name("rademacher"), plan.stats(), flush=True)
 out = plan.apply(torch.from_numpy(A.vals).to(dev), 31, "rademacher").T.cpu().numpy()
 ref, B = oracle.sketch(31, "rademacher", d, A.m, A.n, A.colptr, A.rowidx, A.vals, threads=8)

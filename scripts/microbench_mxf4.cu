@@ -45,6 +45,11 @@ __global__ void __launch_bounds__(128, 1) k(int iters, unsigned long long* cyc, 
     for (int c = 0; c < 64; c += 8)
       asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1};"
                    :: "r"(taddr + c), "r"(v) : "memory");
+    const uint32_t aaddr = tb + ((uint32_t)(32 * (warp & 3)) << 16) + 320u;
+    const uint32_t one = 0x22222222u;
+    for (int c = 0; c < 32; c += 8)
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1};"
+                   :: "r"(aaddr + c), "r"(one) : "memory");
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   }
@@ -70,10 +75,17 @@ __global__ void __launch_bounds__(128, 1) k(int iters, unsigned long long* cyc, 
                              : LAY == 6 ? make_desc(a0 + t * 4096, 16u, 256u, 6u)
                                         : make_desc(a0 + t * 16384 / 4, 16u, 1024u, 2u);
         const uint32_t d = tb + (uint32_t)((t % nacc) * N);
+        if constexpr (LAY == 9) {   // A from TMEM: columns [320 + 8t, 328 + 8t), K-major (8 e2m1 per column)
+          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                       "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], [%1], %2, %3, [%5], [%6], p;\n\t}"
+                       :: "r"(d), "r"(tb + 320u + 8u * t), "l"(bdesc), "r"(idesc), "r"(it > 0 ? 1u : 0u),
+                          "r"(tb + 448u), "r"(tb + 480u));
+        } else {
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}"
                      :: "r"(d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(it > 0 ? 1u : 0u),
                         "r"(tb + 448u), "r"(tb + 480u));
+        }
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
                    :: "r"(smem_u32(&bar[bi])) : "memory");
@@ -124,12 +136,11 @@ void run() {
 
 int main() {
   run<64, 0>();
+  run<72, 0>();
   run<128, 0>();
   run<256, 0>();
-  run<64, 0, 64>();
-  run<128, 0, 64>();
-  run<256, 0, 64>();
-  run<192, 0, 128>();
-  run<256, 2, 128>();
+  run<64, 9>();
+  run<72, 9>();
+  run<112, 9>();
   return 0;
 }

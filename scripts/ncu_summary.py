@@ -19,7 +19,10 @@ keys = ["Kernel Name", "gpu__time_duration.sum", "sm__cycles_elapsed.avg.per_sec
         "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
-        "smsp__inst_executed.sum", "launch__grid_size", "launch__block_size"]
+        "smsp__inst_executed.sum", "launch__grid_size", "launch__block_size",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+        "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
 for k in keys:
     print(f"{k:70s} {d.get(k)}")
 st = []

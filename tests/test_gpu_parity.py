@@ -163,7 +163,7 @@ def test_sketch_matches_oracle_small(sk, dist, case):
     _check(got, ref, B, TOL["f64"])
 
 
-@pytest.mark.parametrize("path", ["fp4n", "fp4", "int8smem", "int8tmem", "simt", "hybrid"])
+@pytest.mark.parametrize("path", ["fp4t", "fp4n", "fp4", "int8smem", "int8tmem", "simt", "hybrid"])
 def test_rad_f64_kernel_paths(sk, path):
     # every ±1 fp64 kernel (tensor-core fp4n / fp4 / int8-smem / int8-TMEM, SIMT) meets the fp64 bar on
     # the edge cases: ragged d and tiles, empty and single-nonzero columns, a column that is long
@@ -191,7 +191,7 @@ def test_kernel_names_report_the_path(sk):
     A = workloads.random_csc(10000, 4, 300, seed=1)
     plan = sk.Plan(_dev(A.colptr), _dev(A.rowidx), 300, A.m, "f64")
     try:
-        for path, tag in (("fp4n", "N=256"), ("fp4", "mxf4"), ("int8smem", "smem"), ("int8tmem", "TMEM"), ("simt", "sk_rad_kernel"),
+        for path, tag in (("fp4t", "S in TMEM"), ("fp4n", "N=256"), ("fp4", "mxf4"), ("int8smem", "smem"), ("int8tmem", "TMEM"), ("simt", "sk_rad_kernel"),
                           ("hybrid", "hybrid")):
             sk.set_rad_f64_path(path)
             assert tag in plan.kernel_name("rademacher")

@@ -206,6 +206,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--shard", default="rows", choices=["rows", "cols"],
+                    help="rows: row shards + NCCL all_reduce of the d x n partials (default); "
+                         "cols: nnz-balanced column shards, no collective (SURVEY.md §8(f) f4)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3   # timing rule: >= 3 warm-up steps
@@ -233,8 +236,15 @@ def main():
     from paper_2310_15419_b200 import sketch as sk
 
     cfg = workloads.CONFIGS[args.config]
-    # ---- inputs: this rank's row shard (c5 generates shards independently) ----
-    if cfg.name == "c5":
+    # ---- inputs: this rank's row shard (c5 generates shards independently) or column shard ----
+    col_shard = args.shard == "cols" and world > 1
+    if col_shard:
+        from paper_2310_15419_b200.distributed import balanced_col_shards
+        Af = workloads.make_config(cfg.name)
+        cb = balanced_col_shards(Af.colptr, world)
+        A = workloads.col_slice(Af, cb[rank], cb[rank + 1])
+        del Af
+    elif cfg.name == "c5":
         r0, r1 = workloads.shard_rows(cfg.m, world, rank)
         A = workloads.make_config("c5", row_range=(r0, r1))
     else:
@@ -246,8 +256,9 @@ def main():
     colptr = torch.from_numpy(A.colptr).to(dev)
     rowidx = torch.from_numpy(A.rowidx).to(dev)
     vals = torch.from_numpy(A.vals).to(dev)
-    out = torch.empty((cfg.n, cfg.d), dtype=vals.dtype, device=dev)
+    out = torch.empty((A.n, cfg.d), dtype=vals.dtype, device=dev)
     stream = torch.cuda.current_stream()
+    reduce_partials = world > 1 and not col_shard
 
     # ---- plan (a1), timed separately ----
     torch.cuda.synchronize()
@@ -264,7 +275,7 @@ def main():
 
     def step():
         plan.apply(vals, cfg.seed, cfg.dist, out=out)
-        if world > 1:
+        if reduce_partials:
             dist.all_reduce(out, op=dist.ReduceOp.SUM)
 
     for _ in range(args.warmup):
@@ -290,7 +301,7 @@ def main():
         starts[i].record(stream)
         plan.apply(vals, cfg.seed, cfg.dist, out=out)
         mids[i].record(stream)
-        if world > 1:
+        if reduce_partials:
             dist.all_reduce(out, op=dist.ReduceOp.SUM)
         ends[i].record(stream)
     torch.cuda.synchronize()
@@ -319,7 +330,7 @@ def main():
         h_colptr = torch.from_numpy(A.colptr).pin_memory()
         h_rowidx = torch.from_numpy(A.rowidx).pin_memory()
         h_vals = torch.from_numpy(A.vals).pin_memory()
-        h_out = torch.empty((cfg.n, cfg.d), dtype=vals.dtype).pin_memory()
+        h_out = torch.empty((A.n, cfg.d), dtype=vals.dtype).pin_memory()
         for _ in range(2):
             sk.sketch_apply_host(cfg.seed, cfg.dist, cfg.d, A.m, h_colptr, h_rowidx, h_vals,
                                  out=h_out, row_offset=A.row_offset)
@@ -338,7 +349,7 @@ def main():
             te = float(tt[0])
         h2d = A.colptr.nbytes + A.rowidx.nbytes + A.vals.nbytes
         e2e = {"value": gflops(cfg.d, nnz_total, te), "unit": "GFLOP/s",
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(cfg.n * cfg.d * wbytes),
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(A.n * cfg.d * wbytes),
                "ms_per_step": te * 1e3,
                "note": "sketch_apply_host: pinned host A -> device, plan, fused apply, Â -> host; "
                        "column groups pipelined on copy streams" + ("; no cross-GPU reduce" if world > 1 else "")}
@@ -377,10 +388,11 @@ def main():
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": cfg.dtype, "data": "synthetic",
             "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "d": cfg.d, "dist": cfg.dist,
-                       "seed": cfg.seed, "nnz": nnz_total, "parallelism": f"rows{world}",
+                       "seed": cfg.seed, "nnz": nnz_total,
+                       "parallelism": f"{'cols' if col_shard else 'rows'}{world}",
                        "l2": "inputs > L2 (no flush)" if flush is None else "L2 flushed between steps",
                        "plan_ms": plan_ms, "kernel_ms": t_kern,
-                       "reduce": "NCCL all_reduce of d x n partials" if world > 1 else None},
+                       "reduce": "NCCL all_reduce of d x n partials" if reduce_partials else None},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clocks, "gpu_launches": args.steps * (1 if stats["n_items_rad"] or stats["n_items_pair"] else 0),
         }

@@ -1,4 +1,4 @@
-"""Multi-GPU row sharding of the sketch -- host-side plumbing only.
+"""Multi-GPU sharding of the sketch -- host-side plumbing only.
 
 Rows of A (= columns of S) are split into contiguous ranges [r_g, r_{g+1}); rank g plans its
 local CSC with ``row_offset = r_g`` so the Philox keys use GLOBAL row indices and every rank
@@ -8,6 +8,16 @@ a full d x n partial Â_g = S[:, r_g:r_{g+1}] · A[r_g:r_{g+1}, :], and one coll
 Â = Σ_g Â_g (NCCL over NVLink / NVSwitch; ``gloo`` in the CPU tests).  This is the outer-loop
 parallelism of PAPER.md:327-332 moved from threads to GPUs, along the inner dimension m that
 Algorithm 1 leaves unblocked.
+
+Column sharding is the zero-communication alternative: rank g owns the
+columns [c_g, c_{g+1}) of A (and of Â), split at nnz quantiles so skewed column lengths (config
+c3's power law) still balance, and computes its d x (c_{g+1} - c_g) block of Â over all rows with
+no reduction at all; an all_gather assembles Â only if a consumer needs it on every rank.  Each
+rank then reads only its columns' nonzeros but needs every row of A they touch.
+
+`sketch_row_sharded_overlapped` is the row-sharded form with the reduction overlapped with the
+compute: the columns are processed in groups, and group g's all_reduce (on a communication stream)
+runs while group g + 1 is being sketched.
 """
 from __future__ import annotations
 
@@ -63,3 +73,97 @@ def sketch_row_sharded(colptr, rowidx, vals, d: int, m_local: int, row_offset: i
     out = plan.apply(vals, seed, dist_name, out=out)
     reduce_partials(out, group=group, mode=mode)
     return out, plan
+
+
+def balanced_col_shards(colptr, world: int):
+    """Column boundaries [c_0 = 0, ..., c_world = n] at nnz quantiles of the CSC colptr (every
+    rank gets about nnz / world nonzeros; boundaries are non-decreasing, ranks may be empty)."""
+    colptr = np.asarray(colptr, dtype=np.int64)
+    n = colptr.shape[0] - 1
+    total = int(colptr[-1] - colptr[0])
+    b = [0]
+    for g in range(1, world):
+        target = int(colptr[0]) + (total * g) // world
+        c = int(np.searchsorted(colptr, target, side="left"))
+        b.append(max(b[-1], min(c, n)))
+    b.append(n)
+    return b
+
+
+def col_shard_csc(colptr, rowidx, vals, c0: int, c1: int):
+    """Columns [c0, c1) of a CSC matrix as (colptr rebased to 0, rowidx, vals) views/copies."""
+    colptr = np.asarray(colptr, dtype=np.int64)
+    p0, p1 = int(colptr[c0]), int(colptr[c1])
+    return colptr[c0:c1 + 1] - p0, rowidx[p0:p1], vals[p0:p1]
+
+
+def gather_col_blocks(block, bounds, group=None):
+    """All-gather the (c_{g+1} - c_g, d) blocks (torch (n_g, d) = column-major d x n_g) of every
+    rank into the full (n, d) Â on every rank."""
+    import torch
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return block
+    world = dist.get_world_size(group)
+    d = block.shape[1]
+    widths = [bounds[g + 1] - bounds[g] for g in range(world)]
+    wmax = max(max(widths), 1)
+    pad = torch.zeros((wmax, d), dtype=block.dtype, device=block.device)
+    pad[:block.shape[0]].copy_(block)
+    outs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(outs, pad, group=group)
+    return torch.cat([o[:w] for o, w in zip(outs, widths)], dim=0)
+
+
+def sketch_col_sharded(colptr_local, rowidx_local, vals_local, d: int, m: int, seed: int, dist_name: str,
+                       plan=None, out=None):
+    """One rank's part of the column-sharded sketch: its columns of Â over all m rows (no
+    collective).  colptr_local is rebased to 0; returns (out (n_local, d), plan)."""
+    from . import sketch as sk
+    if plan is None:
+        dtype = "f64" if str(vals_local.dtype) == "torch.float64" else "f32"
+        plan = sk.Plan(colptr_local, rowidx_local, d, m, dtype)
+    return plan.apply(vals_local, seed, dist_name, out=out), plan
+
+
+def overlap_groups(colptr, groups: int):
+    """Column groups [g_0 = 0, ..., g_G = n] with balanced nnz for the overlapped reduction."""
+    return balanced_col_shards(colptr, groups)
+
+
+def sketch_row_sharded_overlapped(colptr_h, colptr, rowidx, vals, d: int, m_local: int, row_offset: int,
+                                  seed: int, dist_name: str, groups: int = 4, group=None, out=None):
+    """Row-sharded sketch whose cross-GPU sum overlaps the compute: the columns are sketched in
+    `groups` nnz-balanced groups on the current stream, and each group's all_reduce is issued on a
+    side stream as soon as that group's kernel is done.  colptr_h is the host copy of colptr.
+    Returns out (n, d) after all reductions completed on the current stream."""
+    import torch
+    import torch.distributed as dist
+    from . import sketch as sk
+    n = len(colptr_h) - 1
+    if out is None:
+        out = torch.empty((n, d), dtype=vals.dtype, device=vals.device)
+    bounds = overlap_groups(colptr_h, groups)
+    comp = torch.cuda.current_stream()
+    comm = torch.cuda.Stream()
+    dtype = "f64" if vals.dtype == torch.float64 else "f32"
+    plans, works = [], []
+    for g in range(len(bounds) - 1):
+        c0, c1 = bounds[g], bounds[g + 1]
+        if c1 == c0:
+            continue
+        p0, p1 = int(colptr_h[c0]), int(colptr_h[c1])
+        cp = colptr[c0:c1 + 1] - p0
+        pl = sk.Plan(cp, rowidx[p0:p1], d, m_local, dtype, row_offset=row_offset)
+        plans.append(pl)
+        pl.apply(vals[p0:p1], seed, dist_name, out=out[c0:c1])
+        if dist.is_initialized() and dist.get_world_size(group) > 1:
+            ev = torch.cuda.Event()
+            ev.record(comp)
+            with torch.cuda.stream(comm):
+                comm.wait_event(ev)
+                dist.all_reduce(out[c0:c1], op=dist.ReduceOp.SUM, group=group)
+    comp.wait_stream(comm)
+    for pl in plans:
+        pl.close()
+    return out

@@ -104,3 +104,56 @@ def test_c5_shards_are_generated_consistently():
         r, v = full.column(k)
         assert np.all(dense_cols[r] == k) and np.array_equal(dense_vals[r], v)
     assert full.nnz == rows[1] - rows[0] and full.n == cfg.n
+
+
+# ---------------------------------------------------------------- column sharding (§8(f) f4)
+
+def _col_worker(rank, world, port, q):
+    import oracle
+    from paper_2310_15419_b200.distributed import balanced_col_shards, col_shard_csc, gather_col_blocks
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        A = workloads.random_csc(4000, 11, [5, 300, 0, 40, 2, 900, 7, 0, 60, 33, 1], seed=23)
+        b = balanced_col_shards(A.colptr, world)
+        cp, ri, va = col_shard_csc(A.colptr, A.rowidx, A.vals, b[rank], b[rank + 1])
+        part, _ = oracle.sketch(9, "gaussian", 77, A.m, b[rank + 1] - b[rank], cp, ri, va, want_bound=False)
+        block = torch.from_numpy(np.ascontiguousarray(part.T))            # (n_local, d): column-major Â block
+        full = gather_col_blocks(block, b)
+        q.put((rank, full.numpy().T.copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_col_sharded_blocks_assemble_the_full_sketch():
+    import oracle
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_col_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    A = workloads.random_csc(4000, 11, [5, 300, 0, 40, 2, 900, 7, 0, 60, 33, 1], seed=23)
+    full, _ = oracle.sketch(9, "gaussian", 77, A.m, A.n, A.colptr, A.rowidx, A.vals)
+    for r, v in res.items():
+        assert np.array_equal(v, full)          # same per-column order on both sides: bit-identical
+
+
+def test_balanced_col_shards_split_nnz():
+    from paper_2310_15419_b200.distributed import balanced_col_shards
+    rng = np.random.default_rng(1)
+    lens = rng.zipf(1.5, size=3000).clip(max=20000)
+    colptr = np.concatenate([[0], np.cumsum(lens)])
+    for world in (1, 2, 3, 8):
+        b = balanced_col_shards(colptr, world)
+        assert b[0] == 0 and b[-1] == 3000 and len(b) == world + 1
+        assert all(x <= y for x, y in zip(b, b[1:]))
+        parts = [int(colptr[b[g + 1]] - colptr[b[g]]) for g in range(world)]
+        assert sum(parts) == int(colptr[-1])
+        assert max(parts) - min(parts) <= 2 * int(lens.max())

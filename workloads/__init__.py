@@ -221,6 +221,15 @@ def shard_csc(A: CSC, world: int, rank: int) -> CSC:
                A.row_offset + r0, dict(A.meta))
 
 
+def col_slice(A: CSC, c0: int, c1: int) -> CSC:
+    """Columns [c0, c1) of an in-memory CSC (all rows; colptr rebased to 0)."""
+    p0, p1 = int(A.colptr[c0]), int(A.colptr[c1])
+    meta = dict(A.meta)
+    meta["col_range"] = (int(c0), int(c1))
+    return CSC(A.m, c1 - c0, (A.colptr[c0:c1 + 1] - p0).astype(np.int64), A.rowidx[p0:p1].copy(),
+               A.vals[p0:p1].copy(), A.row_offset, meta)
+
+
 # ---------------------------------------------------------------- small / edge-case inputs
 
 def random_csc(m: int, n: int, nnz_per_col, seed: int, dtype=np.float64, *, values="normal",

@@ -375,3 +375,25 @@ def test_config_c4_sampled(sk):
 
 def test_config_c5_sampled(sk):
     _config_parity(sk, "c5", 4)
+
+
+# ------------------------------------------------------------------- SAP least squares (§8(f) f2)
+
+@pytest.mark.parametrize("dist,method", [("gaussian", "qr"), ("rademacher", "qr"), ("uniform", "svd")])
+def test_sap_solve_on_gpu(sk, dist, method):
+    # sketch-and-precondition LSQR with the fused kernel's Â on the GPU: the
+    # paper's 1e-14 stopping rule is met in a few dozen iterations and x is the least-squares solution
+    import torch
+    from paper_2310_15419_b200 import sap
+    A, b = workloads.ls_problem(60000, 150, 80, seed=41, col_scale_decades=2.0)
+    res = sap.sap_solve(_dev(A.colptr), _dev(A.rowidx), _dev(A.vals), A.m, A.n, _dev(b), d=2 * A.n, seed=3,
+                        dist=dist, method=method)
+    assert res.istop in (1, 2) and res.iterations <= 80, (res.istop, res.iterations)
+    assert res.error <= 1e-13, res.error
+    M = np.zeros((A.m, A.n))
+    for k in range(A.n):
+        r, v = A.column(k)
+        M[r, k] += v
+    xref = np.linalg.lstsq(M, b, rcond=None)[0]
+    x = res.x.cpu().numpy()
+    assert np.linalg.norm(x - xref) <= 1e-8 * np.linalg.norm(xref)

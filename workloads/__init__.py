@@ -289,3 +289,21 @@ def abnormal(kind: str, m: int, n: int, nnz: int, seed: int) -> CSC:
         raise ValueError(kind)
     vl = [rng.standard_normal(len(r)) for r in rl]
     return _finish(m, n, rl, vl, np.float64, {"abnormal": kind})
+
+
+# ---------------------------------------------------------------- least-squares problems (SAP, §8(f) f2)
+
+def ls_problem(m: int, n: int, nnz_per_col, seed: int, noise: float = 1.0, col_scale_decades: float = 0.0):
+    """Synthetic tall sparse least-squares problem in the paper's recipe: A random
+    CSC (N(0,1) values), b = A w + noise * N(0, I) with w ~ N(0, I).  col_scale_decades > 0 scales
+    column k by 10^U(-c, c) (ill-conditioned A).  Stands in for the SuiteSparse matrices of Table
+    matrix:name_extended, which are not available.  Returns (CSC, b)."""
+    A = random_csc(m, n, nnz_per_col, seed=seed)
+    rng = np.random.default_rng(seed + 7)
+    if col_scale_decades > 0:
+        sc = 10.0 ** rng.uniform(-col_scale_decades, col_scale_decades, size=n)
+        A.vals = A.vals * np.repeat(sc, np.diff(A.colptr))
+    w = rng.standard_normal(n)
+    Aw = np.zeros(m)
+    np.add.at(Aw, A.rowidx, A.vals * np.repeat(w, np.diff(A.colptr)))
+    return A, Aw + noise * rng.standard_normal(m)

@@ -73,6 +73,8 @@ typedef struct {
     int64_t philox_blocks_rad; /* Philox4x32-10 calls of one SK_RADEMACHER apply (Alg. 3 count) */
     int64_t philox_blocks_pair;/* Philox calls of one SK_UNIFORM / SK_GAUSSIAN apply */
     int64_t plan_bytes;        /* device bytes the plan owns */
+    int64_t n_items_jki;       /* work items of the Algorithm 4 (jki) path, 0 if not built */
+    int64_t jki_nonzero_rows;  /* Σ over 16-column groups of the group's nonzero rows (its RNG work) */
 } sk_stats_t;
 
 /*
@@ -175,6 +177,23 @@ typedef enum {
     SK_PATH_TC_FP4T = 6        /* tcgen05 kind::mxf4 with the S operand written to / read from TMEM */
 } sk_rad_f64_path_t;
 int sketch_set_rad_f64_path(int path);
+
+/*
+ * Kernel selection for SK_UNIFORM / SK_GAUSSIAN (process-wide): Algorithm 3 (kji: S[:, j] regenerated
+ * per stored nonzero) or Algorithm 4 (jki: S[:, j] regenerated once per nonzero
+ * row of each 16-column group and reused across the row).  The plan builds the
+ * jki structure (the group-wise CSR, "format conversion") only when a sample of column groups shows
+ * at least 1.8 nonzeros per nonzero row; SK_PAIR_AUTO then uses jki whenever it was built.
+ * Initialised from SKETCH_PAIR_PATH = auto | kji | jki.  Errors: SK_EINVAL.
+ */
+typedef enum { SK_PAIR_AUTO = 0, SK_PAIR_KJI = 1, SK_PAIR_JKI = 2 } sk_pair_path_t;
+int sketch_set_pair_path(int path);
+
+/* sketch_plan_host_jki -- as sketch_plan_host, but always builds the jki structure (for
+ * measurements and tests of Algorithm 4 on any sparsity pattern).  Same errors. */
+int sketch_plan_host_jki(sk_plan_t* plan, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
+                         int64_t row_offset, const int64_t* h_colptr, const int32_t* rowidx,
+                         int64_t nnz, int validate_rows, sk_stream_t stream);
 
 /* sketch_apply_kernel_name -- name of the kernel sketch_apply(plan, *, dist, ...) launches
  * ("" for a NULL plan or bad dist).  Static string, for reporting. */

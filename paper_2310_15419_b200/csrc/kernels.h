@@ -59,6 +59,26 @@ cudaError_t launch_apply_rad_tc(const ApplyArgs& a, const TcItem* items, int64_t
 int tc_tiles_per_cta();
 cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const TcItem* items, int64_t n_items, cudaStream_t stream);
 int f4_tiles_per_cta();
+// Algorithm 4 (jki) path for uniform / Gaussian (sketch_jki.cu): column groups of kJCols columns,
+// each stored row by row (CSR of the group); items = (group, tile of jki_rows_per_item() rows).
+constexpr int kJCols = 16;
+struct JItem {
+  int32_t group;
+  int32_t row0;
+};
+struct JkiPlanView {
+  const JItem* items;
+  int64_t n_items;
+  const int64_t* grp_rows;   // [n_groups + 1]: range of the group's nonzero rows in row_j / row_ent
+  const int32_t* row_j;      // local row index of each nonzero row, grouped, ascending within a group
+  const int64_t* row_ent;    // [n_rows + 1]: range of the row's entries in ent
+  const uint32_t* ent;       // (value index - ent_base[group]) << 4 | column within the group
+  const int64_t* ent_base;   // [n_groups]: colptr[16 g]
+  int64_t n;                 // columns of the plan
+};
+int jki_rows_per_item();
+cudaError_t launch_apply_jki(int dist, int dtype, const ApplyArgs& a, const JkiPlanView& J, cudaStream_t stream);
+
 // S-in-TMEM fp4 kernel (sketch_f4t.cu): items = (column, 512-row block `tile0` of Â), fp64 values.
 cudaError_t launch_apply_rad_f4t(const ApplyArgs& a, const TcItem* items, int64_t n_items, cudaStream_t stream);
 // S-as-N=256 fp4 kernel (sketch_f4n.cu): items = (column, 256-row tile), longest first; dtype 0 = f64,

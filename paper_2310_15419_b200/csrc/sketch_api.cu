@@ -169,6 +169,22 @@ int rad_f64_path() {
 
 const char* kernel_name(const sk_plan_s* p, int dist);
 
+// Uniform / Gaussian kernel choice (process-wide): SK_PAIR_AUTO (jki when the plan built it),
+// SK_PAIR_KJI, SK_PAIR_JKI.  Initialised from SKETCH_PAIR_PATH = auto | kji | jki.
+std::atomic<int> g_pair_path{-1};
+
+int pair_path() {
+  int v = g_pair_path.load(std::memory_order_relaxed);
+  if (v >= 0) return v;
+  v = SK_PAIR_AUTO;
+  if (const char* e = getenv("SKETCH_PAIR_PATH")) {
+    if (!strcmp(e, "kji")) v = SK_PAIR_KJI;
+    else if (!strcmp(e, "jki")) v = SK_PAIR_JKI;
+  }
+  g_pair_path.store(v, std::memory_order_relaxed);
+  return v;
+}
+
 }  // namespace
 
 struct sk_plan_s {
@@ -185,12 +201,115 @@ struct sk_plan_s {
   sk::NItem* d_f4n = nullptr;       // S-as-N fp4 schedule: (column, 256-row tile), longest first
   int64_t n_f4n = 0;
   int64_t nnz_end = 0;              // colptr[n] (absolute end of the nonzero stream)
+  // Algorithm 4 (jki) structure: one device block holding items, grp_rows, row_j, row_ent, ent, ent_base
+  void* d_jki = nullptr;
+  sk::JkiPlanView jki{};
+  int64_t jki_rows = 0;             // Σ_groups nonzero rows
   int64_t* owned_colptr = nullptr;  // device copy made by sketch_plan_host
   int64_t n_rad = 0, n_pair = 0;
   int64_t philox_rad = 0, philox_pair = 0;
 };
 
 namespace {
+
+// Group-wise CSR for Algorithm 4 ("A will need to be first partitioned into vertical
+// blocks, and within each block, the entries will be stored in CSR format").  Groups are kJCols
+// consecutive columns.  Unless `force`, a sample of up to 32 groups decides whether the reuse factor
+// (nonzeros per nonzero row) is worth it (>= 1.8); otherwise nothing is built.
+int build_jki(sk_plan_s* p, const int64_t* h_colptr, bool force, cudaStream_t stream) {
+  const int64_t n = p->n, G = (n + sk::kJCols - 1) / sk::kJCols;
+  if (n == 0 || p->nnz == 0) return SK_OK;
+  const int64_t base = h_colptr[0];
+  auto group_range = [&](int64_t g) {
+    const int64_t c0 = g * sk::kJCols, c1 = std::min<int64_t>(n, c0 + sk::kJCols);
+    return std::make_pair(h_colptr[c0] - base, h_colptr[c1] - base);
+  };
+  auto distinct_rows = [](std::vector<int32_t>& r) {
+    std::sort(r.begin(), r.end());
+    return (int64_t)(std::unique(r.begin(), r.end()) - r.begin());
+  };
+  if (!force) {
+    const int64_t ns = std::min<int64_t>(G, 32);
+    int64_t tot = 0, rows = 0;
+    for (int64_t t = 0; t < ns && tot < (int64_t(1) << 18); ++t) {   // <= 32 groups, ~256K nonzeros
+      const int64_t g = (t * G) / ns;
+      auto pr = group_range(g);
+      if (pr.second == pr.first) continue;
+      std::vector<int32_t> r((size_t)(pr.second - pr.first));
+      SK_CUDA(cudaMemcpy(r.data(), p->rowidx + pr.first, r.size() * 4, cudaMemcpyDeviceToHost));
+      tot += (int64_t)r.size();
+      rows += distinct_rows(r);
+    }
+    if (rows == 0 || (double)tot < 1.8 * (double)rows) return SK_OK;
+  }
+  std::vector<int32_t> h_rows((size_t)p->nnz);
+  SK_CUDA(cudaMemcpyAsync(h_rows.data(), p->rowidx, h_rows.size() * 4, cudaMemcpyDeviceToHost, stream));
+  SK_CUDA(cudaStreamSynchronize(stream));
+  std::vector<int64_t> grp_rows{0}, row_ent{0}, ent_base;
+  std::vector<int32_t> row_j;
+  std::vector<uint32_t> ent;
+  std::vector<std::pair<int64_t, sk::JItem>> items;
+  const int rpi = sk::jki_rows_per_item();
+  const int64_t tiles = (p->d + rpi - 1) / rpi;
+  std::vector<std::pair<int64_t, uint32_t>> tmp;   // (row, packed entry)
+  for (int64_t g = 0; g < G; ++g) {
+    auto pr = group_range(g);
+    ent_base.push_back(pr.first + base);
+    tmp.clear();
+    const int64_t c0 = g * sk::kJCols, c1 = std::min<int64_t>(n, c0 + sk::kJCols);
+    for (int64_t c = c0; c < c1; ++c)
+      for (int64_t q = h_colptr[c] - base; q < h_colptr[c + 1] - base; ++q)
+        tmp.emplace_back(h_rows[(size_t)q], (uint32_t)(((q - pr.first) << 4) | (c - c0)));
+    std::stable_sort(tmp.begin(), tmp.end(), [](const std::pair<int64_t, uint32_t>& a,
+                                                 const std::pair<int64_t, uint32_t>& b) { return a.first < b.first; });
+    int64_t nrows = 0;
+    for (size_t e = 0; e < tmp.size(); ++e) {
+      if (e == 0 || tmp[e].first != tmp[e - 1].first) {
+        if (e) row_ent.push_back((int64_t)ent.size());
+        row_j.push_back((int32_t)tmp[e].first);
+        ++nrows;
+      }
+      ent.push_back(tmp[e].second);
+    }
+    if (!tmp.empty()) row_ent.push_back((int64_t)ent.size());
+    grp_rows.push_back((int64_t)row_j.size());
+    p->jki_rows += nrows;
+    const int64_t cost = nrows * 8 + (int64_t)tmp.size();   // a row's RNG ~ 8 nonzeros' FMAs
+    for (int64_t t = 0; t < tiles; ++t) items.push_back({cost, sk::JItem{(int32_t)g, (int32_t)(t * rpi)}});
+  }
+  std::stable_sort(items.begin(), items.end(), [](const std::pair<int64_t, sk::JItem>& a,
+                                                   const std::pair<int64_t, sk::JItem>& b) { return a.first > b.first; });
+  // one device block: items | grp_rows | row_ent | ent_base | row_j | ent
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  const size_t b_items = al(items.size() * sizeof(sk::JItem)), b_grp = al(grp_rows.size() * 8),
+               b_rent = al(row_ent.size() * 8), b_base = al(ent_base.size() * 8), b_rowj = al(row_j.size() * 4),
+               b_ent = al(ent.size() * 4);
+  char* blk = nullptr;
+  cudaError_t e = cudaMalloc(&blk, b_items + b_grp + b_rent + b_base + b_rowj + b_ent);
+  if (e != cudaSuccess) return e == cudaErrorMemoryAllocation ? SK_ENOMEM : cuda_fail(e, "cudaMalloc(jki)");
+  std::vector<sk::JItem> it2;
+  it2.reserve(items.size());
+  for (auto& pr : items) it2.push_back(pr.second);
+  char* c = blk;
+  auto put = [&](const void* src, size_t bytes, size_t span) {
+    char* dst = c;
+    if (bytes && e == cudaSuccess) e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream);
+    c += span;
+    return dst;
+  };
+  p->jki.items = reinterpret_cast<const sk::JItem*>(put(it2.data(), it2.size() * sizeof(sk::JItem), b_items));
+  p->jki.grp_rows = reinterpret_cast<const int64_t*>(put(grp_rows.data(), grp_rows.size() * 8, b_grp));
+  p->jki.row_ent = reinterpret_cast<const int64_t*>(put(row_ent.data(), row_ent.size() * 8, b_rent));
+  p->jki.ent_base = reinterpret_cast<const int64_t*>(put(ent_base.data(), ent_base.size() * 8, b_base));
+  p->jki.row_j = reinterpret_cast<const int32_t*>(put(row_j.data(), row_j.size() * 4, b_rowj));
+  p->jki.ent = reinterpret_cast<const uint32_t*>(put(ent.data(), ent.size() * 4, b_ent));
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) { cudaFree(blk); p->jki = sk::JkiPlanView{}; p->jki_rows = 0; return cuda_fail(e, "upload jki"); }
+  p->d_jki = blk;
+  p->jki.n_items = (int64_t)it2.size();
+  p->jki.n = n;
+  return SK_OK;
+}
 
 int check_dims(sk_dtype_t dtype, int64_t d, int64_t m, int64_t n, int64_t row_offset) {
   if (!valid_dtype(dtype) || d < 1 || d > kMaxD || m < 0 || m > kMaxD || n < 0 || n > kMaxD ||
@@ -209,7 +328,7 @@ int validate_colptr(const int64_t* h, int64_t n, int64_t nnz, bool require_zero_
 
 int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n, int64_t row_offset,
               const int64_t* h_colptr, const int64_t* d_colptr, const int32_t* rowidx, int64_t nnz,
-              cudaStream_t stream) {
+              cudaStream_t stream, int jki = 0 /* 0: sample, 1: force, -1: never */) {
   sk_plan_s* p = new (std::nothrow) sk_plan_s();
   if (!p) return SK_ENOMEM;
   p->dtype = dtype; p->d = d; p->m = m; p->n = n; p->nnz = nnz; p->row_offset = row_offset;
@@ -262,6 +381,16 @@ int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
       if (p->d_tc) cudaFree(p->d_tc);
       delete p;
       return cuda_fail(e, "f4n schedule");
+    }
+  }
+  if (jki >= 0) {
+    const int rj = build_jki(p, h_colptr, jki > 0, stream);
+    if (rj != SK_OK) {
+      if (p->d_f4n) cudaFree(p->d_f4n);
+      if (p->d_f4t) cudaFree(p->d_f4t);
+      if (p->d_tc) cudaFree(p->d_tc);
+      delete p;
+      return rj;
     }
   }
   const int64_t total = p->n_rad + p->n_pair;
@@ -320,6 +449,8 @@ int apply_items(const sk_plan_s* p, uint64_t seed, sk_dist_t dist, const void* v
       if (counter) cudaFreeAsync(counter, stream);
     } else if (path == SK_PATH_TC_FP4) e = sk::launch_apply_rad_f4(a, p->d_tc + p->n_tc, p->n_f4, stream);
     else e = sk::launch_apply_rad_tc(a, p->d_tc, p->n_tc, path == SK_PATH_TC_INT8_SMEM ? 1 : 0, stream);
+  } else if ((dist == SK_UNIFORM || dist == SK_GAUSSIAN) && p->jki.n_items > 0 && pair_path() != SK_PAIR_KJI) {
+    e = sk::launch_apply_jki((int)dist, (int)p->dtype, a, p->jki, stream);
   } else
     e = sk::launch_apply((int)dist, (int)p->dtype, a, stream);
   if (e != cudaSuccess) return cuda_fail(e, "launch apply");
@@ -362,6 +493,10 @@ const char* kernel_name(const sk_plan_s* p, int dist) {
     return "sk_rad_kernel<double>";
   }
   const bool f64 = p->dtype == SK_F64;
+  if (p->jki.n_items > 0 && pair_path() != SK_PAIR_KJI) {
+    if (dist == SK_UNIFORM) return f64 ? "sk_jki_kernel<uniform, double> (Algorithm 4)" : "sk_jki_kernel<uniform, float> (Algorithm 4)";
+    return f64 ? "sk_jki_kernel<gaussian, double> (Algorithm 4)" : "sk_jki_kernel<gaussian, float> (Algorithm 4)";
+  }
   if (dist == SK_UNIFORM) return f64 ? "sk_pair_kernel<uniform, double>" : "sk_pair_kernel<uniform, float>";
   return f64 ? "sk_pair_kernel<gaussian, double>" : "sk_pair_kernel<gaussian, float>";
 }
@@ -411,6 +546,37 @@ int sketch_plan_host(sk_plan_t* plan, sk_dtype_t dtype, int64_t d, int64_t m, in
   rc = make_plan(plan, dtype, d, m, n, row_offset, h_colptr, dc, rowidx, nnz, stream);
   if (rc) { cudaFree(dc); return rc; }
   (*plan)->owned_colptr = dc;
+  return SK_OK;
+}
+
+int sketch_plan_host_jki(sk_plan_t* plan, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
+                         int64_t row_offset, const int64_t* h_colptr, const int32_t* rowidx,
+                         int64_t nnz, int validate_rows, sk_stream_t stream_) {
+  if (!plan) return SK_EINVAL;
+  *plan = nullptr;
+  int rc = check_dims(dtype, d, m, n, row_offset);
+  if (rc) return rc;
+  if (nnz < 0 || !h_colptr || (nnz > 0 && !rowidx)) return SK_EINVAL;
+  rc = validate_colptr(h_colptr, n, nnz, true);
+  if (rc) return rc;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (validate_rows) {
+    rc = validate_rows_sync(rowidx, nnz, m, stream);
+    if (rc) return rc;
+  }
+  int64_t* dc = nullptr;
+  SK_CUDA(cudaMalloc(&dc, (size_t)(n + 1) * sizeof(int64_t)));
+  cudaError_t e = cudaMemcpyAsync(dc, h_colptr, (size_t)(n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, stream);
+  if (e != cudaSuccess) { cudaFree(dc); return cuda_fail(e, "upload colptr"); }
+  rc = make_plan(plan, dtype, d, m, n, row_offset, h_colptr, dc, rowidx, nnz, stream, 1);
+  if (rc) { cudaFree(dc); return rc; }
+  (*plan)->owned_colptr = dc;
+  return SK_OK;
+}
+
+int sketch_set_pair_path(int path) {
+  if (path < SK_PAIR_AUTO || path > SK_PAIR_JKI) return SK_EINVAL;
+  g_pair_path.store(path, std::memory_order_relaxed);
   return SK_OK;
 }
 
@@ -499,7 +665,7 @@ int sketch_apply_host(uint64_t seed, sk_dist_t dist, sk_dtype_t dtype, int64_t d
   for (int g = 0; g < G && e == cudaSuccess; ++g) {
     const int64_t c0 = cb[g], c1 = cb[g + 1];
     const int rcp = make_plan(&plans[g], dtype, d, m, c1 - c0, row_offset, h_colptr + c0, d_colptr + c0,
-                              d_rowidx, h_colptr[c1] - h_colptr[c0], stream);
+                              d_rowidx, h_colptr[c1] - h_colptr[c0], stream, -1);
     if (rcp != SK_OK) { e = cudaErrorUnknown; what = "make_plan(group)"; }
   }
   SK_STEP(cudaEventRecord(ev_start, stream));
@@ -572,6 +738,8 @@ int sketch_plan_stats(sk_plan_t plan, sk_stats_t* h) {
   h->n_items_pair = plan->n_pair;
   h->philox_blocks_rad = plan->philox_rad;
   h->philox_blocks_pair = plan->philox_pair;
+  h->n_items_jki = plan->jki.n_items;
+  h->jki_nonzero_rows = plan->jki_rows;
   h->plan_bytes = (plan->n_rad + plan->n_pair) * (int64_t)sizeof(Item) +
                   (plan->n_tc + plan->n_f4 + plan->n_f4t) * (int64_t)sizeof(sk::TcItem) +
                   plan->n_f4n * (int64_t)sizeof(sk::NItem) +
@@ -587,6 +755,7 @@ int sketch_plan_destroy(sk_plan_t plan) {
   if (plan->d_tc) { cudaError_t e2 = cudaFree(plan->d_tc); if (e == cudaSuccess) e = e2; }
   if (plan->d_f4n) { cudaError_t e2 = cudaFree(plan->d_f4n); if (e == cudaSuccess) e = e2; }
   if (plan->d_f4t) { cudaError_t e2 = cudaFree(plan->d_f4t); if (e == cudaSuccess) e = e2; }
+  if (plan->d_jki) { cudaError_t e2 = cudaFree(plan->d_jki); if (e == cudaSuccess) e = e2; }
   delete plan;
   if (e != cudaSuccess) return cuda_fail(e, "cudaFree(plan)");
   return SK_OK;

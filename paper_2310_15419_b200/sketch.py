@@ -28,8 +28,10 @@ SK_OK, SK_EINVAL, SK_ECSC, SK_ENOMEM, SK_ECUDA, SK_EUNSUPPORTED = 0, -1, -2, -3,
 EXPORTS = ["sketch_plan", "sketch_plan_host", "sketch_apply", "sketch_apply_csc",
            "sketch_apply_host", "sketch_fill_s", "sketch_plan_stats", "sketch_plan_destroy",
            "sketch_error_string", "sketch_last_error_detail", "sketch_version",
-           "sketch_set_rad_f64_path", "sketch_apply_kernel_name"]
+           "sketch_set_rad_f64_path", "sketch_apply_kernel_name", "sketch_set_pair_path",
+           "sketch_plan_host_jki"]
 RAD_F64_PATHS = {"fp4": 0, "int8smem": 1, "int8tmem": 2, "simt": 3, "hybrid": 4, "fp4n": 5, "fp4t": 6}
+PAIR_PATHS = {"auto": 0, "kji": 1, "jki": 2}
 _STRING_RESULTS = ("sketch_error_string", "sketch_last_error_detail", "sketch_version",
                    "sketch_apply_kernel_name")
 
@@ -43,7 +45,7 @@ class SketchError(RuntimeError):
 class sk_stats_t(ctypes.Structure):
     _fields_ = [(name, ctypes.c_int64) for name in
                 ("d", "m", "n", "nnz", "row_offset", "max_col_nnz", "n_items_rad", "n_items_pair",
-                 "philox_blocks_rad", "philox_blocks_pair", "plan_bytes")]
+                 "philox_blocks_rad", "philox_blocks_pair", "plan_bytes", "n_items_jki", "jki_nonzero_rows")]
 
 
 _lock = threading.Lock()
@@ -81,6 +83,8 @@ def load_library(path: str = LIB_PATH):
         lib.sketch_version.argtypes = []
         lib.sketch_version.restype = ctypes.c_char_p
         lib.sketch_set_rad_f64_path.argtypes = [i32]
+        lib.sketch_set_pair_path.argtypes = [i32]
+        lib.sketch_plan_host_jki.argtypes = [ctypes.POINTER(vp), i32, i64, i64, i64, i64, vp, vp, i64, i32, vp]
         lib.sketch_apply_kernel_name.argtypes = [vp, i32]
         lib.sketch_apply_kernel_name.restype = ctypes.c_char_p
         for name in EXPORTS:
@@ -130,7 +134,9 @@ class Plan:
     """Owning wrapper of an ``sk_plan_t`` built by ``sketch_plan``."""
 
     def __init__(self, colptr, rowidx, d: int, m: int, dtype="f64", row_offset: int = 0,
-                 stream=None):
+                 stream=None, jki: bool = False):
+        """``jki=True`` always builds the Algorithm 4 structure (sketch_plan_host_jki); otherwise
+        the plan builds it only when a sample shows enough row reuse."""
         import torch
         _require_cuda(colptr, rowidx)
         if colptr.dtype != torch.int64 or rowidx.dtype != torch.int32:
@@ -142,9 +148,15 @@ class Plan:
         self.row_offset = int(row_offset)
         self._keep = (colptr, rowidx)     # the plan references these device buffers
         h = ctypes.c_void_p()
-        _check(lib.sketch_plan(ctypes.byref(h), self.dtype, self.d, self.m, self.n, self.row_offset,
-                               ctypes.c_void_p(colptr.data_ptr()), ctypes.c_void_p(rowidx.data_ptr()),
-                               self.nnz, _stream_ptr(stream)), "sketch_plan")
+        if jki:
+            hc = colptr.cpu().contiguous()
+            _check(lib.sketch_plan_host_jki(ctypes.byref(h), self.dtype, self.d, self.m, self.n, self.row_offset,
+                                            ctypes.c_void_p(hc.data_ptr()), ctypes.c_void_p(rowidx.data_ptr()),
+                                            self.nnz, 1, _stream_ptr(stream)), "sketch_plan_host_jki")
+        else:
+            _check(lib.sketch_plan(ctypes.byref(h), self.dtype, self.d, self.m, self.n, self.row_offset,
+                                   ctypes.c_void_p(colptr.data_ptr()), ctypes.c_void_p(rowidx.data_ptr()),
+                                   self.nnz, _stream_ptr(stream)), "sketch_plan")
         self._h = h
 
     def stats(self) -> dict:
@@ -252,6 +264,12 @@ def set_rad_f64_path(path) -> None:
     "int8smem", "int8tmem" or "simt" (process-wide)."""
     p = RAD_F64_PATHS[path] if isinstance(path, str) else int(path)
     _check(load_library().sketch_set_rad_f64_path(p), "sketch_set_rad_f64_path")
+
+
+def set_pair_path(path) -> None:
+    """Uniform / Gaussian kernel: "auto" (Algorithm 4 when the plan built it), "kji", "jki"."""
+    p = PAIR_PATHS[path] if isinstance(path, str) else int(path)
+    _check(load_library().sketch_set_pair_path(p), "sketch_set_pair_path")
 
 
 def version() -> str:

@@ -397,3 +397,54 @@ def test_sap_solve_on_gpu(sk, dist, method):
     xref = np.linalg.lstsq(M, b, rcond=None)[0]
     x = res.x.cpu().numpy()
     assert np.linalg.norm(x - xref) <= 1e-8 * np.linalg.norm(xref)
+
+
+# ------------------------------------------------------------------- Algorithm 4 (jki, §8(f) f1)
+
+JKI_CASES = [
+    ("abnormal_A", lambda: workloads.abnormal_paper("A", m=20000, n=70, seed=1), 700),
+    ("abnormal_B", lambda: workloads.abnormal_paper("B", m=9000, n=60, seed=2), 300),
+    ("abnormal_C", lambda: workloads.abnormal_paper("C", m=3000, n=2100, seed=3), 129),
+    ("random_ragged", lambda: workloads.random_csc(5000, 37, [0, 3, 40, 1, 0, 200] * 6 + [7], seed=4), 1100),
+    ("unsorted_dups", lambda: workloads.random_csc(300, 21, 60, seed=5, sorted_rows=False, duplicates=True), 65),
+]
+
+
+@pytest.mark.parametrize("dist", ["uniform", "gaussian"])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("case", JKI_CASES, ids=[c[0] for c in JKI_CASES])
+def test_jki_matches_oracle(sk, dist, dtype, case):
+    # Algorithm 4 (one S[:, j] per nonzero row of a 16-column group, reused across the row) gives the
+    # same sketch as the oracle's Algorithm 3 loop, within the dtype's bar
+    import torch
+    name, build, d = case
+    A = build()
+    if dtype == "f32":
+        A.vals = A.vals.astype(np.float32)
+    plan = sk.Plan(_dev(A.colptr), _dev(A.rowidx), d, A.m, dtype, jki=True)
+    try:
+        st = plan.stats()
+        assert st["n_items_jki"] > 0 and "Algorithm 4" in plan.kernel_name(dist)
+        got = plan.apply(_dev(A.vals), 19, dist).T.double().cpu().numpy()
+        torch.cuda.synchronize()
+    finally:
+        plan.close()
+    ref, B = oracle.sketch(19, dist, d, A.m, A.n, A.colptr, A.rowidx, A.vals, threads=8)
+    _check(got, ref, B, TOL[dtype])
+
+
+def test_jki_auto_selection(sk):
+    # the plan builds the jki structure on its own only for patterns with row reuse
+    A = workloads.abnormal_paper("A", m=20000, n=64, seed=1)
+    B = workloads.random_csc(200000, 64, 300, seed=2)
+    pa = sk.Plan(_dev(A.colptr), _dev(A.rowidx), 256, A.m)
+    pb = sk.Plan(_dev(B.colptr), _dev(B.rowidx), 256, B.m)
+    try:
+        assert pa.stats()["n_items_jki"] > 0 and pb.stats()["n_items_jki"] == 0
+        assert pa.stats()["jki_nonzero_rows"] * 10 <= A.nnz
+        sk.set_pair_path("kji")
+        assert "Algorithm 4" not in pa.kernel_name("uniform")
+    finally:
+        sk.set_pair_path("auto")
+        pa.close()
+        pb.close()

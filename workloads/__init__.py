@@ -291,6 +291,37 @@ def abnormal(kind: str, m: int, n: int, nnz: int, seed: int) -> CSC:
     return _finish(m, n, rl, vl, np.float64, {"abnormal": kind})
 
 
+def abnormal_paper(kind: str, m: int = 100_000, n: int = 10_000, seed: int = 0) -> CSC:
+    """The exotic patterns of Table tab:extreme_examples as PAPER.md:699-701 describes them
+    (m = 100000, n = 10000, density ~1e-3, N(0,1) values):
+    'A': every 1000th row dense, all other rows zero;
+    'B': ~2998/3000 of the nonzeros in the middle third of the columns (about 300 random rows per
+         middle column), the rest one nonzero in random outer columns;
+    'C': every 1000th column dense, all other columns zero."""
+    rng = np.random.default_rng(seed)
+    if kind == "A":
+        rows = np.arange(0, m, 1000, dtype=np.int64)
+        rl = [rows for _ in range(n)]
+    elif kind == "B":
+        total = int(round(1e-3 * m * n))
+        mid0, mid1 = n // 3, (2 * n) // 3
+        inner = int(round(total * 2998 / 3000))
+        per, extra = divmod(inner, mid1 - mid0)
+        rl = [np.zeros(0, dtype=np.int64) for _ in range(n)]
+        for i, k in enumerate(range(mid0, mid1)):
+            rl[k] = np.sort(rng.choice(m, size=per + (1 if i < extra else 0), replace=False))
+        outer = np.array([k for k in range(n) if not mid0 <= k < mid1])
+        for k in rng.choice(outer, size=min(total - inner, outer.size), replace=False):
+            rl[k] = rng.integers(0, m, size=1)
+    elif kind == "C":
+        full = np.arange(m, dtype=np.int64)
+        rl = [full if k % 1000 == 0 else np.zeros(0, dtype=np.int64) for k in range(n)]
+    else:
+        raise ValueError(kind)
+    vl = [rng.standard_normal(len(r)) for r in rl]
+    return _finish(m, n, rl, vl, np.float64, {"abnormal_paper": kind})
+
+
 # ---------------------------------------------------------------- least-squares problems (SAP, §8(f) f2)
 
 def ls_problem(m: int, n: int, nnz_per_col, seed: int, noise: float = 1.0, col_scale_decades: float = 0.0):

@@ -31,7 +31,11 @@ namespace sk {
 namespace {
 
 constexpr int kTTiles = 4;                        // MMA tiles (M = 128) per item: 512 Â rows
-constexpr int kTSWarps = 8;                       // S producers: (lane quarter s, nonzero half h)
+#ifndef SK_F4T_SWARPS
+#define SK_F4T_SWARPS 8
+#endif
+constexpr int kTSWarps = SK_F4T_SWARPS;           // S producers: (lane quarter s, nonzero half h, K-step class)
+constexpr int kTKC = kTSWarps / 8;                // K-step classes: warp class c takes sub = c, c + kTKC, ...
 constexpr int kTDWarps = 2;                       // digit producers: nonzero half
 constexpr int kTProducers = kTSWarps + kTDWarps;
 constexpr int kTLoaderWarp = kTProducers;
@@ -76,9 +80,9 @@ __device__ __forceinline__ void t_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
       "@!P1 bra WAIT_%=;\n\t}"
-      :: "r"(t_u32(bar)), "r"(parity) : "memory");
+      :: "r"(t_u32(bar)), "r"(parity), "r"(1000000u) : "memory");
 }
 
 // K-major no-swizzle smem descriptor (digits operand): core matrix 8 rows x 16 B, LBO = 128 B,
@@ -151,7 +155,8 @@ __global__ void __launch_bounds__(kTThreads, 1) sk_rad_f4t_kernel(const ApplyArg
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kTStages; ++s) { t_init(&sh.full[s], kTProducers); t_init(&sh.empty[s], 1); }
-    for (int s = 0; s < kTSlots; ++s) { t_init(&sh.jfull[s], 32); t_init(&sh.jempty[s], kTProducers); }
+    // a K-step slot is read by the S warps of one K-step class and by the digit warps
+    for (int s = 0; s < kTSlots; ++s) { t_init(&sh.jfull[s], 32); t_init(&sh.jempty[s], kTSWarps / kTKC + kTDWarps); }
     t_init(&sh.done, 1);
     sh.maxabs_bits = 0ull;
     sh.nonfinite = 0;
@@ -199,15 +204,17 @@ __global__ void __launch_bounds__(kTThreads, 1) sk_rad_f4t_kernel(const ApplyArg
 
   if (warp < kTSWarps) {
     // ===================== S producers: lane quarter s = warp % 4, nonzero half h =====================
-    const int s = warp & 3, h = warp >> 2;
+    const int s = warp & 3, h = (warp >> 2) & 1, kc = warp >> 3;
     const uint32_t q = q0 + (uint32_t)s;
     const uint32_t tq = tmem + ((uint32_t)(32 * s) << 16);
+    constexpr int kMine = kTSub / kTKC;          // K-steps of a stage this warp produces
+    static_assert(kMine * kTKC == kTSub, "K-step classes must divide the stage");
     for (int ss = 0; ss < nsup; ++ss) {
       const int stage = ss % kTStages, use = ss / kTStages;
-      uint32_t x[4 * kTSub];
+      uint32_t x[4 * kMine];
 #pragma unroll
-      for (int sub = 0; sub < kTSub; ++sub) {
-        const int ks = kTSub * ss + sub;
+      for (int i = 0; i < kMine; ++i) {
+        const int ks = kTSub * ss + kc + kTKC * i;
         uint32_t j = 0u;
         if (ks < nsteps) {
           const int slot = ks % kTSlots;
@@ -217,21 +224,23 @@ __global__ void __launch_bounds__(kTThreads, 1) sk_rad_f4t_kernel(const ApplyArg
           if (lane == 0) t_arrive(&sh.jempty[slot]);
         }
         const uint4 b = s_block(q, (uint64_t)P.row_offset + j, P.keys);   // padding nonzeros: digits 0
-        x[4 * sub + 0] = b.x; x[4 * sub + 1] = b.y; x[4 * sub + 2] = b.z; x[4 * sub + 3] = b.w;
+        x[4 * i + 0] = b.x; x[4 * i + 1] = b.y; x[4 * i + 2] = b.z; x[4 * i + 3] = b.w;
       }
-      t_transpose<4 * kTSub>(x, lane);            // lane r: row 32 t + r of block q over 32 nonzeros
+      t_transpose<4 * kMine>(x, lane);            // lane r: row 32 t + r of block q over 32 nonzeros
       if (use > 0) t_wait(&sh.empty[stage], (use - 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-      for (int sub = 0; sub < kTSub; ++sub)
+      for (int i = 0; i < kMine; ++i) {
+        const int sub = kc + kTKC * i;
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
-          const uint32_t y = x[4 * sub + t];
+          const uint32_t y = x[4 * i + t];
           const uint32_t col = kTACol + (uint32_t)(((stage * kTSub + sub) * kTTiles + t) * 8 + 4 * h);
           asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};"
                        :: "r"(tq + col), "r"(t_nib(y << 3)), "r"(t_nib(y << 2)), "r"(t_nib(y << 1)), "r"(t_nib(y))
                        : "memory");
         }
+      }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
@@ -330,16 +339,16 @@ __global__ void __launch_bounds__(kTThreads, 1) sk_rad_f4t_kernel(const ApplyArg
     __syncwarp();
   }
 
-  // ===================== epilogue: S warps read D; warp (s, h) takes tiles h and h + 2 =====================
+  // ===================== epilogue: S warps read D; warp (quarter s, g = warp / 4) takes tiles g, g + kTSWarps/4 ..
   if (warp < kTSWarps) {
     if (nsteps > 0) {
       t_wait(&sh.done, 0);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     }
-    const int s = warp & 3, h = warp >> 2;
+    const int s = warp & 3, g = warp >> 2;
     double* outc = reinterpret_cast<double*>(P.out) + (int64_t)it.col * P.ld;
     const double nan = __longlong_as_double(0x7FF8000000000000ll);
-    for (int t = h; t < kTTiles; t += 2) {
+    for (int t = g; t < kTTiles; t += kTSWarps / 4) {
       long long lo = 0, hi = 0, ones = 0;
       if (nsteps > 0) {
         const uint32_t base = tmem + ((uint32_t)(32 * s) << 16) + (uint32_t)(t * kTN);

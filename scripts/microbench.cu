@@ -36,6 +36,35 @@ __global__ void philox_kernel(uint32_t* out, int iters, sk::PhiloxKeys K) {
   if (f == 0x12345678u) out[0] = f;
 }
 
+// Philox with the products as mul.hi + mul.lo (IMAD.HI + IMAD) instead of mul.wide (IMAD.WIDE)
+__device__ __forceinline__ uint4 philox_hilo(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                            const sk::PhiloxKeys& K) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t h0 = __umulhi(sk::kPhiloxM0, c0), l0 = sk::kPhiloxM0 * c0;
+    const uint32_t h1 = __umulhi(sk::kPhiloxM1, c2), l1 = sk::kPhiloxM1 * c2;
+    const uint32_t n0 = h1 ^ c1 ^ K.k0[r];
+    const uint32_t n2 = h0 ^ c3 ^ K.k1[r];
+    c1 = l1; c3 = l0; c0 = n0; c2 = n2;
+  }
+  return make_uint4(c0, c1, c2, c3);
+}
+
+template <int MODE>
+__global__ void philox_kernel2(uint32_t* out, int iters, sk::PhiloxKeys K) {
+  uint32_t f = 0;
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int it = 0; it < iters; it += 4) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint4 x = MODE == 0 ? sk::s_block((uint32_t)(it + u), (uint64_t)j, K)
+                                : philox_hilo((uint32_t)(it + u), 0u, j, 0u, K);
+      f ^= x.x ^ x.y ^ x.z ^ x.w;
+    }
+  }
+  if (f == 0x12345678u) out[0] = f;
+}
+
 // IMAD.WIDE.U32 vs (IMAD.HI.U32 + IMAD.LO) for the 32x32->64 products of a Philox round.
 template <int MODE>
 __global__ void mul_kernel(uint32_t* out, int iters, uint32_t m) {
@@ -87,6 +116,10 @@ int main() {
   const int piters = 4000;
   timeit([&] { philox_kernel<<<blocks, threads>>>((uint32_t*)buf, piters, sk::make_keys(7)); },
          (double)blocks * threads * piters, "philox_blocks_per_s");
+  timeit([&] { philox_kernel2<0><<<blocks, threads>>>((uint32_t*)buf, piters, sk::make_keys(7)); },
+         (double)blocks * threads * piters, "philox_wide_x4_blocks_per_s");
+  timeit([&] { philox_kernel2<1><<<blocks, threads>>>((uint32_t*)buf, piters, sk::make_keys(7)); },
+         (double)blocks * threads * piters, "philox_hilo_x4_blocks_per_s");
   timeit([&] { mul_kernel<0><<<blocks, threads>>>((uint32_t*)buf, 20000, 0xD2511F53u); },
          (double)blocks * threads * 8 * 20000, "mulwide_per_s");
   timeit([&] { mul_kernel<1><<<blocks, threads>>>((uint32_t*)buf, 20000, 0xD2511F53u); },

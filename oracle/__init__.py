@@ -26,7 +26,7 @@ _CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fopenmp",
 
 RADEMACHER, UNIFORM, GAUSSIAN = 0, 1, 2
 F64, F32 = 0, 1
-DISTS = {"rademacher": RADEMACHER, "uniform": UNIFORM, "gaussian": GAUSSIAN}
+DISTS = {"rademacher": RADEMACHER, "uniform": UNIFORM, "gaussian": GAUSSIAN, "uniform24": 3}
 
 _lock = threading.Lock()
 _lib = None

@@ -28,6 +28,10 @@
  *        Gaussian    q = i/2, k1 = U1>>11, k2 = U2>>11, u1 = (k1+1)2^-53, u2 = k2 2^-53,
  *                    rho = sqrt(-2 ln u1), th = u2 * fl(2 pi),
  *                    S[2q] = rho cos th, S[2q+1] = rho sin th   (Box-Muller)
+ *        Uniform24   (the 32-bit numbers of PAPER.md:464): a cheaper
+ *                    uniform(-1, 1) with 4 entries per block: q = i/4, t = i%4,
+ *                    k = x[t] >> 8 (24 bits), S = (2k + 1 - 2^24) * 2^-24 (odd grid, exact in
+ *                    fp32 and fp64)
  *      For dtype F32 the entry is RN-even(S64) (R5).
  *
  *  (3) The sketch itself in the loop order of Algorithm 3 "Variant kji with RNG"
@@ -46,7 +50,7 @@
 #include <omp.h>
 #endif
 
-enum { OR_RADEMACHER = 0, OR_UNIFORM = 1, OR_GAUSSIAN = 2 };
+enum { OR_RADEMACHER = 0, OR_UNIFORM = 1, OR_GAUSSIAN = 2, OR_UNIFORM24 = 3 };
 enum { OR_F64 = 0, OR_F32 = 1 };
 
 /* ---------------------------------------------------------------------------------
@@ -107,6 +111,10 @@ static double entry_from_block(int dist, const uint32_t x[4], int e)
         uint64_t k = U >> 11;                                     /* 53 random bits */
         int64_t odd = (int64_t)(2u * k + 1u) - ((int64_t)1 << 53); /* odd, |odd| < 2^53: exact */
         return (double)odd * 0x1p-53;
+    } else if (dist == OR_UNIFORM24) {     /* E = 4: entry t uses the top 24 bits of word t */
+        uint32_t k = x[e] >> 8;
+        int32_t odd = (int32_t)(2u * k + 1u) - (int32_t)(1 << 24);   /* odd, |odd| < 2^24: exact */
+        return (double)odd * 0x1p-24;
     } else {                               /* E = 2: Box-Muller pair */
         uint64_t U1 = ((uint64_t)x[0] << 32) | (uint64_t)x[1];
         uint64_t U2 = ((uint64_t)x[2] << 32) | (uint64_t)x[3];
@@ -119,7 +127,7 @@ static double entry_from_block(int dist, const uint32_t x[4], int e)
     }
 }
 
-static int entries_per_block(int dist) { return dist == OR_RADEMACHER ? 128 : 2; }
+static int entries_per_block(int dist) { return dist == OR_RADEMACHER ? 128 : (dist == OR_UNIFORM24 ? 4 : 2); }
 
 static double to_dtype(double v, int dtype)
 {
@@ -167,7 +175,7 @@ int or_fill_s(uint64_t seed, int dist, int dtype, int64_t i0, int64_t i1, int64_
               double* out)
 {
     int64_t i, j, rows = i1 - i0;
-    if (i1 < i0 || j1 < j0 || i0 < 0 || j0 < 0 || dist < 0 || dist > 2 || dtype < 0 || dtype > 1)
+    if (i1 < i0 || j1 < j0 || i0 < 0 || j0 < 0 || dist < 0 || dist > 3 || dtype < 0 || dtype > 1)
         return -1;
     for (j = j0; j < j1; ++j)
         for (i = i0; i < i1; ++i)

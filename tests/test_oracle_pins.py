@@ -73,7 +73,7 @@ def test_philox_bit_balance_and_avalanche():
 
 # ------------------------------------------------------------------------- S entries
 
-@pytest.mark.parametrize("dist", ["rademacher", "uniform", "gaussian"])
+@pytest.mark.parametrize("dist", ["rademacher", "uniform", "gaussian", "uniform24"])
 def test_entrywise_equals_blockwise_generation(dist):
     # S[i, j] must not depend on how it is generated (block reuse vs one entry at a time)
     # nor on d (prefix property, R16): the reproducibility the paper asks of a
@@ -105,6 +105,29 @@ def test_uniform_law_and_exact_grid():
     assert abs(S.mean()) < 5 * np.sqrt(1 / 3 / N)
     assert abs((S**2).mean() - 1 / 3) < 5 * np.sqrt(4 / 45 / N)   # Var U(-1,1) = 1/3
     assert stats.kstest(S, stats.uniform(loc=-1, scale=2).cdf).pvalue > 1e-4
+
+
+def test_uniform24_law_exact_grid_and_words():
+    # the 24-bit odd grid, 4 entries per Philox block.  Pinned to the law (open
+    # interval, exact grid, mean 0, variance (1 - 2^-48)/3, KS) and to the Philox words through the
+    # independent Triton reference: entry 4q + t uses the top 24 bits of word t of block q.
+    from scipy import stats
+    S = oracle.fill_s(16, "uniform24", 0, 400, 0, 300).ravel()
+    assert np.all(np.abs(S) < 1.0)
+    odd = S * 2.0**24
+    assert np.all(odd == np.round(odd)) and np.all(np.mod(odd, 2) == 1)
+    assert np.array_equal(S.astype(np.float32).astype(np.float64), S)   # exact in fp32
+    N = S.size
+    assert abs(S.mean()) < 5 * np.sqrt(1 / 3 / N)
+    assert abs((S**2).mean() - 1 / 3) < 5 * np.sqrt(4 / 45 / N)
+    assert stats.kstest(S, stats.uniform(loc=-1, scale=2).cdf).pvalue > 1e-4
+    seed, j = 2**40 + 9, 5
+    words = _triton_philox([[q, 0, j, 0, seed & 0xFFFFFFFF, seed >> 32] for q in range(3)])
+    col = oracle.get_samples(seed, "uniform24", j, 12)
+    for q in range(3):
+        for t in range(4):
+            k = int(words[q][t]) >> 8
+            assert col[4 * q + t] == (2 * k + 1 - 2**24) / 2.0**24
 
 
 def test_gaussian_law():
@@ -159,7 +182,7 @@ def _dense_check(A, dist, d, seed, dtype="f64"):
     return Ahat, B, ref, bnd
 
 
-@pytest.mark.parametrize("dist", ["rademacher", "uniform", "gaussian"])
+@pytest.mark.parametrize("dist", ["rademacher", "uniform", "gaussian", "uniform24"])
 def test_sketch_matches_bruteforce_dense_product(dist):
     A = workloads.random_csc(300, 12, 9, seed=1)
     Ahat, B, ref, bnd = _dense_check(A, dist, 70, seed=42)
@@ -235,7 +258,8 @@ def test_threads_do_not_change_result():
     assert np.array_equal(a1, a4)
 
 
-@pytest.mark.parametrize("dist,sigma2", [("rademacher", 1.0), ("uniform", 1 / 3), ("gaussian", 1.0)])
+@pytest.mark.parametrize("dist,sigma2", [("rademacher", 1.0), ("uniform", 1 / 3), ("gaussian", 1.0),
+                                          ("uniform24", 1 / 3)])
 def test_expected_gram_matches_AtA(dist, sigma2):
     # North-star invariant: E[ÂᵀÂ] / (d σ²) = AᵀA (R15), averaged over seeds.
     A = workloads.random_csc(60, 4, 6, seed=8)

@@ -19,6 +19,9 @@
  *   SK_GAUSSIAN   : q = i/2, k1 = (x0*2^32+x1)>>11, k2 = (x2*2^32+x3)>>11,
  *                   u1 = (k1+1) 2^-53, u2 = k2 2^-53, rho = sqrt(-2 ln u1),
  *                   th = u2 * fl64(2 pi);  S[2q] = rho cos th, S[2q+1] = rho sin th
+ *   SK_UNIFORM24  : q = i/4, t = i%4, k = x[t] >> 8;  S = (2k + 1 - 2^24) * 2^-24
+ *                   (a cheaper uniform(-1,1) for 32-bit work, PAPER.md:464;
+ *                   4 entries per block, exact in fp32 -- a different S than SK_UNIFORM)
  *   dtype SK_F32  : S32 = round-to-nearest-even(S64); arithmetic in fp32.
  * Here j is the GLOBAL row index of A (row_offset + local row), i the row of Â.
  *
@@ -49,7 +52,7 @@ extern "C" {
 
 typedef struct CUstream_st* sk_stream_t;           /* == cudaStream_t */
 
-typedef enum { SK_RADEMACHER = 0, SK_UNIFORM = 1, SK_GAUSSIAN = 2 } sk_dist_t;
+typedef enum { SK_RADEMACHER = 0, SK_UNIFORM = 1, SK_GAUSSIAN = 2, SK_UNIFORM24 = 3 } sk_dist_t;
 typedef enum { SK_F64 = 0, SK_F32 = 1 } sk_dtype_t;
 
 typedef enum {

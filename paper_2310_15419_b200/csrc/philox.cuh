@@ -88,6 +88,14 @@ __device__ __forceinline__ double uniform53_bits(uint32_t xa, uint32_t xb) {
   return __hiloint2double(__double2hiint(mag) ^ (int)(nb & 0x80000000u), __double2loint(mag));
 }
 
+// Uniform24: S = (2k + 1 - 2^24) 2^-24 with k = the top 24 bits of one
+// Philox word (4 entries per block).  An odd multiple of 2^-24 below 1 in magnitude: exact in fp32
+// (and fp64); I2F of the exact odd integer and one exact scaling.
+__device__ __forceinline__ float uniform24(uint32_t w) {
+  const int odd = (int)(((w >> 8) << 1) | 1u) - (1 << 24);
+  return __int2float_rn(odd) * 0x1p-24f;
+}
+
 // 2*pi rounded to the nearest double, 0x1.921fb54442d18p+2.
 __device__ __forceinline__ double two_pi_f64() { return __longlong_as_double(0x401921FB54442D18ll); }
 

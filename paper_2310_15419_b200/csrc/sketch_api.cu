@@ -38,7 +38,7 @@ int cuda_fail(cudaError_t e, const char* what) {
     if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
   } while (0)
 
-bool valid_dist(int d) { return d == SK_RADEMACHER || d == SK_UNIFORM || d == SK_GAUSSIAN; }
+bool valid_dist(int d) { return d == SK_RADEMACHER || d == SK_UNIFORM || d == SK_GAUSSIAN || d == SK_UNIFORM24; }
 bool valid_dtype(int t) { return t == SK_F64 || t == SK_F32; }
 size_t dtype_bytes(int t) { return t == SK_F64 ? 8 : 4; }
 
@@ -493,11 +493,12 @@ const char* kernel_name(const sk_plan_s* p, int dist) {
     return "sk_rad_kernel<double>";
   }
   const bool f64 = p->dtype == SK_F64;
-  if (p->jki.n_items > 0 && pair_path() != SK_PAIR_KJI) {
+  if (p->jki.n_items > 0 && pair_path() != SK_PAIR_KJI && (dist == SK_UNIFORM || dist == SK_GAUSSIAN)) {
     if (dist == SK_UNIFORM) return f64 ? "sk_jki_kernel<uniform, double> (Algorithm 4)" : "sk_jki_kernel<uniform, float> (Algorithm 4)";
     return f64 ? "sk_jki_kernel<gaussian, double> (Algorithm 4)" : "sk_jki_kernel<gaussian, float> (Algorithm 4)";
   }
   if (dist == SK_UNIFORM) return f64 ? "sk_pair_kernel<uniform, double>" : "sk_pair_kernel<uniform, float>";
+  if (dist == SK_UNIFORM24) return f64 ? "sk_pair_kernel<uniform24, double>" : "sk_pair_kernel<uniform24, float>";
   return f64 ? "sk_pair_kernel<gaussian, double>" : "sk_pair_kernel<gaussian, float>";
 }
 

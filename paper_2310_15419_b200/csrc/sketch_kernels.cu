@@ -160,11 +160,15 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 2 : 1) sk_rad_kerne
   }
 }
 
-// ------------------------------------------------------------------ uniform / Gaussian
+// ------------------------------------------------------------------ uniform / Gaussian / uniform24
 //
-// Lane l owns Â rows warp_row0 + 16 l + e (e = 0..15) = entries of the 8 Philox blocks
-// q = (warp_row0 + 16 l)/2 + h (h = 0..7); each block yields 2 entries, so a lane generates
-// exactly the S entries it consumes (no exchange).
+// Lane l owns Â rows warp_row0 + 16 l + e (e = 0..15) = entries of the 16/E Philox blocks
+// q = (warp_row0 + 16 l)/E + h; each block yields E entries (E = 2 for uniform / Gaussian, 4 for
+// uniform24), so a lane generates exactly the S entries it consumes (no exchange).
+template <int DIST> constexpr int pair_E() { return DIST == 3 ? 4 : 2; }
+template <int DIST, typename T>
+__device__ __forceinline__ void block_entries(const uint4 x, T (&v)[pair_E<DIST>()], const double* __restrict__ logtab);
+
 template <int DIST, typename T>
 __device__ __forceinline__ void pair_entries(const uint4 x, T& v0, T& v1, const double* __restrict__ logtab) {
   if constexpr (DIST == 1) {
@@ -176,6 +180,15 @@ __device__ __forceinline__ void pair_entries(const uint4 x, T& v0, T& v1, const 
     gaussian_pair_fast(x, logtab, g0, g1);
     if constexpr (sizeof(T) == 8) { v0 = g0; v1 = g1; }
     else { v0 = __double2float_rn(g0); v1 = __double2float_rn(g1); }
+  }
+}
+
+template <int DIST, typename T>
+__device__ __forceinline__ void block_entries(const uint4 x, T (&v)[pair_E<DIST>()], const double* __restrict__ logtab) {
+  if constexpr (DIST == 3) {
+    v[0] = (T)uniform24(x.x); v[1] = (T)uniform24(x.y); v[2] = (T)uniform24(x.z); v[3] = (T)uniform24(x.w);
+  } else {
+    pair_entries<DIST, T>(x, v[0], v[1], logtab);
   }
 }
 
@@ -198,7 +211,8 @@ __global__ void __launch_bounds__(kThreads, kPairRows <= 8 ? 2 : 1) sk_pair_kern
   const int64_t L = pe - pb;
   const int64_t s0 = wk < WK ? pb + (L * wk) / WK : pe, s1 = wk < WK ? pb + (L * (wk + 1)) / WK : pe;
   const int64_t lane_row0 = (int64_t)it.row0 + (int64_t)wd * kRowsPerWarpPair + kPairRows * lane;
-  const uint32_t q0 = (uint32_t)(lane_row0 >> 1);
+  constexpr int kE = pair_E<DIST>();
+  const uint32_t q0 = (uint32_t)(lane_row0 / kE);
   // Lanes whose rows all lie past d skip generation (their results are never stored).
   const bool active = lane_row0 < P.d;
 
@@ -220,12 +234,12 @@ __global__ void __launch_bounds__(kThreads, kPairRows <= 8 ? 2 : 1) sk_pair_kern
       if (!active) continue;
       const uint64_t J = (uint64_t)P.row_offset + jr;
 #pragma unroll
-      for (int h = 0; h < kPairRows / 2; ++h) {
+      for (int h = 0; h < kPairRows / kE; ++h) {
         const uint4 x = s_block(q0 + h, J, P.keys);
-        T v0, v1;
-        pair_entries<DIST, T>(x, v0, v1, logtab);
-        acc[2 * h] = fma(v0, a, acc[2 * h]);
-        acc[2 * h + 1] = fma(v1, a, acc[2 * h + 1]);
+        T v[kE];
+        block_entries<DIST, T>(x, v, logtab);
+#pragma unroll
+        for (int t = 0; t < kE; ++t) acc[kE * h + t] = fma(v[t], a, acc[kE * h + t]);
       }
     }
   }
@@ -268,11 +282,14 @@ __global__ void sk_fill_s_kernel(PhiloxKeys K, int64_t i0, int64_t i1, int64_t j
         if (i >= i0 && i < i1) col[i - i0] = ((w[e >> 5] >> (e & 31)) & 1u) ? T(-1) : T(1);
       }
     } else {
-      T v0, v1;
-      pair_entries<DIST, T>(x, v0, v1, &kBmLogTab[0][0]);
-      const int64_t i = q * 2;
-      if (i >= i0 && i < i1) col[i - i0] = v0;
-      if (i + 1 >= i0 && i + 1 < i1) col[i + 1 - i0] = v1;
+      constexpr int kE = pair_E<DIST>();
+      T v[kE];
+      block_entries<DIST, T>(x, v, &kBmLogTab[0][0]);
+#pragma unroll
+      for (int t = 0; t < kE; ++t) {
+        const int64_t i = q * kE + t;
+        if (i >= i0 && i < i1) col[i - i0] = v[t];
+      }
     }
   }
 }
@@ -316,6 +333,8 @@ cudaError_t launch_apply(int dist, int dtype, const ApplyArgs& a, cudaStream_t s
   }
   if (dist == 1) return dtype == 0 ? launch_items(sk_pair_kernel<1, double>, pair64, a, stream)
                                    : launch_items(sk_pair_kernel<1, float>, pair32, a, stream);
+  if (dist == 3) return dtype == 0 ? launch_items(sk_pair_kernel<3, double>, pair64, a, stream)
+                                   : launch_items(sk_pair_kernel<3, float>, pair32, a, stream);
   return dtype == 0 ? launch_items(sk_pair_kernel<2, double>, gauss, a, stream)
                     : launch_items(sk_pair_kernel<2, float>, gauss, a, stream);
 }
@@ -323,7 +342,7 @@ cudaError_t launch_apply(int dist, int dtype, const ApplyArgs& a, cudaStream_t s
 cudaError_t launch_fill_s(int dist, int dtype, uint64_t seed, int64_t i0, int64_t i1, int64_t j0,
                           int64_t j1, void* out, int64_t ld, cudaStream_t stream) {
   if (i1 <= i0 || j1 <= j0) return cudaSuccess;
-  const int64_t E = dist == 0 ? 128 : 2;
+  const int64_t E = dist == 0 ? 128 : (dist == 3 ? 4 : 2);
   const int64_t q0 = i0 / E, q1 = (i1 + E - 1) / E, nq = q1 - q0;
   const int64_t total = nq * (j1 - j0);
   const int threads = 256;
@@ -333,6 +352,7 @@ cudaError_t launch_fill_s(int dist, int dtype, uint64_t seed, int64_t i0, int64_
 #define SK_FILL(D, T) sk_fill_s_kernel<D, T><<<grid, threads, 0, stream>>>(K, i0, i1, j0, j1, q0, nq, (T*)out, ld)
   if (dist == 0) { if (dtype == 0) SK_FILL(0, double); else SK_FILL(0, float); }
   else if (dist == 1) { if (dtype == 0) SK_FILL(1, double); else SK_FILL(1, float); }
+  else if (dist == 3) { if (dtype == 0) SK_FILL(3, double); else SK_FILL(3, float); }
   else { if (dtype == 0) SK_FILL(2, double); else SK_FILL(2, float); }
 #undef SK_FILL
   return cudaGetLastError();

@@ -18,9 +18,9 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SKETCH_LIB") or os.path.join(_HERE, "libsketch.so")   # override: experiments only
 
-RADEMACHER, UNIFORM, GAUSSIAN = 0, 1, 2
+RADEMACHER, UNIFORM, GAUSSIAN, UNIFORM24 = 0, 1, 2, 3
 F64, F32 = 0, 1
-DIST = {"rademacher": RADEMACHER, "uniform": UNIFORM, "gaussian": GAUSSIAN}
+DIST = {"rademacher": RADEMACHER, "uniform": UNIFORM, "gaussian": GAUSSIAN, "uniform24": UNIFORM24}
 DTYPE = {"f64": F64, "f32": F32}
 
 SK_OK, SK_EINVAL, SK_ECSC, SK_ENOMEM, SK_ECUDA, SK_EUNSUPPORTED = 0, -1, -2, -3, -4, -5

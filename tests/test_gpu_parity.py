@@ -67,7 +67,7 @@ FILL_CASES = [
 ]
 
 
-@pytest.mark.parametrize("dist", ["rademacher", "uniform", "gaussian"])
+@pytest.mark.parametrize("dist", ["rademacher", "uniform", "gaussian", "uniform24"])
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 def test_fill_s_matches_oracle(sk, dist, dtype):
     for (i0, i1, j0, j1) in FILL_CASES:
@@ -152,7 +152,7 @@ SMALL = [
 ]
 
 
-@pytest.mark.parametrize("dist", ["rademacher", "uniform", "gaussian"])
+@pytest.mark.parametrize("dist", ["rademacher", "uniform", "gaussian", "uniform24"])
 @pytest.mark.parametrize("case", SMALL, ids=[c[0] for c in SMALL])
 def test_sketch_matches_oracle_small(sk, dist, case):
     name, build, d = case
@@ -201,7 +201,7 @@ def test_kernel_names_report_the_path(sk):
         plan.close()
 
 
-@pytest.mark.parametrize("dist", ["rademacher", "uniform", "gaussian"])
+@pytest.mark.parametrize("dist", ["rademacher", "uniform", "gaussian", "uniform24"])
 def test_sketch_f32_matches_oracle(sk, dist):
     A = workloads.random_csc(20000, 25, 120, seed=10, dtype=np.float32)
     got = _gpu_sketch(sk, A, 2100, dist, 5)

@@ -192,7 +192,7 @@ struct sk_plan_s {
   int64_t d, m, n, nnz, row_offset, max_col;
   const int64_t* colptr;   // device (caller-owned)
   const int32_t* rowidx;   // device (caller-owned)
-  Item* d_items = nullptr; // [rad items | pair items]
+  Item* d_items = nullptr; // [rad items | pair items | Gaussian items]
   sk::TcItem* d_tc = nullptr;       // tensor-core ±1 fp64 schedules (empty if not eligible):
   int64_t n_tc = 0;                 //   [int8 items (16 tiles) | fp4 items (6 tiles)]
   int64_t n_f4 = 0;
@@ -206,7 +206,7 @@ struct sk_plan_s {
   sk::JkiPlanView jki{};
   int64_t jki_rows = 0;             // Σ_groups nonzero rows
   int64_t* owned_colptr = nullptr;  // device copy made by sketch_plan_host
-  int64_t n_rad = 0, n_pair = 0;
+  int64_t n_rad = 0, n_pair = 0, n_gauss = 0;
   int64_t philox_rad = 0, philox_pair = 0;
 };
 
@@ -337,8 +337,10 @@ int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
   for (int64_t k = 0; k < n; ++k) p->max_col = std::max(p->max_col, h_colptr[k + 1] - h_colptr[k]);
   Schedule rad = build_schedule(h_colptr, n, d, sk::kRowsPerWarpRad, sk::kRowsPerWarpRad / 128);
   Schedule pair = build_schedule(h_colptr, n, d, sk::kRowsPerWarpPair, sk::kRowsPerWarpPair / 2);
+  Schedule gauss = build_schedule(h_colptr, n, d, sk::kRowsPerWarpGauss, sk::kRowsPerWarpGauss / 2);
   p->n_rad = (int64_t)rad.items.size();
   p->n_pair = (int64_t)pair.items.size();
+  p->n_gauss = (int64_t)gauss.items.size();
   p->philox_rad = rad.philox_blocks;
   p->philox_pair = pair.philox_blocks;
   // Tensor-core ±1 paths: every column within the exact-accumulation bound, and columns long
@@ -393,12 +395,13 @@ int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
       return rj;
     }
   }
-  const int64_t total = p->n_rad + p->n_pair;
+  const int64_t total = p->n_rad + p->n_pair + p->n_gauss;
   if (total > 0) {
     cudaError_t e = cudaMalloc(&p->d_items, (size_t)total * sizeof(Item));
     if (e != cudaSuccess) { delete p; return e == cudaErrorMemoryAllocation ? SK_ENOMEM : cuda_fail(e, "cudaMalloc(items)"); }
     std::vector<Item> all(rad.items);
     all.insert(all.end(), pair.items.begin(), pair.items.end());
+    all.insert(all.end(), gauss.items.begin(), gauss.items.end());
     e = cudaMemcpyAsync(p->d_items, all.data(), (size_t)total * sizeof(Item), cudaMemcpyHostToDevice, stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(stream);   // `all` is pageable and local
     if (e != cudaSuccess) { cudaFree(p->d_items); delete p; return cuda_fail(e, "upload items"); }
@@ -428,8 +431,9 @@ int apply_items(const sk_plan_s* p, uint64_t seed, sk_dist_t dist, const void* v
   a.rowidx = p->rowidx;
   a.vals = vals;
   a.out = out;
-  a.items = dist == SK_RADEMACHER ? p->d_items : p->d_items + p->n_rad;
-  a.n_items = dist == SK_RADEMACHER ? p->n_rad : p->n_pair;
+  a.items = dist == SK_RADEMACHER ? p->d_items
+            : dist == SK_GAUSSIAN ? p->d_items + p->n_rad + p->n_pair : p->d_items + p->n_rad;
+  a.n_items = dist == SK_RADEMACHER ? p->n_rad : dist == SK_GAUSSIAN ? p->n_gauss : p->n_pair;
   a.d = p->d;
   a.ld = p->d;
   a.row_offset = p->row_offset;
@@ -741,7 +745,7 @@ int sketch_plan_stats(sk_plan_t plan, sk_stats_t* h) {
   h->philox_blocks_pair = plan->philox_pair;
   h->n_items_jki = plan->jki.n_items;
   h->jki_nonzero_rows = plan->jki_rows;
-  h->plan_bytes = (plan->n_rad + plan->n_pair) * (int64_t)sizeof(Item) +
+  h->plan_bytes = (plan->n_rad + plan->n_pair + plan->n_gauss) * (int64_t)sizeof(Item) +
                   (plan->n_tc + plan->n_f4 + plan->n_f4t) * (int64_t)sizeof(sk::TcItem) +
                   plan->n_f4n * (int64_t)sizeof(sk::NItem) +
                   (plan->owned_colptr ? (plan->n + 1) * 8 : 0);

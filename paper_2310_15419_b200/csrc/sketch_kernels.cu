@@ -29,8 +29,6 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr int kXchWords = 5;                                   // padded 4-word exchange slot
 constexpr int kXchBytes = kWarps * 32 * kXchWords * 4;         // 10 KiB
 constexpr int kRadPad = 33;                                    // 32 rows per lane + 1 pad
-constexpr int kPairRows = kRowsPerWarpPair / 32;              // Â rows per lane (uniform / Gaussian)
-constexpr int kPairPad = kPairRows + 1;
 
 template <typename T>
 __device__ __forceinline__ T ldg_val(const void* vals, int64_t p) {
@@ -192,11 +190,16 @@ __device__ __forceinline__ void block_entries(const uint4 x, T (&v)[pair_E<DIST>
   }
 }
 
-constexpr int kPairRedBytes = kWarps * 32 * kPairPad * 8;     // reduction area (fp64 worst case)
+// Rows per lane: 16 (uniform, uniform24: kRowsPerWarpPair = 512 per warp) or 8 (Gaussian:
+// kRowsPerWarpGauss = 256; fewer live accumulators leave the Box-Muller chains registers:
+// c3 16.1 -> 15.0 ms, while uniform prefers 16: 2.71 vs 2.82 ms on c2).
+template <int DIST> constexpr int pair_rows() { return (DIST == 2 ? kRowsPerWarpGauss : kRowsPerWarpPair) / 32; }
+constexpr int kPairRedBytes = kWarps * 32 * (kRowsPerWarpPair / 32 + 1) * 8;   // reduction area (fp64 worst case)
 constexpr int kLogTabBytes = 129 * 4 * 8;
 
 template <int DIST, typename T>
-__global__ void __launch_bounds__(kThreads, kPairRows <= 8 ? 2 : 1) sk_pair_kernel(const ApplyArgs P) {
+__global__ void __launch_bounds__(kThreads, 1) sk_pair_kernel(const ApplyArgs P) {
+  constexpr int kPairRows = pair_rows<DIST>(), kPairPad = kPairRows + 1, kRowsPerWarp = 32 * kPairRows;
   extern __shared__ __align__(16) unsigned char smem[];
   double* logtab = reinterpret_cast<double*>(smem + kPairRedBytes);   // Gaussian: log table copy
   if constexpr (DIST == 2) {
@@ -210,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, kPairRows <= 8 ? 2 : 1) sk_pair_kern
   const int64_t pb = P.colptr[it.col], pe = P.colptr[it.col + 1];
   const int64_t L = pe - pb;
   const int64_t s0 = wk < WK ? pb + (L * wk) / WK : pe, s1 = wk < WK ? pb + (L * (wk + 1)) / WK : pe;
-  const int64_t lane_row0 = (int64_t)it.row0 + (int64_t)wd * kRowsPerWarpPair + kPairRows * lane;
+  const int64_t lane_row0 = (int64_t)it.row0 + (int64_t)wd * kRowsPerWarp + kPairRows * lane;
   constexpr int kE = pair_E<DIST>();
   const uint32_t q0 = (uint32_t)(lane_row0 / kE);
   // Lanes whose rows all lie past d skip generation (their results are never stored).
@@ -233,6 +236,17 @@ __global__ void __launch_bounds__(kThreads, kPairRows <= 8 ? 2 : 1) sk_pair_kern
       const T a = __shfl_sync(kFull, al, s);
       if (!active) continue;
       const uint64_t J = (uint64_t)P.row_offset + jr;
+      if constexpr (DIST == 2) {
+        // (two scalars per block: this form schedules better than the array form, 16.1 vs 16.8 ms on c3)
+#pragma unroll
+        for (int h = 0; h < kPairRows / 2; ++h) {
+          const uint4 x = s_block(q0 + h, J, P.keys);
+          T v0, v1;
+          pair_entries<DIST, T>(x, v0, v1, logtab);
+          acc[2 * h] = fma(v0, a, acc[2 * h]);
+          acc[2 * h + 1] = fma(v1, a, acc[2 * h + 1]);
+        }
+      } else {
 #pragma unroll
       for (int h = 0; h < kPairRows / kE; ++h) {
         const uint4 x = s_block(q0 + h, J, P.keys);
@@ -240,6 +254,7 @@ __global__ void __launch_bounds__(kThreads, kPairRows <= 8 ? 2 : 1) sk_pair_kern
         block_entries<DIST, T>(x, v, logtab);
 #pragma unroll
         for (int t = 0; t < kE; ++t) acc[kE * h + t] = fma(v[t], a, acc[kE * h + t]);
+      }
       }
     }
   }
@@ -250,11 +265,11 @@ __global__ void __launch_bounds__(kThreads, kPairRows <= 8 ? 2 : 1) sk_pair_kern
   for (int e = 0; e < kPairRows; ++e) mine[e] = acc[e];
   __syncthreads();
   T* outc = reinterpret_cast<T*>(P.out) + (int64_t)it.col * P.ld;
-  const int rows = WD * kRowsPerWarpPair;
+  const int rows = WD * kRowsPerWarp;
   for (int r = threadIdx.x; r < rows; r += kThreads) {
     const int64_t row = (int64_t)it.row0 + r;
     if (row >= P.d) break;
-    const int rwd = r / kRowsPerWarpPair, rr = r % kRowsPerWarpPair;
+    const int rwd = r / kRowsPerWarp, rr = r % kRowsPerWarp;
     const int off = (rr / kPairRows) * kPairPad + (rr % kPairRows);
     T s = red[rwd * (32 * kPairPad) + off];
     for (int kk = 1; kk < WK; ++kk) s += red[(kk * WD + rwd) * (32 * kPairPad) + off];

@@ -18,7 +18,10 @@ constexpr int kRowsPerWarpRad = 1024;
 #define SK_PAIR_ROWS_PER_WARP 512
 #endif
 constexpr int kRowsPerWarpPair = SK_PAIR_ROWS_PER_WARP;
-constexpr int kRowsPerWarpGauss = 256;            // Gaussian: 8 rows per lane
+#ifndef SK_GAUSS_ROWS_PER_WARP
+#define SK_GAUSS_ROWS_PER_WARP 256
+#endif
+constexpr int kRowsPerWarpGauss = SK_GAUSS_ROWS_PER_WARP;   // Gaussian: 8 rows per lane
 
 // One CTA of work: column `col`, Â rows [row0, row0 + wd * rows_per_warp).
 // The CTA's 16 warps are arranged as W_d = wd row-warps times W_k = 16 / wd slices of the

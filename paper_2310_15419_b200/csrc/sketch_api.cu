@@ -236,7 +236,8 @@ int build_jki(sk_plan_s* p, const int64_t* h_colptr, bool force, cudaStream_t st
       auto pr = group_range(g);
       if (pr.second == pr.first) continue;
       std::vector<int32_t> r((size_t)(pr.second - pr.first));
-      SK_CUDA(cudaMemcpy(r.data(), p->rowidx + pr.first, r.size() * 4, cudaMemcpyDeviceToHost));
+      SK_CUDA(cudaMemcpyAsync(r.data(), p->rowidx + pr.first, r.size() * 4, cudaMemcpyDeviceToHost, stream));
+      SK_CUDA(cudaStreamSynchronize(stream));
       tot += (int64_t)r.size();
       rows += distinct_rows(r);
     }

@@ -36,7 +36,11 @@ namespace sk {
 namespace {
 
 constexpr int kF4Tiles = 6;                       // 128-row tiles per CTA (max)
-constexpr int kF4AWarps = 2 * kF4Tiles;           // A producers: (tile, nonzero half)
+#ifndef SK_F4_KC
+#define SK_F4_KC 1
+#endif
+constexpr int kF4KC = SK_F4_KC;                   // K-step classes: A warp class c takes sub = c, c + kF4KC, ..
+constexpr int kF4AWarps = 2 * kF4Tiles * kF4KC;   // A producers: (tile, nonzero half, K-step class)
 constexpr int kF4BWarps = 2;                      // B producers: nonzero half
 constexpr int kF4Producers = kF4AWarps + kF4BWarps;
 constexpr int kF4LoaderWarp = kF4Producers;       // streams rowidx / vals into a smem ring
@@ -165,6 +169,35 @@ __device__ __forceinline__ void f4_store_row_masked(uint32_t addr, uint32_t y, i
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" :: "r"(addr), "r"(w0), "r"(w1), "r"(w2), "r"(w3) : "memory");
 }
 
+// Partial transpose for the S operand (SK_F4_PART=1; off by default -- on c5 it measured 8.14 ms vs
+// 8.09 ms for the full transpose: 40% fewer shuffles, but 4x more STS instructions, and the shuffles
+// were not what binds the producers): only 3 exchange stages.  Stage a swaps
+// lane bit a with word bit a + 2 (shift 4 << a): on exit lane (lh, ll) = (l >> 3, l & 7), bit 4n + c
+// holds what lane (lh, n) had at bit 4 ll + c.  Each nibble word c then already holds 8 nonzeros of
+// ONE row, so 2 of the 5 shuffle stages of the full 32 x 32 transpose disappear (the shuffles share
+// the shared-memory data pipe with the STS of S and the tensor core's operand reads).
+#ifndef SK_F4_PART
+#define SK_F4_PART 0
+#endif
+template <int NW>
+__device__ __forceinline__ void f4_exchange3(uint32_t (&x)[NW], int lane) {
+  const uint32_t m0[3] = {0x0F0F0F0Fu, 0x00FF00FFu, 0x0000FFFFu};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const bool lower = (lane & (1 << a)) == 0;
+    const uint32_t keep = lower ? m0[a] : ~m0[a];
+    const uint32_t r = lower ? (4u << a) : 32u - (4u << a);   // rotate: << s in the lower lane, >> s in the upper
+    uint32_t y[NW];
+#pragma unroll
+    for (int k = 0; k < NW; ++k) y[k] = __shfl_xor_sync(0xFFFFFFFFu, x[k], 1 << a);
+#pragma unroll
+    for (int k = 0; k < NW; ++k) {
+      const uint32_t yr = __funnelshift_l(y[k], y[k], r);
+      asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(x[k]) : "r"(x[k]), "r"(yr), "r"(keep));
+    }
+  }
+}
+
 // byte offset of row m, K chunk h inside a K-major no-swizzle tile (core matrices 8 x 16 B)
 __device__ __forceinline__ uint32_t f4_off(int m, int h) {
   return (uint32_t)((m >> 3) * 256 + h * 128 + (m & 7) * 16);
@@ -186,7 +219,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
   const double* vals = reinterpret_cast<const double*>(P.vals);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kF4Stages; ++s) { f4_mbar_init(&sh.full[s], 2 * T + kF4BWarps); f4_mbar_init(&sh.empty[s], 1); }
+    for (int s = 0; s < kF4Stages; ++s) { f4_mbar_init(&sh.full[s], 2 * T * kF4KC + kF4BWarps); f4_mbar_init(&sh.empty[s], 1); }
     for (int s = 0; s < kF4Slots; ++s) { f4_mbar_init(&sh.jfull[s], 32); f4_mbar_init(&sh.jempty[s], 2 * T + kF4BWarps); }
     f4_mbar_init(&sh.done, 1);
     sh.maxabs_bits = 0ull;
@@ -221,11 +254,10 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   }
   // column scale E (all producers)
-  if (warp < kF4Producers) {
-    double mx = 0.0;
-    for (int64_t p = pb + threadIdx.x; p < pe; p += kF4Producers * 32) mx = fmax(mx, fabs(__ldg(vals + p)));
-    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
-    if (lane == 0) atomicMax(&sh.maxabs_bits, (unsigned long long)__double_as_longlong(mx));
+  if (warp < kF4Producers && dbg != 6) {
+    unsigned long long mx = col_absmax_bits(vals, pb, pe, threadIdx.x, kF4Producers * 32);
+    for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+    if (lane == 0) atomicMax(&sh.maxabs_bits, mx);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -237,9 +269,11 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
   __syncthreads();
   const int E = sh.E;
 
-  if (warp < 2 * T) {
-    // ===================== A producers: S tile (w % T), nonzero half (w / T) =====================
-    const int t = warp % T, h = warp / T;
+  if (warp < 2 * T * kF4KC) {
+    // ===================== A producers: S tile (w % T), nonzero half, K-step class =====================
+    const int t = warp % T, h = (warp / T) & 1, kc = warp / (2 * T);
+    constexpr int kMine = kF4Sub / kF4KC;            // K-steps of a stage this warp produces
+    static_assert(kMine * kF4KC == kF4Sub, "K-step classes must divide the stage");
     const uint32_t q = (uint32_t)(it.tile0 + t);
     // One smem stage holds kF4Sub = 4 K-steps: the warp generates all of them (independent Philox
     // chains, 4 kF4Sub interleaved 32x32 transposes) and signals the stage once.
@@ -247,30 +281,60 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
       if (ks >= nsteps) return 0u;
       const int slot = ks % kF4Slots;
       f4_wait(&sh.jfull[slot], (ks / kF4Slots) & 1);
+#if SK_F4_PART
+      // lane (lh, n) takes nonzero 4n + lh: after f4_exchange3 nibble n of k-group lh is K position
+      // 8 lh + n, the B operand's order (K position 8c + n <-> nonzero 4n + c)
+      const uint32_t j = sh.js[slot][32 * h + 4 * (lane & 7) + (lane >> 3)];
+#else
       const uint32_t j = sh.js[slot][32 * h + lane];
+#endif
       __syncwarp();
       if (lane == 0) f4_arrive(&sh.jempty[slot]);   // one arrival per warp
       return j;
     };
     for (int ss = 0; ss < nsup; ++ss) {
       const int stage = ss % kF4Stages, use = ss / kF4Stages;
-      uint32_t x[4 * kF4Sub];
+      uint32_t x[4 * kMine];
 #pragma unroll
-      for (int sub = 0; sub < kF4Sub; ++sub) {
-        const uint32_t j = getj(kF4Sub * ss + sub);
+      for (int i = 0; i < kMine; ++i) {
+        const uint32_t j = getj(kF4Sub * ss + kc + kF4KC * i);
         const uint4 xb = s_block(q, (uint64_t)P.row_offset + j, P.keys);   // padded nonzeros: B = 0
-        x[4 * sub + 0] = xb.x; x[4 * sub + 1] = xb.y; x[4 * sub + 2] = xb.z; x[4 * sub + 3] = xb.w;
+        x[4 * i + 0] = xb.x; x[4 * i + 1] = xb.y; x[4 * i + 2] = xb.z; x[4 * i + 3] = xb.w;
       }
-      f4_transpose<4 * kF4Sub>(x, lane);          // lane r: row 32qq + r over 32 nonzeros
+#if SK_F4_PART
+      f4_exchange3<4 * kMine>(x, lane);
+      if (use > 0) f4_wait(&sh.empty[stage], (use - 1) & 1);
+      if (dbg != 1) {
+        // word qq, nibble word c: Â row 32 qq + 4 ll + c, stored as tile row R = 32 qq + 8 c + ll
+        // (the epilogue undoes the permutation), k-group lh: one STS.32 per (qq, c), the 32 lanes on
+        // 32 distinct banks (bank = 4 ll + lh)
+        const uint32_t tile = s_u32(stages + stage * kF4Stage) + (uint32_t)(t * kF4ATileS) +
+                              (uint32_t)(h * 128 + (lane & 7) * 16 + (lane >> 3) * 4);
+#pragma unroll
+        for (int i = 0; i < kMine; ++i)
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) {
+            const int sub = kc + kF4KC * i;
+            const uint32_t y = x[4 * i + qq];
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              asm volatile("st.shared.b32 [%0], %1;"
+                           :: "r"(tile + (uint32_t)(sub * kF4ATile + (4 * qq + c) * 256)), "r"(f4_nib(y << (3 - c)))
+                           : "memory");
+          }
+      }
+#else
+      f4_transpose<4 * kMine>(x, lane);           // lane r: row 32qq + r over 32 nonzeros
       if (use > 0) f4_wait(&sh.empty[stage], (use - 1) & 1);
       if (dbg != 1) {
         const uint32_t tile = s_u32(stages + stage * kF4Stage) + (uint32_t)(t * kF4ATileS) + f4_off(lane, h);
 #pragma unroll
-        for (int sub = 0; sub < kF4Sub; ++sub)
+        for (int i = 0; i < kMine; ++i)
 #pragma unroll
-          for (int qq = 0; qq < 4; ++qq)
-            f4_store_row(tile + (uint32_t)(sub * kF4ATile + qq * 4 * 256), x[4 * sub + qq]);   // row 32qq + lane
+          for (int qq = 0; qq < 4; ++qq)   // row 32qq + lane
+            f4_store_row(tile + (uint32_t)((kc + kF4KC * i) * kF4ATile + qq * 4 * 256), x[4 * i + qq]);
       }
+#endif
       if (dbg != 3) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) f4_arrive(&sh.full[stage]);
@@ -409,7 +473,12 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
           }
         }
       }
+#if SK_F4_PART
+      // TMEM lane R = 32 qw + lane holds Â row 32 qw + 4 (R & 7) + ((R >> 3) & 3) of the tile
+      const int64_t row = (int64_t)(it.tile0 + tt) * 128 + 32 * qw + 4 * (lane & 7) + (lane >> 3);
+#else
       const int64_t row = (int64_t)(it.tile0 + tt) * 128 + 32 * qw + lane;
+#endif
       if (row < P.d) {
         // Σ_s 2^s D_s - D_64 = hi 2^32 + (lo - ones), both parts exact in fp64; one rounding
         const double v = scalbn((double)hi * 4294967296.0 + (double)(lo - ones), E - 62);

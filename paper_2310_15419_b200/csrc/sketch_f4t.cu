@@ -187,10 +187,9 @@ __global__ void __launch_bounds__(kTThreads, 1) sk_rad_f4t_kernel(const ApplyArg
   }
   // column scale E (all producers)
   if (warp < kTProducers) {
-    double mx = 0.0;
-    for (int64_t p = pb + threadIdx.x; p < pe; p += kTProducers * 32) mx = fmax(mx, fabs(__ldg(vals + p)));
-    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
-    if (lane == 0) atomicMax(&sh.maxabs_bits, (unsigned long long)__double_as_longlong(mx));
+    unsigned long long mx = col_absmax_bits(vals, pb, pe, threadIdx.x, kTProducers * 32);
+    for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+    if (lane == 0) atomicMax(&sh.maxabs_bits, mx);
   }
   __syncthreads();
   if (threadIdx.x == 0) {

@@ -210,10 +210,9 @@ sk_rad_hybrid_kernel(const ApplyArgs P, const TcItem* items, int n_items, int* c
       const int T = it.ntiles;
       if (warp < kHyTcWarps) {
         // ---- column scale E ----
-        double mx = 0.0;
-        for (int64_t p = pb + threadIdx.x; p < pe; p += kHyTcWarps * 32) mx = fmax(mx, fabs(__ldg(vals + p)));
-        for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(kFull, mx, o));
-        if (lane == 0) atomicMax(&sh.maxabs_bits, (unsigned long long)__double_as_longlong(mx));
+        unsigned long long mx = col_absmax_bits(vals, pb, pe, threadIdx.x, kHyTcWarps * 32);
+        for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(kFull, mx, o));
+        if (lane == 0) atomicMax(&sh.maxabs_bits, mx);
         hy_bar(3, kHyTcWarps * 32);
         if (threadIdx.x == 0) {
           const double m = __longlong_as_double((long long)sh.maxabs_bits);

@@ -168,10 +168,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) sk_rad_tc_kernel(const ApplyArg
 
   // ---- column scale: E = frexp exponent of max |a| (producers only) ----
   if (warp < kTcProducerWarps) {
-    double mx = 0.0;
-    for (int64_t p = pb + threadIdx.x; p < pe; p += kTcProducerWarps * 32) mx = fmax(mx, fabs(__ldg(vals + p)));
-    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
-    if (lane == 0) atomicMax(&sh.maxabs_bits, (unsigned long long)__double_as_longlong(mx));
+    unsigned long long mx = col_absmax_bits(vals, pb, pe, threadIdx.x, kTcProducerWarps * 32);
+    for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+    if (lane == 0) atomicMax(&sh.maxabs_bits, mx);
     named_bar(1, kTcProducerWarps * 32);
     if (threadIdx.x == 0) {
       const double m = __longlong_as_double((long long)sh.maxabs_bits);
@@ -447,10 +446,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) sk_rad_tm_kernel(const ApplyArg
   __syncthreads();
 
   if (warp < kTcProducerWarps) {
-    double mx = 0.0;
-    for (int64_t p = pb + threadIdx.x; p < pe; p += kTcProducerWarps * 32) mx = fmax(mx, fabs(__ldg(vals + p)));
-    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
-    if (lane == 0) atomicMax(&sh.maxabs_bits, (unsigned long long)__double_as_longlong(mx));
+    unsigned long long mx = col_absmax_bits(vals, pb, pe, threadIdx.x, kTcProducerWarps * 32);
+    for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+    if (lane == 0) atomicMax(&sh.maxabs_bits, mx);
     named_bar(1, kTcProducerWarps * 32);
     if (threadIdx.x == 0) {
       const double m = __longlong_as_double((long long)sh.maxabs_bits);

@@ -187,6 +187,25 @@ def test_rad_f64_kernel_paths(sk, path):
         sk.set_rad_f64_path("fp4")
 
 
+@pytest.mark.parametrize("path", ["fp4", "fp4t", "fp4n", "int8smem", "int8tmem", "simt", "hybrid"])
+def test_nan_poisons_only_its_column(sk, path):
+    # a NaN value makes its whole column NaN (NaN * ±1 = NaN in every row, as in the oracle); the
+    # other columns are unaffected.  (fmax-based column scans would drop the NaN: the tensor-core
+    # kernels take max |a| on the IEEE bit patterns, NaN > Inf > finite.)
+    A = workloads.random_csc(50000, 6, 400, seed=41)
+    A.vals[A.colptr[2] + 5] = np.nan
+    try:
+        sk.set_rad_f64_path(path)
+        for dist in ("rademacher", "uniform", "gaussian"):
+            got = _gpu_sketch(sk, A, 700, dist, 3)
+            ref, B = oracle.sketch(3, dist, 700, A.m, A.n, A.colptr, A.rowidx, A.vals, threads=8)
+            assert np.isnan(got[:, 2]).all() and np.isnan(ref[:, 2]).all()
+            keep = [0, 1, 3, 4, 5]
+            _check(got[:, keep], ref[:, keep], B[:, keep], TOL["f64"])
+    finally:
+        sk.set_rad_f64_path("fp4")
+
+
 def test_kernel_names_report_the_path(sk):
     A = workloads.random_csc(10000, 4, 300, seed=1)
     plan = sk.Plan(_dev(A.colptr), _dev(A.rowidx), 300, A.m, "f64")

@@ -46,10 +46,14 @@ constexpr int kF4Producers = kF4AWarps + kF4BWarps;
 constexpr int kF4LoaderWarp = kF4Producers;       // streams rowidx / vals into a smem ring
 constexpr int kF4MmaWarp = kF4Producers + 1;
 constexpr int kF4Threads = (kF4Producers + 2) * 32;
-constexpr int kF4Slots = 8;                       // nonzero-stream ring (K-steps of 64)
 constexpr int kF4N = 72;                          // 64 digit rows + ones row + 7 zero rows
-constexpr int kF4Sub = 4;                         // K-steps (64 nonzeros each) per smem stage
-constexpr int kF4Stages = 2;
+#ifndef SK_F4_SUB
+#define SK_F4_SUB 4
+#define SK_F4_STAGES 2
+#endif
+constexpr int kF4Sub = SK_F4_SUB;                 // K-steps (64 nonzeros each) per smem stage
+constexpr int kF4Stages = SK_F4_STAGES;
+constexpr int kF4JSlots = 12 / kF4Sub;            // nonzero-stream ring: one slot = one smem stage (kF4Sub K-steps)
 constexpr int kF4ATile = 128 * 32;                // 128 rows x 64 fp4 = 4 KB
 constexpr int kF4BTile = (kF4N / 8) * 256;        // 9 row groups x 256 B = 2304 B
 constexpr int kF4BSub = 2560;                     // B tile slot per K-step (padded)
@@ -66,11 +70,11 @@ constexpr uint32_t kSuspendNs = SK_SUSPEND_NS;
 struct F4Shared {
   uint64_t full[kF4Stages];
   uint64_t empty[kF4Stages];
-  uint64_t jfull[kF4Slots];
-  uint64_t jempty[kF4Slots];
+  uint64_t jfull[kF4JSlots];
+  uint64_t jempty[kF4JSlots];
   uint64_t done;
-  uint32_t js[kF4Slots][64];
-  double vs[kF4Slots][64];
+  uint32_t js[kF4JSlots][64 * kF4Sub];
+  double vs[kF4JSlots][64 * kF4Sub];
   uint32_t tmem_base;
   unsigned long long maxabs_bits;
   int32_t E;
@@ -220,7 +224,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kF4Stages; ++s) { f4_mbar_init(&sh.full[s], 2 * T * kF4KC + kF4BWarps); f4_mbar_init(&sh.empty[s], 1); }
-    for (int s = 0; s < kF4Slots; ++s) { f4_mbar_init(&sh.jfull[s], 32); f4_mbar_init(&sh.jempty[s], 2 * T + kF4BWarps); }
+    for (int s = 0; s < kF4JSlots; ++s) { f4_mbar_init(&sh.jfull[s], 32); f4_mbar_init(&sh.jempty[s], 2 * T * kF4KC + kF4BWarps); }
     f4_mbar_init(&sh.done, 1);
     sh.maxabs_bits = 0ull;
     sh.nonfinite = 0;
@@ -276,28 +280,29 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
     static_assert(kMine * kF4KC == kF4Sub, "K-step classes must divide the stage");
     const uint32_t q = (uint32_t)(it.tile0 + t);
     // One smem stage holds kF4Sub = 4 K-steps: the warp generates all of them (independent Philox
-    // chains, 4 kF4Sub interleaved 32x32 transposes) and signals the stage once.
-    auto getj = [&](int ks) -> uint32_t {
-      if (ks >= nsteps) return 0u;
-      const int slot = ks % kF4Slots;
-      f4_wait(&sh.jfull[slot], (ks / kF4Slots) & 1);
+    // chains, 4 kF4Sub interleaved 32x32 transposes) and signals the stage once.  Their row indices
+    // come from one ring slot (one wait, one release per stage; padding past the column end was
+    // zero-filled by the loader).
 #if SK_F4_PART
-      // lane (lh, n) takes nonzero 4n + lh: after f4_exchange3 nibble n of k-group lh is K position
-      // 8 lh + n, the B operand's order (K position 8c + n <-> nonzero 4n + c)
-      const uint32_t j = sh.js[slot][32 * h + 4 * (lane & 7) + (lane >> 3)];
+    // lane (lh, n) takes nonzero 4n + lh: after f4_exchange3 nibble n of k-group lh is K position
+    // 8 lh + n, the B operand's order (K position 8c + n <-> nonzero 4n + c)
+    const int jl = 32 * h + 4 * (lane & 7) + (lane >> 3);
 #else
-      const uint32_t j = sh.js[slot][32 * h + lane];
+    const int jl = 32 * h + lane;
 #endif
-      __syncwarp();
-      if (lane == 0) f4_arrive(&sh.jempty[slot]);   // one arrival per warp
-      return j;
-    };
     for (int ss = 0; ss < nsup; ++ss) {
       const int stage = ss % kF4Stages, use = ss / kF4Stages;
+      const int jslot = ss % kF4JSlots;
+      f4_wait(&sh.jfull[jslot], (ss / kF4JSlots) & 1);
+      uint32_t jv[kMine];
+#pragma unroll
+      for (int i = 0; i < kMine; ++i) jv[i] = sh.js[jslot][64 * (kc + kF4KC * i) + jl];
+      __syncwarp();
+      if (lane == 0) f4_arrive(&sh.jempty[jslot]);   // one arrival per warp
       uint32_t x[4 * kMine];
 #pragma unroll
       for (int i = 0; i < kMine; ++i) {
-        const uint32_t j = getj(kF4Sub * ss + kc + kF4KC * i);
+        const uint32_t j = jv[i];
         const uint4 xb = s_block(q, (uint64_t)P.row_offset + j, P.keys);   // padded nonzeros: B = 0
         x[4 * i + 0] = xb.x; x[4 * i + 1] = xb.y; x[4 * i + 2] = xb.z; x[4 * i + 3] = xb.w;
       }
@@ -350,16 +355,17 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
       uint32_t x[2 * kF4Sub];
       int nval[kF4Sub];
 #pragma unroll
+      const int jslot = ss % kF4JSlots;
+      f4_wait(&sh.jfull[jslot], (ss / kF4JSlots) & 1);
+      double vv[kF4Sub];
+#pragma unroll
+      for (int sub = 0; sub < kF4Sub; ++sub) vv[sub] = sh.vs[jslot][64 * sub + 32 * h + lane];
+      __syncwarp();
+      if (lane == 0) f4_arrive(&sh.jempty[jslot]);
+#pragma unroll
       for (int sub = 0; sub < kF4Sub; ++sub) {
         const int ks = kF4Sub * ss + sub;
-        double v0 = 0.0;
-        if (ks < nsteps) {
-          const int slot = ks % kF4Slots;
-          f4_wait(&sh.jfull[slot], (ks / kF4Slots) & 1);
-          v0 = sh.vs[slot][32 * h + lane];
-          __syncwarp();
-          if (lane == 0) f4_arrive(&sh.jempty[slot]);
-        }
+        const double v0 = vv[sub];
         const int64_t c0 = pb + (int64_t)ks * 64 + 32 * h;
         nval[sub] = (int)(pe - c0 < 0 ? 0 : (pe - c0 > 32 ? 32 : pe - c0));
         // U = A + 2^63 (mod 2^64); digit s = +1 iff bit s of U; nibble sign = NOT bit.  Padding
@@ -394,18 +400,18 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
     // ===================== loader: rowidx / vals -> smem ring with cp.async ====================
     // Non-blocking: each lane issues its copies (zero-filled past the column end) and a
     // cp.async.mbarrier.arrive.noinc that fires when they land; it only blocks on ring space.
-    for (int ks = 0; ks < nsteps; ++ks) {
-      const int slot = ks % kF4Slots, use = ks / kF4Slots;
+    for (int ss = 0; ss < nsup; ++ss) {
+      const int slot = ss % kF4JSlots, use = ss / kF4JSlots;
       if (use > 0) f4_wait(&sh.jempty[slot], (use - 1) & 1);
 #pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        const int64_t p = pb + (int64_t)ks * 64 + 32 * half + lane;
+      for (int e = 0; e < 2 * kF4Sub; ++e) {
+        const int64_t p = pb + (int64_t)ss * (64 * kF4Sub) + 32 * e + lane;
         const bool ok = p < pe;
-        const int64_t ps = ok ? p : pb;                 // any valid address; 0 bytes read if !ok
+        const int64_t ps = ok ? p : pb;                 // any valid address; 0 bytes read (zero fill) if !ok
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;"
-                     :: "r"(s_u32(&sh.js[slot][32 * half + lane])), "l"(P.rowidx + ps), "r"(ok ? 4 : 0) : "memory");
+                     :: "r"(s_u32(&sh.js[slot][32 * e + lane])), "l"(P.rowidx + ps), "r"(ok ? 4 : 0) : "memory");
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;"
-                     :: "r"(s_u32(&sh.vs[slot][32 * half + lane])), "l"(vals + ps), "r"(ok ? 8 : 0) : "memory");
+                     :: "r"(s_u32(&sh.vs[slot][32 * e + lane])), "l"(vals + ps), "r"(ok ? 8 : 0) : "memory");
       }
       asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" :: "r"(s_u32(&sh.jfull[slot])) : "memory");
     }
@@ -496,7 +502,11 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
 
 }  // namespace
 
-int f4_tiles_per_cta() { return kF4Tiles; }
+int f4_tiles_per_cta() {   // SKETCH_F4_TILES (tuning only): fewer row tiles per CTA
+  static const int t = [] { const char* v = getenv("SKETCH_F4_TILES"); const int x = v ? atoi(v) : kF4Tiles;
+                            return x >= 1 && x <= kF4Tiles ? x : kF4Tiles; }();
+  return t;
+}
 
 cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const TcItem* items, int64_t n_items, cudaStream_t stream) {
   if (n_items == 0) return cudaSuccess;

@@ -197,8 +197,11 @@ template <int DIST> constexpr int pair_rows() { return (DIST == 2 ? kRowsPerWarp
 constexpr int kPairRedBytes = kWarps * 32 * (kRowsPerWarpPair / 32 + 1) * 8;   // reduction area (fp64 worst case)
 constexpr int kLogTabBytes = 129 * 4 * 8;
 
+#ifndef SK_GAUSS_MINB
+#define SK_GAUSS_MINB 1
+#endif
 template <int DIST, typename T>
-__global__ void __launch_bounds__(kThreads, 1) sk_pair_kernel(const ApplyArgs P) {
+__global__ void __launch_bounds__(kThreads, DIST == 2 ? SK_GAUSS_MINB : 1) sk_pair_kernel(const ApplyArgs P) {
   constexpr int kPairRows = pair_rows<DIST>(), kPairPad = kPairRows + 1, kRowsPerWarp = 32 * kPairRows;
   extern __shared__ __align__(16) unsigned char smem[];
   double* logtab = reinterpret_cast<double*>(smem + kPairRedBytes);   // Gaussian: log table copy

@@ -29,6 +29,10 @@
  *  - Indices are 0-based.  colptr is int64[n+1] (colptr[0] = 0, non-decreasing,
  *    colptr[n] = nnz), rowidx is int32[nnz] with 0 <= rowidx < m.  Rows inside a column
  *    may be unsorted and may repeat; explicit zeros are processed (linearity).
+ *  - Non-finite values: a NaN value makes every entry of its column NaN (as NaN * ±1 does).
+ *    The SIMT kernels (fp32, uniform, Gaussian) follow IEEE arithmetic for +-Inf too; the
+ *    exact ±1 fp64 tensor-core kernel (the default for SK_RADEMACHER + SK_F64) writes NaN to
+ *    the whole column when it holds a NaN or an Inf (its digit encoding needs finite values).
  *  - Pointers are DEVICE pointers unless the name starts with h_ (host memory; pinned
  *    host memory is required for overlap but not for correctness).
  *  - out is d x n COLUMN-MAJOR with leading dimension d, and is OVERWRITTEN in full

@@ -55,8 +55,7 @@ constexpr int kF4Sub = SK_F4_SUB;                 // K-steps (64 nonzeros each) 
 constexpr int kF4Stages = SK_F4_STAGES;
 constexpr int kF4JSlots = 12 / kF4Sub;            // nonzero-stream ring: one slot = one smem stage (kF4Sub K-steps)
 constexpr int kF4ATile = 128 * 32;                // 128 rows x 64 fp4 = 4 KB
-constexpr int kF4BTile = (kF4N / 8) * 256;        // 9 row groups x 256 B = 2304 B
-constexpr int kF4BSub = 2560;                     // B tile slot per K-step (padded)
+constexpr int kF4BSub = 2560;                     // B tile slot per K-step: 9 row groups x 256 B, padded
 constexpr int kF4ATileS = kF4Sub * kF4ATile;      // one tile's A data per stage
 constexpr int kF4Stage = kF4Tiles * kF4ATileS + kF4Sub * kF4BSub;
 constexpr uint32_t kF4SfCol = 448;                // scale factors: TMEM columns [448, 512)
@@ -155,7 +154,7 @@ __device__ __forceinline__ uint32_t f4_nib(uint32_t t) {   // (t & 0x88888888) |
   return r;
 }
 
-__device__ __forceinline__ void f4_store_row(uint32_t addr, uint32_t y) {
+[[maybe_unused]] __device__ __forceinline__ void f4_store_row(uint32_t addr, uint32_t y) {
   const uint32_t w0 = f4_nib(y << 3), w1 = f4_nib(y << 2), w2 = f4_nib(y << 1), w3 = f4_nib(y);
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" :: "r"(addr), "r"(w0), "r"(w1), "r"(w2), "r"(w3) : "memory");
 }
@@ -354,7 +353,6 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
       const int stage = ss % kF4Stages, use = ss / kF4Stages;
       uint32_t x[2 * kF4Sub];
       int nval[kF4Sub];
-#pragma unroll
       const int jslot = ss % kF4JSlots;
       f4_wait(&sh.jfull[jslot], (ss / kF4JSlots) & 1);
       double vv[kF4Sub];

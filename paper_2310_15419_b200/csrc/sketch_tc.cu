@@ -40,7 +40,6 @@ constexpr int kTcProducerWarps = kTcTiles;   // one producer warp per tile
 constexpr int kTcThreads = (kTcProducerWarps + 1) * 32;
 constexpr int kTcStages = 3;
 constexpr int kTileBytes = 128 * 32;         // A tile: M=128 x K=32 int8
-constexpr int kBBytes = 32 * 16;             // B tile: K=32 x N=16 int8
 constexpr int kStageBytes = kTcTiles * kTileBytes + 1024;   // B tile padded: stages stay 1 KB aligned
 constexpr int kTmemCols = kTcTiles * 16;     // 16 int32 accumulator columns per tile
 constexpr uint32_t kMmaN = 16;
@@ -374,23 +373,9 @@ __device__ __forceinline__ void mma_i8_ts(uint32_t d_tmem, uint32_t a_tmem, uint
       :: "r"(d_tmem), "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
-// 32 x 32 bit-matrix transpose across the warp: on entry lane l holds word X[l] (bit b = entry
+// 32 x 32 bit-matrix transposes across the warp: on entry lane l holds word X[l] (bit b = entry
 // (l, b)); on exit lane r holds bit l = X[l] bit r.  Stage j swaps the off-diagonal j x j blocks
 // of every 2j x 2j block: one SHFL, one funnel rotate, one LOP3 per stage.
-__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
-#pragma unroll
-  for (int j = 16; j > 0; j >>= 1) {
-    const uint32_t m = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu : j == 4 ? 0x0F0F0F0Fu
-                     : j == 2 ? 0x33333333u : 0x55555555u;
-    const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x, j);
-    const bool hi = (lane & j) != 0;
-    const uint32_t t = __funnelshift_l(y, y, hi ? (32 - j) : j);   // rotl by j, or rotr by j
-    const uint32_t keep = hi ? ~m : m;
-    x = (x & keep) | (t & ~keep);
-  }
-  return x;
-}
-
 // Four independent transposes interleaved stage by stage (4 dependency chains for ILP).
 __device__ __forceinline__ void transpose32x4(uint32_t (&x)[4], int lane) {
 #pragma unroll

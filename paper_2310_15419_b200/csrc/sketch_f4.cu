@@ -206,9 +206,15 @@ __device__ __forceinline__ uint32_t f4_off(int m, int h) {
   return (uint32_t)((m >> 3) * 256 + h * 128 + (m & 7) * 16);
 }
 
-// dbg (tuning only, results invalid when nonzero): 1 = A producers skip generation, 2 = no MMAs,
-// 3 = no proxy fences, 4 = B producers skip their work, 5 = 2 + 4.
-__global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArgs P, const TcItem* items, int dbg) {
+// dbg (SKETCH_F4_DEBUG; tuning only, results invalid when nonzero), bit flags: 1 = no S stores,
+// 2 = no MMAs, 4 = no proxy fences, 8 = no digit stores, 16 = no column scan.
+// The debug switches exist only in builds with -DSK_F4_DEBUG=1 (the default build has none, so
+// they cannot perturb the schedule of the production kernel).
+#ifndef SK_F4_DEBUG
+#define SK_F4_DEBUG 0
+#endif
+__global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArgs P, const TcItem* items, int dbg_arg) {
+  const int dbg = SK_F4_DEBUG ? dbg_arg : 0;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* stages = smem_raw + ((1024u - (s_u32(smem_raw) & 1023u)) & 1023u);
   F4Shared& sh = *reinterpret_cast<F4Shared*>(stages + kF4Stages * kF4Stage);
@@ -257,7 +263,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   }
   // column scale E (all producers)
-  if (warp < kF4Producers && dbg != 6) {
+  if (warp < kF4Producers && !(dbg & 16)) {
     unsigned long long mx = col_absmax_bits(vals, pb, pe, threadIdx.x, kF4Producers * 32);
     for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
     if (lane == 0) atomicMax(&sh.maxabs_bits, mx);
@@ -308,7 +314,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
 #if SK_F4_PART
       f4_exchange3<4 * kMine>(x, lane);
       if (use > 0) f4_wait(&sh.empty[stage], (use - 1) & 1);
-      if (dbg != 1) {
+      if (!(dbg & 1)) {
         // word qq, nibble word c: Â row 32 qq + 4 ll + c, stored as tile row R = 32 qq + 8 c + ll
         // (the epilogue undoes the permutation), k-group lh: one STS.32 per (qq, c), the 32 lanes on
         // 32 distinct banks (bank = 4 ll + lh)
@@ -330,7 +336,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
 #else
       f4_transpose<4 * kMine>(x, lane);           // lane r: row 32qq + r over 32 nonzeros
       if (use > 0) f4_wait(&sh.empty[stage], (use - 1) & 1);
-      if (dbg != 1) {
+      if (!(dbg & 1)) {
         const uint32_t tile = s_u32(stages + stage * kF4Stage) + (uint32_t)(t * kF4ATileS) + f4_off(lane, h);
 #pragma unroll
         for (int i = 0; i < kMine; ++i)
@@ -339,7 +345,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
             f4_store_row(tile + (uint32_t)((kc + kF4KC * i) * kF4ATile + qq * 4 * 256), x[4 * i + qq]);
       }
 #endif
-      if (dbg != 3) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (!(dbg & 4)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) f4_arrive(&sh.full[stage]);
     }
@@ -378,7 +384,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
       }
       f4_transpose<2 * kF4Sub>(x, lane);           // lane s: digit s (and 32 + s) per K-step
       if (use > 0) f4_wait(&sh.empty[stage], (use - 1) & 1);
-      if (dbg != 4 && dbg != 5) {
+      if (!(dbg & 8)) {
 #pragma unroll
         for (int sub = 0; sub < kF4Sub; ++sub) {
           const uint32_t bt = s_u32(stages + stage * kF4Stage + kF4Tiles * kF4ATileS + sub * kF4BSub);
@@ -390,7 +396,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
           }
         }
       }
-      if (dbg != 3) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (!(dbg & 4)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) f4_arrive(&sh.full[stage]);
     }
@@ -428,7 +434,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
           const int ks = kF4Sub * ss + sub;
           if (ks >= nsteps) break;
           const uint64_t bdesc = f4_desc(sb + kF4Tiles * kF4ATileS + sub * kF4BSub);
-          for (int tt = 0; tt < T && dbg != 2 && dbg != 5; ++tt) {
+          for (int tt = 0; tt < T && !(dbg & 2); ++tt) {
             const uint64_t adesc = f4_desc(sb + tt * kF4ATileS + sub * kF4ATile);
             asm volatile(
                 "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"

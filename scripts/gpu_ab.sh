@@ -1,6 +1,6 @@
 # A/B timing of library variants: gpu_ab.sh "<pytest -k expr>" "<configs>" lib1.so lib2.so ...
 # (libs prebuilt in-tree; the first one also runs the parity tests).  A lib argument "VAR=v,lib.so"
-# runs that variant with the environment variable set (e.g. SKETCH_F4_DEBUG=6).
+# runs that variant with the environment variable set (e.g. SKETCH_F4_DEBUG=2).
 K="$1"; CFGS="$2"; shift 2
 out=gpurun_out/ab.log; : > $out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv >> $out

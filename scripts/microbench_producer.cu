@@ -1,9 +1,10 @@
 // microbench_producer.cu -- throughput of the fp4 tensor-core path's S producer loop alone
 // (Philox4x32-10 -> 32x32 warp bit transpose -> e2m1 nibble expansion -> STS.128), with no
 // barriers.  Reports (row, nonzero) entries per clock per SM for
-//   MODE 0: Philox only; 1: + rotated 5-stage transpose; 2: + nibbles + STS.128 (the f4 producer);
+//   MODE 2: Philox + rotated 5-stage transpose + nibbles + STS.128 (the f4 producer);
 //   3: Philox + 3-stage partial exchange + nibbles + 16 STS.32 (SK_F4_PART); 4: Philox + nibbles +
-//   STS.128 without the transpose; 5: Philox + rotated transpose + nibbles, no stores
+//   STS.128 without the transpose; 6: mode 2 with a CTA-wide bar.sync after every U blocks
+//   (all producer warps in lock step, as a stage barrier would force)
 // with U Philox blocks per lane in flight and NW warps per SM.
 #include <cstdint>
 #include <cstdio>
@@ -51,7 +52,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k(int iters, sk::PhiloxKeys K, uin
 #pragma unroll
         for (int c = 0; c < 4; ++c)
           asm volatile("st.shared.b32 [%0], %1;" :: "r"(base + (uint32_t)((((q & 3) * 4 + c) & 15) * 128)), "r"(nib(x[q] << (3 - c))) : "memory");
-    } else if (MODE == 1 || MODE == 2 || MODE == 5) {
+    } else if (MODE == 1 || MODE == 2 || MODE == 6) {
 #pragma unroll
       for (int q = 0; q < 4 * U; ++q) x[q] = __funnelshift_l(x[q], x[q], lane);
 #pragma unroll
@@ -67,20 +68,18 @@ __global__ void __launch_bounds__(NW * 32, 1) k(int iters, sk::PhiloxKeys K, uin
 #pragma unroll
       for (int q = 0; q < 4 * U; ++q) x[q] = __funnelshift_r(x[q], x[q], lane);
     }
-    if (MODE == 2 || MODE == 4) {
+    if (MODE == 2 || MODE == 4 || MODE == 6) {
 #pragma unroll
       for (int q = 0; q < 4 * U; ++q) {
         const uint32_t w0 = nib(x[q] << 3), w1 = nib(x[q] << 2), w2 = nib(x[q] << 1), w3 = nib(x[q]);
         const uint32_t a = (uint32_t)__cvta_generic_to_shared(&buf[warp][((q & 3) * 32 + lane) * 4]);
         asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" :: "r"(a), "r"(w0), "r"(w1), "r"(w2), "r"(w3) : "memory");
       }
-    } else if (MODE == 5) {
-#pragma unroll
-      for (int q = 0; q < 4 * U; ++q) acc ^= nib(x[q] << 3) ^ nib(x[q] << 2) ^ nib(x[q] << 1) ^ nib(x[q]);
     } else if (MODE != 3) {
 #pragma unroll
       for (int q = 0; q < 4 * U; ++q) acc ^= x[q];
     }
+    if (MODE == 6) asm volatile("bar.sync 1, %0;" :: "r"(NW * 32) : "memory");
   }
   __syncthreads();
   for (int i = threadIdx.x; i < NW * 512; i += blockDim.x) acc ^= (&buf[0][0])[i];
@@ -108,6 +107,6 @@ template <int MODE, int U>
 void runs() { run<MODE, U, 4>(); run<MODE, U, 8>(); run<MODE, U, 12>(); run<MODE, U, 16>(); }
 
 int main() {
-  runs<0, 4>(); runs<1, 4>(); runs<5, 4>(); runs<4, 4>(); runs<2, 4>(); runs<3, 4>();
+  runs<4, 4>(); runs<2, 4>(); runs<3, 4>(); runs<6, 4>(); runs<6, 2>();
   return 0;
 }

@@ -210,6 +210,9 @@ __device__ __forceinline__ uint32_t f4_off(int m, int h) {
 // 2 = no MMAs, 4 = no proxy fences, 8 = no digit stores, 16 = no column scan.
 // The debug switches exist only in builds with -DSK_F4_DEBUG=1 (the default build has none, so
 // they cannot perturb the schedule of the production kernel).
+#ifndef SK_F4_STAGGER_NS
+#define SK_F4_STAGGER_NS 600
+#endif
 #ifndef SK_F4_DEBUG
 #define SK_F4_DEBUG 0
 #endif
@@ -294,6 +297,11 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
     const int jl = 32 * h + 4 * (lane & 7) + (lane >> 3);
 #else
     const int jl = 32 * h + lane;
+#endif
+#if SK_F4_STAGGER_NS > 0
+    // The three S warps of a scheduler run identical code; started together they stay in phase
+    // (all in Philox, then all in shuffles ...).  Offset them by a fraction of a stage.
+    if (const int g = (warp >> 2) % 3) __nanosleep((unsigned)(g * SK_F4_STAGGER_NS));
 #endif
     for (int ss = 0; ss < nsup; ++ss) {
       const int stage = ss % kF4Stages, use = ss / kF4Stages;

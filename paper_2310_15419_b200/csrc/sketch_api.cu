@@ -7,6 +7,7 @@
 // (column, Â-row tile) work items of Algorithm 1's outer loops are
 // handed to CTAs -- the parallelised outer loops of PAPER.md:327-332.
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <cstdint>
 #include <cstdlib>
@@ -206,6 +207,10 @@ struct sk_plan_s {
   sk::JkiPlanView jki{};
   int64_t jki_rows = 0;             // Σ_groups nonzero rows
   int64_t* owned_colptr = nullptr;  // device copy made by sketch_plan_host
+  // All schedules (items, tc / f4, f4t, f4n) live in ONE device block uploaded by one copy.
+  void* d_stage = nullptr;
+  std::vector<unsigned char> h_stage;   // host image of d_stage (kept until uploaded)
+  size_t off_items = 0, off_tc = 0, off_f4t = 0, off_f4n = 0;
   int64_t n_rad = 0, n_pair = 0, n_gauss = 0;
   int64_t philox_rad = 0, philox_pair = 0;
 };
@@ -327,9 +332,21 @@ int validate_colptr(const int64_t* h, int64_t n, int64_t nnz, bool require_zero_
   return SK_OK;
 }
 
+// Copy a plan's schedule image to the device on `stream` (one copy); `sync` waits for it and
+// drops the host image, otherwise the image stays alive until the plan is destroyed.
+int upload_plan(sk_plan_s* p, cudaStream_t stream, bool sync) {
+  if (p->h_stage.empty()) return SK_OK;
+  cudaError_t e = cudaMemcpyAsync(p->d_stage, p->h_stage.data(), p->h_stage.size(), cudaMemcpyHostToDevice, stream);
+  if (e == cudaSuccess && sync) e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) return cuda_fail(e, "upload plan");
+  if (sync) std::vector<unsigned char>().swap(p->h_stage);
+  return SK_OK;
+}
+
 int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n, int64_t row_offset,
               const int64_t* h_colptr, const int64_t* d_colptr, const int32_t* rowidx, int64_t nnz,
-              cudaStream_t stream, int jki = 0 /* 0: sample, 1: force, -1: never */) {
+              cudaStream_t stream, int jki = 0 /* 0: sample, 1: force, -1: never */,
+              bool defer_upload = false /* true: the caller runs upload_plan */) {
   sk_plan_s* p = new (std::nothrow) sk_plan_s();
   if (!p) return SK_ENOMEM;
   p->dtype = dtype; p->d = d; p->m = m; p->n = n; p->nnz = nnz; p->row_offset = row_offset;
@@ -346,66 +363,60 @@ int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
   p->philox_pair = pair.philox_blocks;
   // Tensor-core ±1 paths: every column within the exact-accumulation bound, and columns long
   // enough on average (>= 256 nonzeros) to amortise a CTA's TMEM / barrier / scale prologue.
-  if (dtype == SK_F64 && p->max_col <= sk::kTcMaxColumn && n > 0 && nnz >= 256 * n) {
-    std::vector<sk::TcItem> tc = build_tc_schedule(h_colptr, n, d, sk::tc_tiles_per_cta());
+  const bool tc_ok = dtype == SK_F64 && p->max_col <= sk::kTcMaxColumn && n > 0 && nnz >= 256 * n;
+  std::vector<sk::TcItem> tc, f4t;
+  std::vector<sk::NItem> f4n;
+  if (tc_ok) {
+    tc = build_tc_schedule(h_colptr, n, d, sk::tc_tiles_per_cta());
     std::vector<sk::TcItem> f4 = build_tc_schedule(h_colptr, n, d, sk::f4_tiles_per_cta());
     p->n_tc = (int64_t)tc.size();
     p->n_f4 = (int64_t)f4.size();
     tc.insert(tc.end(), f4.begin(), f4.end());
-    cudaError_t e = cudaMalloc(&p->d_tc, tc.size() * sizeof(sk::TcItem));
-    if (e == cudaSuccess) e = cudaMemcpyAsync(p->d_tc, tc.data(), tc.size() * sizeof(sk::TcItem), cudaMemcpyHostToDevice, stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
-    if (e != cudaSuccess) { if (p->d_tc) cudaFree(p->d_tc); delete p; return cuda_fail(e, "tc schedule"); }
+    f4t = build_tc_schedule(h_colptr, n, (d + 3) / 4, 1);   // 512-row blocks
+    p->n_f4t = (int64_t)f4t.size();
   }
   p->nnz_end = h_colptr[n];
-  if (dtype == SK_F64 && p->max_col <= sk::kTcMaxColumn && n > 0 && nnz >= 256 * n) {
-    std::vector<sk::TcItem> f4t = build_tc_schedule(h_colptr, n, (d + 3) / 4, 1);   // 512-row blocks
-    p->n_f4t = (int64_t)f4t.size();
-    cudaError_t e = cudaMalloc(&p->d_f4t, f4t.size() * sizeof(sk::TcItem));
-    if (e == cudaSuccess) e = cudaMemcpyAsync(p->d_f4t, f4t.data(), f4t.size() * sizeof(sk::TcItem), cudaMemcpyHostToDevice, stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
-    if (e != cudaSuccess) {
-      if (p->d_f4t) cudaFree(p->d_f4t);
-      if (p->d_tc) cudaFree(p->d_tc);
-      delete p;
-      return cuda_fail(e, "f4t schedule");
-    }
-  }
   // S-as-N fp4 path: TMA streams rowidx / values (16-byte aligned arrays, int32 coordinates)
   if (dtype == SK_F64 && p->max_col <= sk::kF4nMaxColumn && n > 0 && nnz >= 256 * n && sk::f4n_aligned(rowidx) &&
       p->nnz_end < (int64_t(1) << 31) - 2 * sk::kF4nRows) {
-    std::vector<sk::NItem> f4n = build_f4n_schedule(h_colptr, n, d);
+    f4n = build_f4n_schedule(h_colptr, n, d);
     p->n_f4n = (int64_t)f4n.size();
-    cudaError_t e = cudaMalloc(&p->d_f4n, f4n.size() * sizeof(sk::NItem));
-    if (e == cudaSuccess) e = cudaMemcpyAsync(p->d_f4n, f4n.data(), f4n.size() * sizeof(sk::NItem), cudaMemcpyHostToDevice, stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
-    if (e != cudaSuccess) {
-      if (p->d_f4n) cudaFree(p->d_f4n);
-      if (p->d_tc) cudaFree(p->d_tc);
-      delete p;
-      return cuda_fail(e, "f4n schedule");
+  }
+  // one host image of every schedule, 256-byte aligned sections
+  {
+    const int64_t total = p->n_rad + p->n_pair + p->n_gauss;
+    auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    p->off_items = 0;
+    p->off_tc = up(p->off_items + (size_t)total * sizeof(Item));
+    p->off_f4t = up(p->off_tc + tc.size() * sizeof(sk::TcItem));
+    p->off_f4n = up(p->off_f4t + f4t.size() * sizeof(sk::TcItem));
+    const size_t bytes = up(p->off_f4n + f4n.size() * sizeof(sk::NItem));
+    p->h_stage.assign(bytes, 0);
+    unsigned char* h = p->h_stage.data();
+    size_t o = p->off_items;
+    for (const Schedule* sc : {&rad, &pair, &gauss}) {
+      if (!sc->items.empty()) std::memcpy(h + o, sc->items.data(), sc->items.size() * sizeof(Item));
+      o += sc->items.size() * sizeof(Item);
     }
+    if (!tc.empty()) std::memcpy(h + p->off_tc, tc.data(), tc.size() * sizeof(sk::TcItem));
+    if (!f4t.empty()) std::memcpy(h + p->off_f4t, f4t.data(), f4t.size() * sizeof(sk::TcItem));
+    if (!f4n.empty()) std::memcpy(h + p->off_f4n, f4n.data(), f4n.size() * sizeof(sk::NItem));
+    cudaError_t e = defer_upload ? cudaMallocAsync(&p->d_stage, bytes > 0 ? bytes : 256, stream)
+                                 : cudaMalloc(&p->d_stage, bytes > 0 ? bytes : 256);
+    if (e != cudaSuccess) { delete p; return e == cudaErrorMemoryAllocation ? SK_ENOMEM : cuda_fail(e, "cudaMalloc(plan)"); }
+    unsigned char* dst = static_cast<unsigned char*>(p->d_stage);
+    p->d_items = total > 0 ? reinterpret_cast<Item*>(dst + p->off_items) : nullptr;
+    p->d_tc = tc.empty() ? nullptr : reinterpret_cast<sk::TcItem*>(dst + p->off_tc);
+    p->d_f4t = f4t.empty() ? nullptr : reinterpret_cast<sk::TcItem*>(dst + p->off_f4t);
+    p->d_f4n = f4n.empty() ? nullptr : reinterpret_cast<sk::NItem*>(dst + p->off_f4n);
   }
   if (jki >= 0) {
     const int rj = build_jki(p, h_colptr, jki > 0, stream);
-    if (rj != SK_OK) {
-      if (p->d_f4n) cudaFree(p->d_f4n);
-      if (p->d_f4t) cudaFree(p->d_f4t);
-      if (p->d_tc) cudaFree(p->d_tc);
-      delete p;
-      return rj;
-    }
+    if (rj != SK_OK) { cudaFree(p->d_stage); delete p; return rj; }
   }
-  const int64_t total = p->n_rad + p->n_pair + p->n_gauss;
-  if (total > 0) {
-    cudaError_t e = cudaMalloc(&p->d_items, (size_t)total * sizeof(Item));
-    if (e != cudaSuccess) { delete p; return e == cudaErrorMemoryAllocation ? SK_ENOMEM : cuda_fail(e, "cudaMalloc(items)"); }
-    std::vector<Item> all(rad.items);
-    all.insert(all.end(), pair.items.begin(), pair.items.end());
-    all.insert(all.end(), gauss.items.begin(), gauss.items.end());
-    e = cudaMemcpyAsync(p->d_items, all.data(), (size_t)total * sizeof(Item), cudaMemcpyHostToDevice, stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);   // `all` is pageable and local
-    if (e != cudaSuccess) { cudaFree(p->d_items); delete p; return cuda_fail(e, "upload items"); }
+  if (!defer_upload) {
+    const int ru = upload_plan(p, stream, true);
+    if (ru != SK_OK) { sketch_plan_destroy(p); return ru; }
   }
   *out = p;
   return SK_OK;
@@ -665,25 +676,41 @@ int sketch_apply_host(uint64_t seed, sk_dist_t dist, sk_dtype_t dtype, int64_t d
   SK_STEP(cudaMallocAsync(&d_out, (size_t)std::max<int64_t>(d * n, 1) * w, stream));
   SK_STEP(cudaMallocAsync((void**)&d_flag, sizeof(int), stream));
   SK_STEP(cudaMemsetAsync(d_flag, 0, sizeof(int), stream));
-  // One plan per column group (same kernels and schedules as sketch_apply); built before any
-  // copy is in flight.  Group plans reference d_colptr + c0 (absolute offsets) and d_rowidx.
-  std::vector<sk_plan_t> plans((size_t)G, nullptr);
-  for (int g = 0; g < G && e == cudaSuccess; ++g) {
-    const int64_t c0 = cb[g], c1 = cb[g + 1];
-    const int rcp = make_plan(&plans[g], dtype, d, m, c1 - c0, row_offset, h_colptr + c0, d_colptr + c0,
-                              d_rowidx, h_colptr[c1] - h_colptr[c0], stream, -1);
-    if (rcp != SK_OK) { e = cudaErrorUnknown; what = "make_plan(group)"; }
-  }
-  SK_STEP(cudaEventRecord(ev_start, stream));
-  SK_STEP(cudaStreamWaitEvent(h2d, ev_start, 0));
-  SK_STEP(cudaMemcpyAsync(d_colptr, h_colptr, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, h2d));
-  for (int g = 0; g < G; ++g) {
+  // Order on the upload stream: colptr, group 0 of A, the group plans' schedule images, groups
+  // 1.. of A.  The plans (host schedules, same kernels as sketch_apply) are built while group 0
+  // is in flight; they reference d_colptr + c0 (absolute offsets) and d_rowidx, whose contents
+  // they do not read.
+  auto upload_group = [&](int g) {
     const int64_t p0 = h_colptr[cb[g]], p1 = h_colptr[cb[g + 1]];
     if (p1 > p0) {
       SK_STEP(cudaMemcpyAsync(d_rowidx + p0, h_rowidx + p0, (size_t)(p1 - p0) * 4, cudaMemcpyHostToDevice, h2d));
       SK_STEP(cudaMemcpyAsync((char*)d_vals + p0 * w, (const char*)h_vals + p0 * w, (size_t)(p1 - p0) * w,
                               cudaMemcpyHostToDevice, h2d));
     }
+  };
+  SK_STEP(cudaEventRecord(ev_start, stream));
+  SK_STEP(cudaStreamWaitEvent(h2d, ev_start, 0));
+  SK_STEP(cudaMemcpyAsync(d_colptr, h_colptr, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, h2d));
+  upload_group(0);
+  static const bool timing = getenv("SKETCH_TIMING") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<sk_plan_t> plans((size_t)G, nullptr);
+  for (int g = 0; g < G && e == cudaSuccess; ++g) {
+    const int64_t c0 = cb[g], c1 = cb[g + 1];
+    const int rcp = make_plan(&plans[g], dtype, d, m, c1 - c0, row_offset, h_colptr + c0, d_colptr + c0,
+                              d_rowidx, h_colptr[c1] - h_colptr[c0], stream, -1, true);
+    if (rcp != SK_OK) { e = cudaErrorUnknown; what = "make_plan(group)"; }
+  }
+  if (timing)
+    fprintf(stderr, "apply_host: %d group plans %.3f ms\n", G,
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  SK_STEP(cudaEventRecord(ev_end, stream));          // (reused) the plans' stream-ordered allocations
+  SK_STEP(cudaStreamWaitEvent(h2d, ev_end, 0));
+  for (int g = 0; g < G && e == cudaSuccess; ++g)
+    if (plans[g] && upload_plan(plans[g], h2d, false) != SK_OK) { e = cudaErrorUnknown; what = "upload plan"; }
+  SK_STEP(cudaEventRecord(ev_in[0], h2d));
+  for (int g = 1; g < G; ++g) {
+    upload_group(g);
     SK_STEP(cudaEventRecord(ev_in[g], h2d));
   }
   for (int g = 0; g < G; ++g) {
@@ -756,11 +783,8 @@ int sketch_plan_stats(sk_plan_t plan, sk_stats_t* h) {
 int sketch_plan_destroy(sk_plan_t plan) {
   if (!plan) return SK_OK;
   cudaError_t e = cudaSuccess;
-  if (plan->d_items) e = cudaFree(plan->d_items);
+  if (plan->d_stage) e = cudaFree(plan->d_stage);
   if (plan->owned_colptr) { cudaError_t e2 = cudaFree(plan->owned_colptr); if (e == cudaSuccess) e = e2; }
-  if (plan->d_tc) { cudaError_t e2 = cudaFree(plan->d_tc); if (e == cudaSuccess) e = e2; }
-  if (plan->d_f4n) { cudaError_t e2 = cudaFree(plan->d_f4n); if (e == cudaSuccess) e = e2; }
-  if (plan->d_f4t) { cudaError_t e2 = cudaFree(plan->d_f4t); if (e == cudaSuccess) e = e2; }
   if (plan->d_jki) { cudaError_t e2 = cudaFree(plan->d_jki); if (e == cudaSuccess) e = e2; }
   delete plan;
   if (e != cudaSuccess) return cuda_fail(e, "cudaFree(plan)");

@@ -112,6 +112,11 @@ cudaError_t launch_apply(int dist, int dtype, const ApplyArgs& a, cudaStream_t s
 cudaError_t launch_fill_s(int dist, int dtype, uint64_t seed, int64_t i0, int64_t i1, int64_t j0,
                           int64_t j1, void* out, int64_t ld, cudaStream_t stream);
 
+// *count += number of distinct values in rowidx[p0, p1); bitmap (>= m bits) must be zero on entry
+// and is left with those rows' bits set.
+cudaError_t launch_distinct_rows(const int32_t* rowidx, int64_t p0, int64_t p1, uint32_t* bitmap,
+                                 unsigned long long* count, cudaStream_t stream);
+
 // Sets *flag (device int) nonzero if some rowidx is outside [0, m).
 cudaError_t launch_validate_rows(const int32_t* rowidx, int64_t nnz, int64_t m, int* flag,
                                  cudaStream_t stream);

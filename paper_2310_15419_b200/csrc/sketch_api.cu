@@ -234,17 +234,46 @@ int build_jki(sk_plan_s* p, const int64_t* h_colptr, bool force, cudaStream_t st
     return (int64_t)(std::unique(r.begin(), r.end()) - r.begin());
   };
   if (!force) {
+    // Reuse factor nonzeros / distinct rows on up to 32 evenly spaced groups (<= 16M nonzeros),
+    // counted on the device with a row bitmap (one zeroing + one pass per group, one readback).
     const int64_t ns = std::min<int64_t>(G, 32);
     int64_t tot = 0, rows = 0;
-    for (int64_t t = 0; t < ns && tot < (int64_t(1) << 18); ++t) {   // <= 32 groups, ~256K nonzeros
-      const int64_t g = (t * G) / ns;
-      auto pr = group_range(g);
+    std::vector<std::pair<int64_t, int64_t>> picked;
+    for (int64_t t = 0; t < ns && tot < (int64_t(1) << 24); ++t) {
+      auto pr = group_range((t * G) / ns);
       if (pr.second == pr.first) continue;
-      std::vector<int32_t> r((size_t)(pr.second - pr.first));
-      SK_CUDA(cudaMemcpyAsync(r.data(), p->rowidx + pr.first, r.size() * 4, cudaMemcpyDeviceToHost, stream));
-      SK_CUDA(cudaStreamSynchronize(stream));
-      tot += (int64_t)r.size();
-      rows += distinct_rows(r);
+      picked.push_back(pr);
+      tot += pr.second - pr.first;
+    }
+    if (picked.empty()) return SK_OK;
+    const size_t words = (size_t)((p->m + 31) / 32);
+    if (p->m <= (int64_t(1) << 31)) {
+      uint32_t* bitmap = nullptr;
+      unsigned long long* cnt = nullptr;
+      std::vector<unsigned long long> h_cnt(picked.size(), 0);
+      SK_CUDA(cudaMallocAsync((void**)&bitmap, words * 4, stream));
+      cudaError_t e = cudaMallocAsync((void**)&cnt, picked.size() * 8, stream);
+      if (e == cudaSuccess) e = cudaMemsetAsync(cnt, 0, picked.size() * 8, stream);
+      for (size_t i = 0; i < picked.size() && e == cudaSuccess; ++i) {
+        e = cudaMemsetAsync(bitmap, 0, words * 4, stream);
+        if (e == cudaSuccess) e = sk::launch_distinct_rows(p->rowidx, picked[i].first, picked[i].second, bitmap, cnt + i, stream);
+      }
+      if (e == cudaSuccess) e = cudaMemcpyAsync(h_cnt.data(), cnt, picked.size() * 8, cudaMemcpyDeviceToHost, stream);
+      cudaFreeAsync(bitmap, stream);
+      if (cnt) cudaFreeAsync(cnt, stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+      if (e != cudaSuccess) return cuda_fail(e, "jki sample");
+      for (auto c : h_cnt) rows += (int64_t)c;
+    } else {
+      tot = 0;
+      for (auto& pr : picked) {
+        if (tot >= (int64_t(1) << 18)) break;
+        std::vector<int32_t> r((size_t)(pr.second - pr.first));
+        SK_CUDA(cudaMemcpyAsync(r.data(), p->rowidx + pr.first, r.size() * 4, cudaMemcpyDeviceToHost, stream));
+        SK_CUDA(cudaStreamSynchronize(stream));
+        tot += (int64_t)r.size();
+        rows += distinct_rows(r);
+      }
     }
     if (rows == 0 || (double)tot < 1.8 * (double)rows) return SK_OK;
   }
@@ -353,6 +382,13 @@ int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
   p->colptr = d_colptr; p->rowidx = rowidx;
   p->max_col = 0;
   for (int64_t k = 0; k < n; ++k) p->max_col = std::max(p->max_col, h_colptr[k + 1] - h_colptr[k]);
+  static const bool timing = getenv("SKETCH_TIMING") != nullptr;
+  const auto tm0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (timing)
+      fprintf(stderr, "  make_plan %s: %.3f ms\n", what,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tm0).count());
+  };
   Schedule rad = build_schedule(h_colptr, n, d, sk::kRowsPerWarpRad, sk::kRowsPerWarpRad / 128);
   Schedule pair = build_schedule(h_colptr, n, d, sk::kRowsPerWarpPair, sk::kRowsPerWarpPair / 2);
   Schedule gauss = build_schedule(h_colptr, n, d, sk::kRowsPerWarpGauss, sk::kRowsPerWarpGauss / 2);
@@ -375,6 +411,7 @@ int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
     f4t = build_tc_schedule(h_colptr, n, (d + 3) / 4, 1);   // 512-row blocks
     p->n_f4t = (int64_t)f4t.size();
   }
+  lap("rad/pair/gauss/tc schedules");
   p->nnz_end = h_colptr[n];
   // S-as-N fp4 path: TMA streams rowidx / values (16-byte aligned arrays, int32 coordinates)
   if (dtype == SK_F64 && p->max_col <= sk::kF4nMaxColumn && n > 0 && nnz >= 256 * n && sk::f4n_aligned(rowidx) &&
@@ -410,14 +447,17 @@ int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
     p->d_f4t = f4t.empty() ? nullptr : reinterpret_cast<sk::TcItem*>(dst + p->off_f4t);
     p->d_f4n = f4n.empty() ? nullptr : reinterpret_cast<sk::NItem*>(dst + p->off_f4n);
   }
+  lap("f4n schedule + image + malloc");
   if (jki >= 0) {
     const int rj = build_jki(p, h_colptr, jki > 0, stream);
     if (rj != SK_OK) { cudaFree(p->d_stage); delete p; return rj; }
   }
+  lap("jki");
   if (!defer_upload) {
     const int ru = upload_plan(p, stream, true);
     if (ru != SK_OK) { sketch_plan_destroy(p); return ru; }
   }
+  lap("upload");
   *out = p;
   return SK_OK;
 }
@@ -532,13 +572,25 @@ int sketch_plan(sk_plan_t* plan, sk_dtype_t dtype, int64_t d, int64_t m, int64_t
   if (nnz < 0 || !colptr || (nnz > 0 && !rowidx)) return SK_EINVAL;
   cudaStream_t stream = (cudaStream_t)stream_;
   std::vector<int64_t> h((size_t)n + 1);
+  static const bool timing = getenv("SKETCH_TIMING") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto ms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+    return std::chrono::duration<double, std::milli>(b - a).count();
+  };
+  const auto t0 = now();
   SK_CUDA(cudaMemcpyAsync(h.data(), colptr, (size_t)(n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
   SK_CUDA(cudaStreamSynchronize(stream));
+  const auto t1 = now();
   rc = validate_colptr(h.data(), n, nnz, true);
   if (rc) return rc;
   rc = validate_rows_sync(rowidx, nnz, m, stream);
   if (rc) return rc;
-  return make_plan(plan, dtype, d, m, n, row_offset, h.data(), colptr, rowidx, nnz, stream);
+  const auto t2 = now();
+  rc = make_plan(plan, dtype, d, m, n, row_offset, h.data(), colptr, rowidx, nnz, stream);
+  if (timing)
+    fprintf(stderr, "sketch_plan: colptr D2H %.3f ms, validation %.3f ms, make_plan %.3f ms\n", ms(t0, t1), ms(t1, t2),
+            ms(t2, now()));
+  return rc;
 }
 
 int sketch_plan_host(sk_plan_t* plan, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,

@@ -376,6 +376,29 @@ cudaError_t launch_fill_s(int dist, int dtype, uint64_t seed, int64_t i0, int64_
   return cudaGetLastError();
 }
 
+// Distinct rows of rowidx[p0, p1) (plan-time sampling for Algorithm 4): each entry sets its row's
+// bit in a zeroed bitmap; entries that find the bit clear are counted (warp-aggregated).
+__global__ void sk_distinct_rows_kernel(const int32_t* __restrict__ rowidx, int64_t p0, int64_t p1,
+                                        uint32_t* __restrict__ bitmap, unsigned long long* __restrict__ count) {
+  unsigned long long mine = 0;
+  for (int64_t p = p0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < p1; p += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t r = (uint32_t)__ldg(rowidx + p), bit = 1u << (r & 31);
+    mine += (atomicOr(bitmap + (r >> 5), bit) & bit) ? 0 : 1;
+  }
+  for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xFFFFFFFFu, mine, o);
+  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(count, mine);
+}
+
+cudaError_t launch_distinct_rows(const int32_t* rowidx, int64_t p0, int64_t p1, uint32_t* bitmap,
+                                 unsigned long long* count, cudaStream_t stream) {
+  if (p1 <= p0) return cudaSuccess;
+  const int threads = 256;
+  int64_t blocks = (p1 - p0 + threads - 1) / threads;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  sk_distinct_rows_kernel<<<(unsigned)blocks, threads, 0, stream>>>(rowidx, p0, p1, bitmap, count);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_validate_rows(const int32_t* rowidx, int64_t nnz, int64_t m, int* flag,
                                  cudaStream_t stream) {
   if (nnz == 0) return cudaSuccess;

@@ -46,7 +46,18 @@ constexpr int kF4Producers = kF4AWarps + kF4BWarps;
 constexpr int kF4LoaderWarp = kF4Producers;       // streams rowidx / vals into a smem ring
 constexpr int kF4MmaWarp = kF4Producers + 1;
 constexpr int kF4Threads = (kF4Producers + 2) * 32;
+#ifndef SK_F4_B4
+#define SK_F4_B4 0
+#endif
+#if SK_F4_B4
+// Base-4 signed digits {-3, -1, 1, 3} (e2m1 0xD / 0xA / 0x2 / 0x5): 32 digit rows + ones row +
+// 7 zero rows, so the digits operand is 1280 B per K-step instead of 2304.
+constexpr int kF4N = 40;
+constexpr int kF4Ones = 32;
+#else
 constexpr int kF4N = 72;                          // 64 digit rows + ones row + 7 zero rows
+constexpr int kF4Ones = 64;
+#endif
 #ifndef SK_F4_SUB
 #define SK_F4_SUB 4
 #define SK_F4_STAGES 2
@@ -55,7 +66,7 @@ constexpr int kF4Sub = SK_F4_SUB;                 // K-steps (64 nonzeros each) 
 constexpr int kF4Stages = SK_F4_STAGES;
 constexpr int kF4JSlots = 12 / kF4Sub;            // nonzero-stream ring: one slot = one smem stage (kF4Sub K-steps)
 constexpr int kF4ATile = 128 * 32;                // 128 rows x 64 fp4 = 4 KB
-constexpr int kF4BSub = 2560;                     // B tile slot per K-step: 9 row groups x 256 B, padded
+constexpr int kF4BSub = SK_F4_B4 ? 1280 : 2560;   // B tile slot per K-step: row groups x 256 B (padded)
 constexpr int kF4ATileS = kF4Sub * kF4ATile;      // one tile's A data per stage
 constexpr int kF4Stage = kF4Tiles * kF4ATileS + kF4Sub * kF4BSub;
 constexpr uint32_t kF4SfCol = 448;                // scale factors: TMEM columns [448, 512)
@@ -207,7 +218,8 @@ __device__ __forceinline__ uint32_t f4_off(int m, int h) {
 }
 
 // dbg (SKETCH_F4_DEBUG; tuning only, results invalid when nonzero), bit flags: 1 = no S stores,
-// 2 = no MMAs, 4 = no proxy fences, 8 = no digit stores, 16 = no column scan.
+// 2 = no MMAs, 4 = no proxy fences, 8 = no digit stores, 16 = no column scan, 32 = S warps skip
+// Philox and the transposes.
 // The debug switches exist only in builds with -DSK_F4_DEBUG=1 (the default build has none, so
 // they cannot perturb the schedule of the production kernel).
 #ifndef SK_F4_STAGGER_NS
@@ -243,10 +255,10 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
                  :: "r"(s_u32(&sh.tmem_base)), "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  // B rows 64..71 of every stage are constant: row 64 = +1.0 (0x2), rows 65..71 = 0
+  // B rows kF4Ones.. of every stage are constant: the ones row = +1.0 (0x2), the 7 rows after it 0
   for (int i = threadIdx.x; i < kF4Stages * kF4Sub * 8 * 2; i += blockDim.x) {
-    const int s = i / (16 * kF4Sub), sub = (i / 16) % kF4Sub, row = 64 + (i % 16) / 2, h = i & 1;
-    const uint32_t v = row == 64 ? 0x22222222u : 0u;
+    const int s = i / (16 * kF4Sub), sub = (i / 16) % kF4Sub, row = kF4Ones + (i % 16) / 2, h = i & 1;
+    const uint32_t v = row == kF4Ones ? 0x22222222u : 0u;
     const uint32_t a = s_u32(stages + s * kF4Stage + kF4Tiles * kF4ATileS + sub * kF4BSub) + f4_off(row, h);
     asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" :: "r"(a), "r"(v) : "memory");
   }
@@ -316,7 +328,8 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
 #pragma unroll
       for (int i = 0; i < kMine; ++i) {
         const uint32_t j = jv[i];
-        const uint4 xb = s_block(q, (uint64_t)P.row_offset + j, P.keys);   // padded nonzeros: B = 0
+        const uint4 xb = (dbg & 32) ? make_uint4(j, j ^ 1u, j ^ 2u, j ^ 3u)
+                                    : s_block(q, (uint64_t)P.row_offset + j, P.keys);   // padded nonzeros: B = 0
         x[4 * i + 0] = xb.x; x[4 * i + 1] = xb.y; x[4 * i + 2] = xb.z; x[4 * i + 3] = xb.w;
       }
 #if SK_F4_PART
@@ -342,7 +355,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
           }
       }
 #else
-      f4_transpose<4 * kMine>(x, lane);           // lane r: row 32qq + r over 32 nonzeros
+      if (!(dbg & 32)) f4_transpose<4 * kMine>(x, lane);   // lane r: row 32qq + r over 32 nonzeros
       if (use > 0) f4_wait(&sh.empty[stage], (use - 1) & 1);
       if (!(dbg & 1)) {
         const uint32_t tile = s_u32(stages + stage * kF4Stage) + (uint32_t)(t * kF4ATileS) + f4_off(lane, h);
@@ -387,20 +400,55 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
           const long long A = __double2ll_rn((v0 * sc1) * sc2);
           U = (unsigned long long)A ^ 0x8000000000000000ull;
         }
+#if SK_F4_B4
+        x[2 * sub] = (uint32_t)U;                  // bits of U (digit s uses bits 2s, 2s+1)
+        x[2 * sub + 1] = (uint32_t)(U >> 32);
+#else
         x[2 * sub] = ~(uint32_t)U;                 // sign bits of the digit nibbles
         x[2 * sub + 1] = ~(uint32_t)(U >> 32);
+#endif
       }
-      f4_transpose<2 * kF4Sub>(x, lane);           // lane s: digit s (and 32 + s) per K-step
+      f4_transpose<2 * kF4Sub>(x, lane);           // lane r: bit r (and 32 + r) of U per K-step
+#if SK_F4_B4
+      // digit s = 4 b_{2s+1} + 2 b_{2s} - 3: even lane r pairs its bit r of the low word with lane
+      // r+1's (digit r/2), odd lane r pairs lane r-1's bit of the high word with its own (digit
+      // 16 + r/2).  One SHFL per K-step brings the pairs together.
+      const bool odd = lane & 1;
+      const int brow = odd ? 16 + (lane >> 1) : (lane >> 1);
+      uint32_t b0w[kF4Sub], b1w[kF4Sub];
+#pragma unroll
+      for (int sub = 0; sub < kF4Sub; ++sub) {
+        const uint32_t lo = x[2 * sub], hi = x[2 * sub + 1];
+        const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, odd ? lo : hi, 1);
+        b0w[sub] = odd ? y : lo;
+        b1w[sub] = odd ? hi : y;
+      }
+#endif
       if (use > 0) f4_wait(&sh.empty[stage], (use - 1) & 1);
       if (!(dbg & 8)) {
 #pragma unroll
         for (int sub = 0; sub < kF4Sub; ++sub) {
           const uint32_t bt = s_u32(stages + stage * kF4Stage + kF4Tiles * kF4ATileS + sub * kF4BSub);
+#if SK_F4_B4
+          // nibble n of word c = nonzero 4n + c: sign = !b1, magnitude 3 (0b101) iff b1 == b0, else 1 (0b010)
+          const uint32_t sg = ~b1w[sub], eq = ~(b1w[sub] ^ b0w[sub]);
+          uint32_t wv[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const uint32_t a = sg << (3 - c);
+            const uint32_t t = c <= 2 ? eq << (2 - c) : eq >> 1;   // bit 4n + c -> 4n + 2
+            wv[c] = (a & 0x88888888u) | (t & 0x44444444u) | (~(t >> 1) & 0x22222222u) | ((t >> 2) & 0x11111111u);
+            if (nval[sub] < 32) wv[c] &= f4_valid_mask(c, nval[sub]);
+          }
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};"
+                       :: "r"(bt + f4_off(brow, h)), "r"(wv[0]), "r"(wv[1]), "r"(wv[2]), "r"(wv[3]) : "memory");
+#else
           f4_store_row_masked(bt + f4_off(lane, h), x[2 * sub], nval[sub]);
           f4_store_row_masked(bt + f4_off(32 + lane, h), x[2 * sub + 1], nval[sub]);
+#endif
           if (nval[sub] < 32 && lane == 0) {   // partial (last) K chunk: the ones row too
             const uint32_t z = 0u;              // (y = 0 -> nibbles 0x2 = +1.0)
-            f4_store_row_masked(bt + f4_off(64, h), z, nval[sub]);
+            f4_store_row_masked(bt + f4_off(kF4Ones, h), z, nval[sub]);
           }
         }
       }
@@ -475,7 +523,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
       if (nsteps > 0) {
         const uint32_t base = tmem + ((uint32_t)(32 * qw) << 16) + (uint32_t)(tt * kF4N);
 #pragma unroll
-        for (int c = 0; c < 72; c += 8) {
+        for (int c = 0; c < kF4N; c += 8) {
           uint32_t D[8];
           asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
                        : "=r"(D[0]), "=r"(D[1]), "=r"(D[2]), "=r"(D[3]), "=r"(D[4]), "=r"(D[5]), "=r"(D[6]), "=r"(D[7])
@@ -485,9 +533,16 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
           for (int u = 0; u < 8; ++u) {
             const long long dv = (long long)__float2ll_rn(__uint_as_float(D[u]));
             const int s = c + u;
+#if SK_F4_B4
+            // Σ_s 4^s D_s - D_32: low 16 digits into lo, high 16 into hi (weights 4^(s-16))
+            if (s < 16) lo += dv << (2 * s);
+            else if (s < 32) hi += dv << (2 * (s - 16));
+            else if (s == 32) ones = dv;
+#else
             if (s < 32) lo += dv << s;
             else if (s < 64) hi += dv << (s - 32);
             else if (s == 64) ones = dv;
+#endif
           }
         }
       }

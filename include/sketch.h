@@ -186,6 +186,17 @@ typedef enum {
 int sketch_set_rad_f64_path(int path);
 
 /*
+ * Kernel selection for SK_RADEMACHER with SK_F32 values (process-wide; both compute Â in fp32
+ * within the parity bound 2e-5 |S||A|).  SK_PATH32_SIMT (default): one predicated add per
+ * (row, nonzero).  SK_PATH32_TABLE: per 4 nonzeros the CTA tabulates the 16 signed sums
+ * ±a_1 ±a_2 ±a_3 ±a_4 and each row adds the one its 4 sign bits select (one table load + one add
+ * per 4 entries; sums formed in nonzero order).  Initialised from SKETCH_RAD_F32_PATH = simt | tab.
+ * Errors: SK_EINVAL for an unknown path.
+ */
+typedef enum { SK_PATH32_SIMT = 1, SK_PATH32_TABLE = 0 } sk_rad_f32_path_t;
+int sketch_set_rad_f32_path(int path);
+
+/*
  * Kernel selection for SK_UNIFORM / SK_GAUSSIAN (process-wide): Algorithm 3 (kji: S[:, j] regenerated
  * per stored nonzero) or Algorithm 4 (jki: S[:, j] regenerated once per nonzero
  * row of each 16-column group and reused across the row).  The plan builds the

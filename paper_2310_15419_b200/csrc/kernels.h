@@ -62,6 +62,10 @@ cudaError_t launch_apply_rad_tc(const ApplyArgs& a, const TcItem* items, int64_t
                                 cudaStream_t stream);
 int tc_tiles_per_cta();
 cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const TcItem* items, int64_t n_items, cudaStream_t stream);
+
+// ±1 x fp32 values through 4-nonzero subset-sum tables (sketch_tab.cu); items of <= 16 row tiles.
+int tab_tiles_per_cta();
+cudaError_t launch_apply_rad_tab(const ApplyArgs& a, const TcItem* items, int64_t n_items, cudaStream_t stream);
 int f4_tiles_per_cta();
 // Algorithm 4 (jki) path for uniform / Gaussian (sketch_jki.cu): column groups of kJCols columns,
 // each stored row by row (CSR of the group); items = (group, tile of jki_rows_per_item() rows).

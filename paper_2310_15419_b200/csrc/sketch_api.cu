@@ -151,6 +151,19 @@ std::vector<sk::NItem> build_f4n_schedule(const int64_t* colptr, int64_t n, int6
 // SK_PATH_SIMT, SK_PATH_HYBRID.  Initialised from SKETCH_RAD_F64_PATH = fp4 | fp4n | int8smem |
 // int8tmem | simt | hybrid, else fp4.
 std::atomic<int> g_rad_f64_path{-1};
+// ±1 with fp32 values: SK_PATH32_SIMT (default; c4 1.49 ms) or SK_PATH32_TABLE (2.09 ms: more
+// instructions per entry than the predicated adds); SKETCH_RAD_F32_PATH = simt | tab.
+std::atomic<int> g_rad_f32_path{-1};
+
+int rad_f32_path() {
+  int v = g_rad_f32_path.load(std::memory_order_relaxed);
+  if (v >= 0) return v;
+  v = SK_PATH32_SIMT;
+  if (const char* e = getenv("SKETCH_RAD_F32_PATH"))
+    if (!strcmp(e, "tab")) v = SK_PATH32_TABLE;
+  g_rad_f32_path.store(v, std::memory_order_relaxed);
+  return v;
+}
 
 int rad_f64_path() {
   int v = g_rad_f64_path.load(std::memory_order_relaxed);
@@ -200,6 +213,8 @@ struct sk_plan_s {
   sk::TcItem* d_f4t = nullptr;      // S-in-TMEM fp4 schedule: (column, 512-row block), longest first
   int64_t n_f4t = 0;
   sk::NItem* d_f4n = nullptr;       // S-as-N fp4 schedule: (column, 256-row tile), longest first
+  sk::TcItem* d_tab = nullptr;      // ±1 fp32 subset-sum-table schedule: (column, <= 16 row tiles)
+  int64_t n_tab = 0;
   int64_t n_f4n = 0;
   int64_t nnz_end = 0;              // colptr[n] (absolute end of the nonzero stream)
   // Algorithm 4 (jki) structure: one device block holding items, grp_rows, row_j, row_ent, ent, ent_base
@@ -210,7 +225,7 @@ struct sk_plan_s {
   // All schedules (items, tc / f4, f4t, f4n) live in ONE device block uploaded by one copy.
   void* d_stage = nullptr;
   std::vector<unsigned char> h_stage;   // host image of d_stage (kept until uploaded)
-  size_t off_items = 0, off_tc = 0, off_f4t = 0, off_f4n = 0;
+  size_t off_items = 0, off_tc = 0, off_f4t = 0, off_f4n = 0, off_tab = 0;
   int64_t n_rad = 0, n_pair = 0, n_gauss = 0;
   int64_t philox_rad = 0, philox_pair = 0;
 };
@@ -400,7 +415,11 @@ int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
   // Tensor-core ±1 paths: every column within the exact-accumulation bound, and columns long
   // enough on average (>= 256 nonzeros) to amortise a CTA's TMEM / barrier / scale prologue.
   const bool tc_ok = dtype == SK_F64 && p->max_col <= sk::kTcMaxColumn && n > 0 && nnz >= 256 * n;
-  std::vector<sk::TcItem> tc, f4t;
+  std::vector<sk::TcItem> tc, f4t, tab;
+  if (dtype == SK_F32 && n > 0) {
+    tab = build_tc_schedule(h_colptr, n, d, sk::tab_tiles_per_cta());
+    p->n_tab = (int64_t)tab.size();
+  }
   std::vector<sk::NItem> f4n;
   if (tc_ok) {
     tc = build_tc_schedule(h_colptr, n, d, sk::tc_tiles_per_cta());
@@ -427,7 +446,8 @@ int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
     p->off_tc = up(p->off_items + (size_t)total * sizeof(Item));
     p->off_f4t = up(p->off_tc + tc.size() * sizeof(sk::TcItem));
     p->off_f4n = up(p->off_f4t + f4t.size() * sizeof(sk::TcItem));
-    const size_t bytes = up(p->off_f4n + f4n.size() * sizeof(sk::NItem));
+    p->off_tab = up(p->off_f4n + f4n.size() * sizeof(sk::NItem));
+    const size_t bytes = up(p->off_tab + tab.size() * sizeof(sk::TcItem));
     p->h_stage.assign(bytes, 0);
     unsigned char* h = p->h_stage.data();
     size_t o = p->off_items;
@@ -438,6 +458,7 @@ int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
     if (!tc.empty()) std::memcpy(h + p->off_tc, tc.data(), tc.size() * sizeof(sk::TcItem));
     if (!f4t.empty()) std::memcpy(h + p->off_f4t, f4t.data(), f4t.size() * sizeof(sk::TcItem));
     if (!f4n.empty()) std::memcpy(h + p->off_f4n, f4n.data(), f4n.size() * sizeof(sk::NItem));
+    if (!tab.empty()) std::memcpy(h + p->off_tab, tab.data(), tab.size() * sizeof(sk::TcItem));
     cudaError_t e = defer_upload ? cudaMallocAsync(&p->d_stage, bytes > 0 ? bytes : 256, stream)
                                  : cudaMalloc(&p->d_stage, bytes > 0 ? bytes : 256);
     if (e != cudaSuccess) { delete p; return e == cudaErrorMemoryAllocation ? SK_ENOMEM : cuda_fail(e, "cudaMalloc(plan)"); }
@@ -446,6 +467,7 @@ int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
     p->d_tc = tc.empty() ? nullptr : reinterpret_cast<sk::TcItem*>(dst + p->off_tc);
     p->d_f4t = f4t.empty() ? nullptr : reinterpret_cast<sk::TcItem*>(dst + p->off_f4t);
     p->d_f4n = f4n.empty() ? nullptr : reinterpret_cast<sk::NItem*>(dst + p->off_f4n);
+    p->d_tab = tab.empty() ? nullptr : reinterpret_cast<sk::TcItem*>(dst + p->off_tab);
   }
   lap("f4n schedule + image + malloc");
   if (jki >= 0) {
@@ -492,7 +514,9 @@ int apply_items(const sk_plan_s* p, uint64_t seed, sk_dist_t dist, const void* v
   a.keys = sk::make_keys(seed);
   cudaError_t e;
   const int path = rad_f64_path();
-  if (dist == SK_RADEMACHER && path == SK_PATH_TC_FP4T && p->n_f4t > 0) {
+  if (dist == SK_RADEMACHER && p->dtype == SK_F32 && p->n_tab > 0 && rad_f32_path() == SK_PATH32_TABLE) {
+    e = sk::launch_apply_rad_tab(a, p->d_tab, p->n_tab, stream);
+  } else if (dist == SK_RADEMACHER && path == SK_PATH_TC_FP4T && p->n_f4t > 0) {
     e = sk::launch_apply_rad_f4t(a, p->d_f4t, p->n_f4t, stream);
   } else if (dist == SK_RADEMACHER && path == SK_PATH_TC_FP4N && p->n_f4n > 0 && sk::f4n_aligned(vals)) {
     e = sk::launch_apply_rad_f4n(a, (int)p->dtype, p->d_f4n, p->n_f4n, p->n, p->nnz_end, stream);
@@ -536,7 +560,9 @@ const char* kernel_name(const sk_plan_s* p, int dist) {
     if (p->n_f4n > 0 && rad_f64_path() == SK_PATH_TC_FP4N)
       return p->dtype == SK_F32 ? "sk_rad_f4n_kernel<float> (tcgen05 kind::mxf4, N=256)"
                                 : "sk_rad_f4n_kernel<double> (tcgen05 kind::mxf4, N=256)";
-    if (p->dtype == SK_F32) return "sk_rad_kernel<float>";
+    if (p->dtype == SK_F32)
+      return p->n_tab > 0 && rad_f32_path() == SK_PATH32_TABLE ? "sk_rad_tab_kernel (fp32, 4-nonzero subset-sum tables)"
+                                                                : "sk_rad_kernel<float>";
     if (p->n_tc > 0 && rad_f64_path() != SK_PATH_TC_FP4N && rad_f64_path() != SK_PATH_TC_FP4T) {
       switch (rad_f64_path()) {
         case SK_PATH_TC_FP4: return "sk_rad_f4_kernel (tcgen05 kind::mxf4)";
@@ -862,6 +888,12 @@ const char* sketch_version(void) { return "libsketch 0.2.0 sm_100a"; }
 int sketch_set_rad_f64_path(int path) {
   if (path < SK_PATH_TC_FP4 || path > SK_PATH_TC_FP4T) return SK_EINVAL;
   g_rad_f64_path.store(path, std::memory_order_relaxed);
+  return SK_OK;
+}
+
+int sketch_set_rad_f32_path(int path) {
+  if (path != SK_PATH32_TABLE && path != SK_PATH32_SIMT) return SK_EINVAL;
+  g_rad_f32_path.store(path, std::memory_order_relaxed);
   return SK_OK;
 }
 

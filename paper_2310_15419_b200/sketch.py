@@ -29,8 +29,9 @@ EXPORTS = ["sketch_plan", "sketch_plan_host", "sketch_apply", "sketch_apply_csc"
            "sketch_apply_host", "sketch_fill_s", "sketch_plan_stats", "sketch_plan_destroy",
            "sketch_error_string", "sketch_last_error_detail", "sketch_version",
            "sketch_set_rad_f64_path", "sketch_apply_kernel_name", "sketch_set_pair_path",
-           "sketch_plan_host_jki"]
+           "sketch_plan_host_jki", "sketch_set_rad_f32_path"]
 RAD_F64_PATHS = {"fp4": 0, "int8smem": 1, "int8tmem": 2, "simt": 3, "hybrid": 4, "fp4n": 5, "fp4t": 6}
+RAD_F32_PATHS = {"tab": 0, "simt": 1}
 PAIR_PATHS = {"auto": 0, "kji": 1, "jki": 2}
 _STRING_RESULTS = ("sketch_error_string", "sketch_last_error_detail", "sketch_version",
                    "sketch_apply_kernel_name")
@@ -83,6 +84,7 @@ def load_library(path: str = LIB_PATH):
         lib.sketch_version.argtypes = []
         lib.sketch_version.restype = ctypes.c_char_p
         lib.sketch_set_rad_f64_path.argtypes = [i32]
+        lib.sketch_set_rad_f32_path.argtypes = [i32]
         lib.sketch_set_pair_path.argtypes = [i32]
         lib.sketch_plan_host_jki.argtypes = [ctypes.POINTER(vp), i32, i64, i64, i64, i64, vp, vp, i64, i32, vp]
         lib.sketch_apply_kernel_name.argtypes = [vp, i32]
@@ -264,6 +266,13 @@ def set_rad_f64_path(path) -> None:
     "int8smem", "int8tmem" or "simt" (process-wide)."""
     p = RAD_F64_PATHS[path] if isinstance(path, str) else int(path)
     _check(load_library().sketch_set_rad_f64_path(p), "sketch_set_rad_f64_path")
+
+
+def set_rad_f32_path(path) -> None:
+    """Select the kernel for ±1 sketches of fp32 values: "simt" (predicated adds, default) or
+    "tab" (subset-sum tables) (process-wide)."""
+    p = RAD_F32_PATHS[path] if isinstance(path, str) else int(path)
+    _check(load_library().sketch_set_rad_f32_path(p), "sketch_set_rad_f32_path")
 
 
 def set_pair_path(path) -> None:

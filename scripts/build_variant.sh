@@ -3,7 +3,7 @@ set -e
 OUT="$1"; shift
 D=paper_2310_15419_b200/csrc
 T=$(mktemp -d)
-for s in sketch_kernels sketch_tc sketch_f4 sketch_f4t sketch_f4n sketch_hybrid sketch_jki sketch_api; do
+for s in sketch_kernels sketch_tc sketch_f4 sketch_f4t sketch_f4n sketch_hybrid sketch_jki sketch_tab sketch_api; do
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
     --expt-relaxed-constexpr "$@" -I include -c $D/$s.cu -o $T/$s.o &
 done

@@ -206,6 +206,27 @@ def test_nan_poisons_only_its_column(sk, path):
         sk.set_rad_f64_path("fp4")
 
 
+@pytest.mark.parametrize("path", ["tab", "simt"])
+def test_rad_f32_kernel_paths(sk, path):
+    # both ±1 fp32 kernels (subset-sum tables, predicated adds) on the edge cases: ragged d and
+    # item tails (d not a multiple of 128 or 2048), empty / single / long columns, chunk tails
+    # (lengths not multiples of 32 or 4), unsorted rows with duplicates, d = 1
+    try:
+        sk.set_rad_f32_path(path)
+        f32 = np.float32
+        cases = [(workloads.random_csc(50000, 40, 300, seed=2, dtype=f32), 1000),
+                 (workloads.random_csc(30000, 12, [0, 500, 0, 0, 641, 1, 0, 3303, 0, 2, 0, 99], seed=5, dtype=f32), 2100),
+                 (workloads.random_csc(5000, 10, 37, seed=7, sorted_rows=False, duplicates=True, dtype=f32), 129),
+                 (workloads.random_csc(4000, 7, 45, seed=9, dtype=f32), 1),
+                 (workloads.random_csc(200000, 3, [20000, 3, 7], seed=6, dtype=f32), 4097)]
+        for A, d in cases:
+            got = _gpu_sketch(sk, A, d, "rademacher", 13)
+            ref, B = oracle.sketch(13, "rademacher", d, A.m, A.n, A.colptr, A.rowidx, A.vals, threads=8)
+            _check(got, ref, B, TOL["f32"])
+    finally:
+        sk.set_rad_f32_path("simt")
+
+
 def test_kernel_names_report_the_path(sk):
     A = workloads.random_csc(10000, 4, 300, seed=1)
     plan = sk.Plan(_dev(A.colptr), _dev(A.rowidx), 300, A.m, "f64")
@@ -215,8 +236,15 @@ def test_kernel_names_report_the_path(sk):
             sk.set_rad_f64_path(path)
             assert tag in plan.kernel_name("rademacher")
         assert "uniform" in plan.kernel_name("uniform") and "gaussian" in plan.kernel_name("gaussian")
+        A32 = workloads.random_csc(10000, 4, 300, seed=1, dtype=np.float32)
+        plan32 = sk.Plan(_dev(A32.colptr), _dev(A32.rowidx), 300, A32.m, "f32")
+        for path, tag in (("tab", "sk_rad_tab_kernel"), ("simt", "sk_rad_kernel<float>")):
+            sk.set_rad_f32_path(path)
+            assert tag in plan32.kernel_name("rademacher")
+        plan32.close()
     finally:
         sk.set_rad_f64_path("fp4")
+        sk.set_rad_f32_path("simt")
         plan.close()
 
 

@@ -186,7 +186,7 @@ def run_reference(args):
     print(json.dumps({
         "impl": "reference", "metric": "sketch GFLOP/s (2·d·nnz(A)/s)", "value": v,
         "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": cfg.dtype, "data": "synthetic",
         "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "d": cfg.d, "dist": cfg.dist,
                    "seed": cfg.seed, "sample_nnz": nnz_s},

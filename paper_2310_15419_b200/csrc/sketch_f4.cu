@@ -219,7 +219,7 @@ __device__ __forceinline__ uint32_t f4_off(int m, int h) {
 
 // dbg (SKETCH_F4_DEBUG; tuning only, results invalid when nonzero), bit flags: 1 = no S stores,
 // 2 = no MMAs, 4 = no proxy fences, 8 = no digit stores, 16 = no column scan, 32 = S warps skip
-// Philox and the transposes.
+// Philox and the transposes, 64 = MMAs with N = 8.
 // The debug switches exist only in builds with -DSK_F4_DEBUG=1 (the default build has none, so
 // they cannot perturb the schedule of the production kernel).
 #ifndef SK_F4_STAGGER_NS
@@ -480,7 +480,8 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
     // ===================== MMA issuer =====================
     if (lane == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t idesc = f4_idesc();
+      // (debug flag 64: N = 8, i.e. the MMAs read 256 B of the digits operand instead of 2304)
+      const uint32_t idesc = (dbg & 64) ? ((f4_idesc() & ~(0x3Fu << 17)) | (1u << 17)) : f4_idesc();
       for (int ss = 0; ss < nsup; ++ss) {
         const int stage = ss % kF4Stages;
         f4_wait(&sh.full[stage], (ss / kF4Stages) & 1);

@@ -489,6 +489,11 @@ def test_jki_auto_selection(sk):
     try:
         assert pa.stats()["n_items_jki"] > 0 and pb.stats()["n_items_jki"] == 0
         assert pa.stats()["jki_nonzero_rows"] * 10 <= A.nnz
+        # the plan's Algorithm 4 structure holds exactly the distinct rows of every 16-column
+        # block (the rows whose S column Algorithm 4 generates)
+        exact = sum(len(np.unique(A.rowidx[A.colptr[c0]:A.colptr[min(A.n, c0 + 16)]]))
+                    for c0 in range(0, A.n, 16))
+        assert pa.stats()["jki_nonzero_rows"] == exact
         sk.set_pair_path("kji")
         assert "Algorithm 4" not in pa.kernel_name("uniform")
     finally:

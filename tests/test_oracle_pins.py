@@ -319,3 +319,20 @@ def test_paper_gflops_metric_golden():
         g = gflops(int(r["d"]), int(r["nnz"]), t)
         tol = g * (0.005 / t) + 0.006            # time printed to 0.01 s, GFlops to 0.01
         assert abs(g - float(r["gflops"])) <= tol, r
+
+
+def test_expected_nonzero_rows_formula():
+    # PAPER.md:361-365 (cost model): with entries nonzero independently with probability rho,
+    # the number Y of rows of an m1 x n1 block holding a nonzero has E[Y] = m1 (1 - (1-rho)^n1).
+    # Pinned by simulation (not by retyping the formula): mean of Y over many Bernoulli blocks,
+    # within 5 standard errors, for several (m1, n1, rho); and the limits rho = 0, rho = 1, n1 = 1.
+    from paper_2310_15419_b200.metrics import expected_nonzero_rows
+    rng = np.random.default_rng(365)
+    for m1, n1, rho in ((1000, 16, 0.01), (500, 4, 0.2), (2000, 64, 0.002)):
+        trials = 400
+        ys = np.array([(rng.random((m1, n1)) < rho).any(axis=1).sum() for _ in range(trials)], dtype=float)
+        se = ys.std(ddof=1) / np.sqrt(trials)
+        assert abs(ys.mean() - expected_nonzero_rows(m1, n1, rho)) <= 5 * se + 1e-9, (m1, n1, rho)
+    assert expected_nonzero_rows(100, 8, 0.0) == 0.0
+    assert expected_nonzero_rows(100, 8, 1.0) == 100.0
+    assert abs(expected_nonzero_rows(100, 1, 0.3) - 30.0) < 1e-12

@@ -144,9 +144,32 @@ __device__ __forceinline__ double bm_log(double u, const double* __restrict__ ta
   return shi + (r + fma(r2, p, slo));
 }
 
-// sin and cos of th in [0, 2 pi): Cody-Waite reduction by pi/2 in four parts (exact products for
-// k <= 4), fdlibm kernels on |r| <= pi/4, quadrant by k mod 4 (signs applied as bit flips).
+// sin and cos of th in [0, 2 pi) by table: j = rint(64 th / pi), r = th - j pi/64 (pi/64 in three
+// parts, the first two products exact), |r| <= pi/128, Taylor sin r / cos r to degree 7 / 6, and
+// sin th = S_j cos r + C_j sin r, cos th = C_j cos r - S_j sin r with the correctly rounded
+// S_j, C_j of kBmSinCosTab (exact zeros at multiples of pi/2: no cancellation where sin or cos
+// vanishes).  17 FP64 operations + one 16-byte load (L1-resident 2 KB table) instead of ~25
+// for the quadrant form below; <= 2.5e-16 relative (scripts/gen_bm_tables.py --check).
 __device__ __forceinline__ void bm_sincos(double th, double& s, double& c) {
+  const double kr = fma(th, kBm[k64OverPi], kBm[kRound]);    // 1.5 2^52 + rint(64 th / pi)
+  const double kd = kr - kBm[kRound];
+  double r = fma(-kd, kBm[kPi64_0], th);
+  r = fma(-kd, kBm[kPi64_1], r);
+  r = fma(-kd, kBm[kPi64_2], r);
+  const int j = __double2loint(kr) & 0xFF;                   // 0..128
+  const double2 t = __ldg(reinterpret_cast<const double2*>(&kBmSinCosTab[j][0]));
+  const double z = r * r;
+  const double ps = fma(z, fma(z, kBm[kT7], kBm[kT5]), kBm[kT3]);
+  const double sr = fma(z * r, ps, r);
+  const double cr = fma(z, fma(z, fma(z, kBm[kU6], kBm[kU4]), kBm[kU2]), 1.0);
+  s = fma(t.x, cr, t.y * sr);
+  c = fma(t.y, cr, -(t.x * sr));
+}
+
+// The quadrant form (previous version, kept for reference): Cody-Waite reduction by pi/2 in four
+// parts (exact products for k <= 4), fdlibm kernels on |r| <= pi/4, quadrant by k mod 4 (signs
+// applied as bit flips).
+__device__ __forceinline__ void bm_sincos_quadrant(double th, double& s, double& c) {
   const double kr = fma(th, kBm[kTwoOverPi], kBm[kRound]);   // 1.5 2^52 + rint(th 2/pi)
   const double kd = kr - kBm[kRound];
   double r = fma(-kd, kBm[kPio2_0], th);

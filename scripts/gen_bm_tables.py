@@ -13,6 +13,12 @@ log(u), u in (0, 1]:  u = 2^e m, m in [1, 2); idx = round(128 (m - 1)) in [0, 12
   and P the Taylor polynomial of (log1p(r) - r) / r^2 to degree 5.
 sin / cos on |r| <= pi/4 after the Cody-Waite reduction r = theta - k pi/2 (pi/2 in four parts):
   the minimax kernels of fdlibm (Sun Microsystems, 1993; public domain), error < 1 ulp.
+sin / cos by table (bm_sincos, the one in use): j = rint(64 theta / pi) in [0, 128],
+  r = theta - j pi/64 (pi/64 in three parts, j pi/64 exact for the first two), |r| <= pi/128;
+  sin r = r + r^3 (-1/6 + r^2 (1/120 - r^2/5040)), cos r = 1 + r^2 (-1/2 + r^2 (1/24 - r^2/720))
+  (Taylor; the next terms are below 2^-60 relative); sin theta = S_j cos r + C_j sin r,
+  cos theta = C_j cos r - S_j sin r with S_j, C_j = sin, cos (j pi/64) correctly rounded (exact
+  zeros at multiples of pi/2, so no cancellation near the zeros of sin and cos).
 """
 import argparse
 import os
@@ -50,6 +56,33 @@ def round_grid(x, g):
 LN2 = mp.log(2)
 LN2_HI = round_grid(LN2, 42)
 LN2_LO = float(LN2 - LN2_HI)
+PI64 = mp.pi / 64
+PI64_0 = round_bits(PI64, 44)                  # j * PI64_0 exact for j <= 128 (8 + 44 bits)
+PI64_1 = round_bits(PI64 - PI64_0, 44)
+PI64_2 = float(PI64 - PI64_0 - PI64_1)
+SC_TAB = [(float(mp.sin(j * PI64)), float(mp.cos(j * PI64))) for j in range(129)]
+for j in (0, 32, 64, 96, 128):                 # exact zeros / ones at multiples of pi/2
+    SC_TAB[j] = (float(mp.nint(mp.sin(j * PI64))), float(mp.nint(mp.cos(j * PI64))))
+
+
+def fma(a, b, c):
+    return float(mp.mpf(a) * mp.mpf(b) + mp.mpf(c))
+
+
+def bm_sincos_tab(th: float):
+    """float64 emulation (with fma) of philox.cuh bm_sincos."""
+    kr = fma(th, float(64 / mp.pi), 6755399441055744.0)
+    kd = kr - 6755399441055744.0
+    j = int(kd)
+    r = fma(-kd, PI64_0, th)
+    r = fma(-kd, PI64_1, r)
+    r = fma(-kd, PI64_2, r)
+    S, C = SC_TAB[j]
+    z = r * r
+    ps = fma(z, fma(z, -1.0 / 5040.0, 1.0 / 120.0), -1.0 / 6.0)
+    sr = fma(z * r, ps, r)
+    cr = fma(z, fma(z, fma(z, -1.0 / 720.0, 1.0 / 24.0), -0.5), 1.0)
+    return fma(S, cr, C * sr), fma(C, cr, -(S * sr))
 
 
 def table():
@@ -112,6 +145,23 @@ def check(n: int, rows) -> None:
     print(f"max rel error: log {worst_log:.3g}, sin kernel {worst_s:.3g}, cos kernel {worst_c:.3g} "
           f"(2^-52 = {2.0 ** -52:.3g})")
     assert worst_log < 8 * 2.0 ** -53 and worst_s < 4 * 2.0 ** -53 and worst_c < 4 * 2.0 ** -53
+    # table sincos over theta = u2 fl(2 pi), u2 = k 2^-53 (random k, and k near the multiples of
+    # 2^51 = the quadrant boundaries where sin or cos vanishes)
+    two_pi = 6.283185307179586
+    ks = [rng.randrange(0, 2 ** 53) for _ in range(n)]
+    ks += [q * 2 ** 51 + dk for q in range(4) for dk in range(-40, 41) if 0 <= q * 2 ** 51 + dk < 2 ** 53]
+    ks += [2 ** 53 - 1, 1, 2, 3]
+    worst_ts = worst_tc = 0.0
+    for k in ks:
+        th = (k * 2.0 ** -53) * two_pi                              # u2 fl(2 pi), one IEEE multiply
+        s, c = bm_sincos_tab(th)
+        rs, rc = mp.sin(mp.mpf(th)), mp.cos(mp.mpf(th))
+        if rs != 0:
+            worst_ts = max(worst_ts, float(abs((s - rs) / rs)))
+        if rc != 0:
+            worst_tc = max(worst_tc, float(abs((c - rc) / rc)))
+    print(f"table sincos max rel error: sin {worst_ts:.3g}, cos {worst_tc:.3g}")
+    assert worst_ts < 16 * 2.0 ** -53 and worst_tc < 16 * 2.0 ** -53
 
 
 def write(rows) -> None:
@@ -123,7 +173,8 @@ def write(rows) -> None:
              "// Scalar constants live in the constant bank so DFMA / DMUL read them as c[][] operands",
              "// (fp64 immediates would be rebuilt with UMOV pairs at every use).",
              "enum BmK { kLn2Hi, kLn2Lo, kPio2_0, kPio2_1, kPio2_2, kPio2_3, kS1, kS2, kS3, kS4, kS5, kS6,",
-             "           kC1, kC2, kC3, kC4, kC5, kC6, kL7, kL6, kL5, kL4, kL3, kL2, kTwoOverPi, kRound, kTwoPi, kBmKCount };",
+             "           kC1, kC2, kC3, kC4, kC5, kC6, kL7, kL6, kL5, kL4, kL3, kL2, kTwoOverPi, kRound, kTwoPi,",
+             "           k64OverPi, kPi64_0, kPi64_1, kPi64_2, kT3, kT5, kT7, kU2, kU4, kU6, kBmKCount };",
              "__device__ __constant__ double kBm[kBmKCount] = {",
              f"    {LN2_HI!r}, {LN2_LO!r},",
              "    1.57079632673412561417e+00, 6.07710050630396597660e-11, 2.02226624871116645580e-21,",
@@ -131,11 +182,17 @@ def write(rows) -> None:
              "    " + ", ".join(repr(x) for x in S) + ",",
              "    " + ", ".join(repr(x) for x in C) + ",",
              "    1.0 / 7.0, -1.0 / 6.0, 1.0 / 5.0, -1.0 / 4.0, 1.0 / 3.0, -0.5,",
-             "    0.63661977236758138243, 6755399441055744.0, 6.283185307179586 /* fl(2 pi) */};",
+             "    0.63661977236758138243, 6755399441055744.0, 6.283185307179586 /* fl(2 pi) */,",
+             f"    {float(64 / mp.pi)!r}, {PI64_0!r}, {PI64_1!r}, {PI64_2!r},",
+             "    -1.0 / 6.0, 1.0 / 120.0, -1.0 / 5040.0, -0.5, 1.0 / 24.0, -1.0 / 720.0};",
              "", "// {c_i, log(c_i)_hi, log(c_i)_lo, 0}, i = 0..128 (32-byte rows; copied to shared memory)",
              "__device__ const double kBmLogTab[129][4] = {"]
     for c, hi, lo in rows:
         lines.append(f"    {{{c!r}, {hi!r}, {lo!r}, 0.0}},")
+    lines += ["};", "", "// {sin(j pi/64), cos(j pi/64)}, j = 0..128, correctly rounded (exact 0 / +-1 at multiples of pi/2)",
+              "__device__ const double kBmSinCosTab[129][2] = {"]
+    for sv, cv in SC_TAB:
+        lines.append(f"    {{{sv!r}, {cv!r}}},")
     lines += ["};", "", "}  // namespace sk", ""]
     with open(OUT, "w") as f:
         f.write("\n".join(lines))

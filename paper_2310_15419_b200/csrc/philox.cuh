@@ -122,26 +122,31 @@ __device__ __forceinline__ void gaussian_pair(const uint4 x, double& g0, double&
 // instead of the libdevice calls.  Results agree with the libm-based oracle far inside the
 // Gaussian parity bound (1e-14 relative).
 
-// log(u) for u in (0, 1] (u normal).  tab = kBmLogTab rows {c, log c hi, log c lo, pad}.
-__device__ __forceinline__ double bm_log(double u, const double* __restrict__ tab) {
-  const unsigned long long b = (unsigned long long)__double_as_longlong(u);
-  const int e = (int)(b >> 52) - 1023;
+// -2 log(u1) for u1 = U 2^-53, U = k1 + 1 an integer in [1, 2^53] passed as an exact double (so
+// u1's scaling costs no multiply: exponent bias 53).  u = 2^e m, idx = round(128 (m - 1)), and with
+// the table rows {-2 c, 2 log(c)_hi, 2 log(c)_lo, pad}: s = fma(m, -2c, 2) = -2 (m c - 1) exactly
+// (|s| < 0.009), -2 log u = (e (-2 ln2_hi) + 2 L_hi) + (s + s^2 Q(s) + (e (-2 ln2_lo) + 2 L_lo)),
+// Q(s) = 1/4 + s/12 + s^2/32 + s^3/80 + s^4/192 + s^5/448 (= -P(-s/2)/2 for the Taylor P of
+// (log1p(r) - r) / r^2), the first bracket exact (2^-42 grid).  The factor -2 of Box-Muller is
+// folded into the constants: 12 FP64 operations, no multiply by -2.
+__device__ __forceinline__ double bm_m2log_u53(double U, const double* __restrict__ tab) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(U);
+  const int e = (int)(b >> 52) - (1023 + 53);
   const double m = __longlong_as_double((long long)((b & 0x000FFFFFFFFFFFFFull) | 0x3FF0000000000000ull));
   const int idx = (int)(((b >> 44) & 0xFFu) + 1u) >> 1;        // round(128 (m - 1)), 0..128
   const double2 ch = *reinterpret_cast<const double2*>(tab + 4 * idx);
   const double lo = tab[4 * idx + 2];
-  const double r = fma(m, ch.x, -1.0);                         // |r| < 0.0045
-  // (log1p(r) - r) / r^2 = L2 + L3 r + ... + L7 r^5 (Horner; Estrin measured slower)
-  const double r2 = r * r;
-  double p = fma(r, kBm[kL7], kBm[kL6]);
-  p = fma(r, p, kBm[kL5]);
-  p = fma(r, p, kBm[kL4]);
-  p = fma(r, p, kBm[kL3]);
-  p = fma(r, p, kBm[kL2]);
+  const double s = fma(m, ch.x, 2.0);                          // -2 r, |r| < 0.0045
+  const double s2 = s * s;
+  double q = fma(s, kBm[kQ5], kBm[kQ4]);
+  q = fma(s, q, kBm[kQ3]);
+  q = fma(s, q, kBm[kQ2]);
+  q = fma(s, q, kBm[kQ1]);
+  q = fma(s, q, kBm[kQ0]);
   const double ed = (double)e;
-  const double shi = fma(ed, kBm[kLn2Hi], -ch.y);              // exact: both on the 2^-42 grid
-  const double slo = fma(ed, kBm[kLn2Lo], -lo);
-  return shi + (r + fma(r2, p, slo));
+  const double shi = fma(ed, kBm[kM2Ln2Hi], ch.y);             // exact: both on the 2^-42 grid
+  const double slo = fma(ed, kBm[kM2Ln2Lo], lo);
+  return shi + (s + fma(s2, q, slo));
 }
 
 // sin and cos of th in [0, 2 pi) by table: j = rint(64 th / pi), r = th - j pi/64 (pi/64 in three
@@ -218,10 +223,10 @@ __device__ __forceinline__ double bm_sqrt(double x) {
 __device__ __forceinline__ void gaussian_pair_fast(const uint4 x, const double* __restrict__ tab, double& g0, double& g1) {
   const unsigned long long k1 = (((unsigned long long)x.x << 32) | x.y) >> 11;
   const unsigned long long k2 = (((unsigned long long)x.z << 32) | x.w) >> 11;
-  const double u1 = __dmul_rn(__ull2double_rn(k1 + 1ull), 0x1p-53);
-  const double u2 = __dmul_rn(__ull2double_rn(k2), 0x1p-53);
-  const double rho = bm_sqrt(-2.0 * bm_log(u1, tab));
-  const double th = __dmul_rn(u2, kBm[kTwoPi]);
+  // u1 = (k1 + 1) 2^-53 and u2 = k2 2^-53 are never formed: -2 log u1 takes the integer with an
+  // exponent bias, and th = u2 fl(2 pi) = k2 (2^-53 fl(2 pi)) is the same single rounding.
+  const double rho = bm_sqrt(bm_m2log_u53(__ull2double_rn(k1 + 1ull), tab));
+  const double th = __dmul_rn(__ull2double_rn(k2), kBm[kTwoPi53]);
   double s, c;
   bm_sincos(th, s, c);
   g0 = __dmul_rn(rho, c);

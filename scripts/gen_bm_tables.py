@@ -13,6 +13,10 @@ log(u), u in (0, 1]:  u = 2^e m, m in [1, 2); idx = round(128 (m - 1)) in [0, 12
   and P the Taylor polynomial of (log1p(r) - r) / r^2 to degree 5.
 sin / cos on |r| <= pi/4 after the Cody-Waite reduction r = theta - k pi/2 (pi/2 in four parts):
   the minimax kernels of fdlibm (Sun Microsystems, 1993; public domain), error < 1 ulp.
+-2 log(u1) directly (bm_m2log_u53, the form in use): the same table scaled by -2 / 2 (rows {-2c,
+  2 L_hi, 2 L_lo}), s = fma(m, -2c, 2) = -2r exactly, and Q(s) = -P(-s/2)/2 = 1/4 + s/12 + s^2/32
+  + s^3/80 + s^4/192 + s^5/448, so the factor -2 of Box-Muller costs no multiply; u1 enters as
+  the integer k1 + 1 (exponent bias 53) and theta = k2 (2^-53 fl(2 pi)), one multiply each.
 sin / cos by table (bm_sincos, the one in use): j = rint(64 theta / pi) in [0, 128],
   r = theta - j pi/64 (pi/64 in three parts, j pi/64 exact for the first two), |r| <= pi/128;
   sin r = r + r^3 (-1/6 + r^2 (1/120 - r^2/5040)), cos r = 1 + r^2 (-1/2 + r^2 (1/24 - r^2/720))
@@ -112,6 +116,26 @@ def bm_log(u: float, rows) -> float:
     return (e * LN2_HI - hi) + (r + (r * r * p + (e * LN2_LO - lo)))
 
 
+Q = [1 / 4, 1 / 12, 1 / 32, 1 / 80, 1 / 192, 1 / 448]
+
+
+def bm_m2log_u53(K: int, rows) -> float:
+    """float64 emulation (with fma) of philox.cuh bm_m2log_u53: -2 log(K 2^-53), 1 <= K <= 2^53."""
+    U = float(K)
+    b = struct.unpack("<Q", struct.pack("<d", U))[0]
+    e = ((b >> 52) & 0x7FF) - 1023 - 53
+    m = struct.unpack("<d", struct.pack("<Q", (b & ((1 << 52) - 1)) | (0x3FF << 52)))[0]
+    idx = (((b >> 44) & 0xFF) + 1) >> 1
+    c, hi, lo = rows[idx]
+    sv = fma(m, -2.0 * c, 2.0)
+    q = fma(sv, Q[5], Q[4])
+    for k in (3, 2, 1, 0):
+        q = fma(sv, q, Q[k])
+    shi = fma(float(e), -2.0 * LN2_HI, 2.0 * hi)
+    slo = fma(float(e), -2.0 * LN2_LO, 2.0 * lo)
+    return shi + (sv + fma(sv * sv, q, slo))
+
+
 def kernels(r: float):
     z = r * r
     v = z * r
@@ -137,6 +161,18 @@ def check(n: int, rows) -> None:
             worst_log = max(worst_log, float(abs((got - ref) / ref)))
         else:
             assert got == 0.0
+    worst_m2 = 0.0
+    Ks = [rng.randrange(1, 2 ** 53 + 1) for _ in range(n)] + [1, 2, 2 ** 52, 2 ** 53, 2 ** 53 - 1]
+    Ks += [2 ** 53 - k for k in range(1, 200)] + [2 ** 52 + k for k in range(-50, 50)]
+    for K in Ks:
+        ref = -2 * mp.log(mp.mpf(K) * mp.mpf(2) ** -53)
+        got = bm_m2log_u53(K, rows)
+        if ref != 0:
+            worst_m2 = max(worst_m2, float(abs((got - ref) / ref)))
+        else:
+            assert got == 0.0
+    print(f"-2 log(u1) max rel error {worst_m2:.3g}")
+    assert worst_m2 < 8 * 2.0 ** -53
     for _ in range(n):
         r = rng.uniform(-float(mp.pi / 4), float(mp.pi / 4))
         s, c = kernels(r)
@@ -174,7 +210,8 @@ def write(rows) -> None:
              "// (fp64 immediates would be rebuilt with UMOV pairs at every use).",
              "enum BmK { kLn2Hi, kLn2Lo, kPio2_0, kPio2_1, kPio2_2, kPio2_3, kS1, kS2, kS3, kS4, kS5, kS6,",
              "           kC1, kC2, kC3, kC4, kC5, kC6, kL7, kL6, kL5, kL4, kL3, kL2, kTwoOverPi, kRound, kTwoPi,",
-             "           k64OverPi, kPi64_0, kPi64_1, kPi64_2, kT3, kT5, kT7, kU2, kU4, kU6, kBmKCount };",
+             "           k64OverPi, kPi64_0, kPi64_1, kPi64_2, kT3, kT5, kT7, kU2, kU4, kU6,",
+             "           kQ0, kQ1, kQ2, kQ3, kQ4, kQ5, kM2Ln2Hi, kM2Ln2Lo, kTwoPi53, kBmKCount };",
              "__device__ __constant__ double kBm[kBmKCount] = {",
              f"    {LN2_HI!r}, {LN2_LO!r},",
              "    1.57079632673412561417e+00, 6.07710050630396597660e-11, 2.02226624871116645580e-21,",
@@ -184,11 +221,14 @@ def write(rows) -> None:
              "    1.0 / 7.0, -1.0 / 6.0, 1.0 / 5.0, -1.0 / 4.0, 1.0 / 3.0, -0.5,",
              "    0.63661977236758138243, 6755399441055744.0, 6.283185307179586 /* fl(2 pi) */,",
              f"    {float(64 / mp.pi)!r}, {PI64_0!r}, {PI64_1!r}, {PI64_2!r},",
-             "    -1.0 / 6.0, 1.0 / 120.0, -1.0 / 5040.0, -0.5, 1.0 / 24.0, -1.0 / 720.0};",
-             "", "// {c_i, log(c_i)_hi, log(c_i)_lo, 0}, i = 0..128 (32-byte rows; copied to shared memory)",
+             "    -1.0 / 6.0, 1.0 / 120.0, -1.0 / 5040.0, -0.5, 1.0 / 24.0, -1.0 / 720.0,",
+             "    1.0 / 4.0, 1.0 / 12.0, 1.0 / 32.0, 1.0 / 80.0, 1.0 / 192.0, 1.0 / 448.0,",
+             f"    {-2.0 * LN2_HI!r}, {-2.0 * LN2_LO!r}, {6.283185307179586 * 2.0 ** -53!r} /* fl(2 pi) 2^-53 */}};",
+             "", "// {-2 c_i, 2 log(c_i)_hi, 2 log(c_i)_lo, 0}, i = 0..128 (32-byte rows; copied to shared memory):",
+             "// the table of log u scaled for -2 log u (bm_m2log_u53)",
              "__device__ const double kBmLogTab[129][4] = {"]
     for c, hi, lo in rows:
-        lines.append(f"    {{{c!r}, {hi!r}, {lo!r}, 0.0}},")
+        lines.append(f"    {{{-2.0 * c!r}, {2.0 * hi!r}, {2.0 * lo!r}, 0.0}},")
     lines += ["};", "", "// {sin(j pi/64), cos(j pi/64)}, j = 0..128, correctly rounded (exact 0 / +-1 at multiples of pi/2)",
               "__device__ const double kBmSinCosTab[129][2] = {"]
     for sv, cv in SC_TAB:

@@ -103,6 +103,15 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def launches_per_apply(plan, dist: str, stats: dict) -> int:
+    """Kernels one sketch_apply launches: the fused kernel, plus the zeroing kernel of the fp4
+    path's K-split last wave when the plan made one."""
+    if not (stats["n_items_rad"] or stats["n_items_pair"]):
+        return 0
+    split = stats.get("n_items_f4_split", 0) > 0 and "sk_rad_f4_kernel" in plan.kernel_name(dist)
+    return 2 if split else 1
+
+
 def load_profile_traffic(config: str, kernel: str):
     """dram bytes (read + write) per launch of `kernel` on `config` from the committed
     `ncu --set full` capture (profiles/traffic.json), or None."""
@@ -394,7 +403,7 @@ def main():
                        "plan_ms": plan_ms, "kernel_ms": t_kern,
                        "reduce": "NCCL all_reduce of d x n partials" if reduce_partials else None},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "clocks": clocks, "gpu_launches": args.steps * (1 if stats["n_items_rad"] or stats["n_items_pair"] else 0),
+            "clocks": clocks, "gpu_launches": args.steps * launches_per_apply(plan, cfg.dist, stats),
         }
         print(json.dumps(line))
     plan.close()

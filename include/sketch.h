@@ -82,6 +82,8 @@ typedef struct {
     int64_t plan_bytes;        /* device bytes the plan owns */
     int64_t n_items_jki;       /* work items of the Algorithm 4 (jki) path, 0 if not built */
     int64_t jki_nonzero_rows;  /* Σ over 16-column groups of the group's nonzero rows (its RNG work) */
+    int64_t n_items_f4_split;  /* fp4 tensor-core items that are halves of a last-wave item split along
+                                  K (0: no split; > 0: apply also launches a small zeroing kernel) */
 } sk_stats_t;
 
 /*

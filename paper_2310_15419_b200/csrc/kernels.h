@@ -62,6 +62,9 @@ cudaError_t launch_apply_rad_tc(const ApplyArgs& a, const TcItem* items, int64_t
                                 cudaStream_t stream);
 int tc_tiles_per_cta();
 cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const TcItem* items, int64_t n_items, cudaStream_t stream);
+// Zeroes the output rows of K-split fp4 items (TcItem.pad: 0 whole column, 1 / 2 first / second half
+// of its K-steps; the halves atomically add into the zeroed rows).
+cudaError_t launch_f4_zero_split(const ApplyArgs& a, const TcItem* items, int64_t n_items, cudaStream_t stream);
 
 // ±1 x fp32 values through 4-nonzero subset-sum tables (sketch_tab.cu); items of <= 16 row tiles.
 int tab_tiles_per_cta();

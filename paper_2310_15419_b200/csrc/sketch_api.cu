@@ -210,6 +210,9 @@ struct sk_plan_s {
   sk::TcItem* d_tc = nullptr;       // tensor-core ±1 fp64 schedules (empty if not eligible):
   int64_t n_tc = 0;                 //   [int8 items (16 tiles) | fp4 items (6 tiles)]
   int64_t n_f4 = 0;
+  int64_t f4_tail_first = 0;        // fp4 items [f4_tail_first, n_f4): the last wave, split along K
+  int64_t f4_tail_n = 0;            //   (0 if not split)
+  int64_t f4_split_items = 0;       // half items among them
   sk::TcItem* d_f4t = nullptr;      // S-in-TMEM fp4 schedule: (column, 512-row block), longest first
   int64_t n_f4t = 0;
   sk::NItem* d_f4n = nullptr;       // S-as-N fp4 schedule: (column, 256-row tile), longest first
@@ -376,6 +379,38 @@ int validate_colptr(const int64_t* h, int64_t n, int64_t nnz, bool require_zero_
   return SK_OK;
 }
 
+// Last-wave split of the fp4 schedule.  Items cost about the same and the hardware hands them to
+// SMs in order, so N items on W SMs take ceil(N / W) item-times; when the last wave is less than
+// half full (0 < N mod W < W/2), splitting the last W + N mod W items into two halves along K
+// (same rows, half the nonzeros each) turns the final 2 item-times into 1.5.  The halves add into
+// Â with one fp64 atomicAdd each onto zeroed rows: 0 + a + b rounds identically in either order,
+// so results stay deterministic.  SKETCH_F4_SPLIT=0 disables it.
+void split_f4_tail(sk_plan_s* p, std::vector<sk::TcItem>& f4, const int64_t* h_colptr) {
+  static const bool off = [] { const char* v = getenv("SKETCH_F4_SPLIT"); return v && !strcmp(v, "0"); }();
+  int W = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&W, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t N = (int64_t)f4.size(), r = W > 0 ? N % W : 0;
+  if (off || W <= 0 || N <= W || r == 0 || 2 * r >= W) return;
+  const int64_t first = N - W - r;
+  std::vector<sk::TcItem> out(f4.begin(), f4.begin() + first);
+  int64_t halves = 0;
+  for (int64_t i = first; i < N; ++i) {
+    sk::TcItem it = f4[(size_t)i];
+    if (h_colptr[it.col + 1] - h_colptr[it.col] >= 128) {   // at least two K-steps
+      it.pad = 1; out.push_back(it);
+      it.pad = 2; out.push_back(it);
+      halves += 2;
+    } else {
+      out.push_back(it);
+    }
+  }
+  if (halves == 0) return;
+  p->f4_tail_first = first;
+  p->f4_tail_n = (int64_t)out.size() - first;
+  p->f4_split_items = halves;
+  f4.swap(out);
+}
+
 // Copy a plan's schedule image to the device on `stream` (one copy); `sync` waits for it and
 // drops the host image, otherwise the image stays alive until the plan is destroyed.
 int upload_plan(sk_plan_s* p, cudaStream_t stream, bool sync) {
@@ -424,6 +459,7 @@ int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
   if (tc_ok) {
     tc = build_tc_schedule(h_colptr, n, d, sk::tc_tiles_per_cta());
     std::vector<sk::TcItem> f4 = build_tc_schedule(h_colptr, n, d, sk::f4_tiles_per_cta());
+    split_f4_tail(p, f4, h_colptr);
     p->n_tc = (int64_t)tc.size();
     p->n_f4 = (int64_t)f4.size();
     tc.insert(tc.end(), f4.begin(), f4.end());
@@ -527,7 +563,10 @@ int apply_items(const sk_plan_s* p, uint64_t seed, sk_dist_t dist, const void* v
       e = cudaMallocAsync((void**)&counter, sizeof(int), stream);
       if (e == cudaSuccess) e = sk::launch_apply_rad_hybrid(a, p->d_tc, p->n_tc, counter, stream);
       if (counter) cudaFreeAsync(counter, stream);
-    } else if (path == SK_PATH_TC_FP4) e = sk::launch_apply_rad_f4(a, p->d_tc + p->n_tc, p->n_f4, stream);
+    } else if (path == SK_PATH_TC_FP4) {
+      e = sk::launch_f4_zero_split(a, p->d_tc + p->n_tc + p->f4_tail_first, p->f4_tail_n, stream);
+      if (e == cudaSuccess) e = sk::launch_apply_rad_f4(a, p->d_tc + p->n_tc, p->n_f4, stream);
+    }
     else e = sk::launch_apply_rad_tc(a, p->d_tc, p->n_tc, path == SK_PATH_TC_INT8_SMEM ? 1 : 0, stream);
   } else if ((dist == SK_UNIFORM || dist == SK_GAUSSIAN) && p->jki.n_items > 0 && pair_path() != SK_PAIR_KJI) {
     e = sk::launch_apply_jki((int)dist, (int)p->dtype, a, p->jki, stream);
@@ -851,6 +890,7 @@ int sketch_plan_stats(sk_plan_t plan, sk_stats_t* h) {
   h->philox_blocks_pair = plan->philox_pair;
   h->n_items_jki = plan->jki.n_items;
   h->jki_nonzero_rows = plan->jki_rows;
+  h->n_items_f4_split = plan->f4_split_items;
   h->plan_bytes = (plan->n_rad + plan->n_pair + plan->n_gauss) * (int64_t)sizeof(Item) +
                   (plan->n_tc + plan->n_f4 + plan->n_f4t) * (int64_t)sizeof(sk::TcItem) +
                   plan->n_f4n * (int64_t)sizeof(sk::NItem) +

@@ -235,7 +235,11 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
   F4Shared& sh = *reinterpret_cast<F4Shared*>(stages + kF4Stages * kF4Stage);
   const TcItem it = items[blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t pb = P.colptr[it.col], pe = P.colptr[it.col + 1];
+  int64_t pb = P.colptr[it.col], pe = P.colptr[it.col + 1];
+  if (it.pad) {   // last-wave item split along K: pad 1 = first half of the K-steps, 2 = second half
+    const int64_t half = ((((pe - pb) + 63) >> 6) >> 1) << 6;
+    if (it.pad == 1) pe = pb + half; else pb += half;
+  }
   const int64_t L = pe - pb;
   const int nsteps = (int)((L + 63) >> 6);
   const int nsup = (nsteps + kF4Sub - 1) / kF4Sub;
@@ -556,7 +560,9 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
       if (row < P.d) {
         // Σ_s 2^s D_s - D_64 = hi 2^32 + (lo - ones), both parts exact in fp64; one rounding
         const double v = scalbn((double)hi * 4294967296.0 + (double)(lo - ones), E - 62);
-        outc[row] = sh.nonfinite ? nan : v;
+        const double res = sh.nonfinite ? nan : v;
+        // K-split halves add into the zeroed output: 0 + a + b rounds the same in either order
+        if (it.pad) atomicAdd(outc + row, res); else outc[row] = res;
       }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -574,6 +580,22 @@ int f4_tiles_per_cta() {   // SKETCH_F4_TILES (tuning only): fewer row tiles per
   static const int t = [] { const char* v = getenv("SKETCH_F4_TILES"); const int x = v ? atoi(v) : kF4Tiles;
                             return x >= 1 && x <= kF4Tiles ? x : kF4Tiles; }();
   return t;
+}
+
+// Zero the Â rows of the K-split items (pad == 1 marks the first half of each pair).
+__global__ void sk_f4_zero_split_kernel(const ApplyArgs P, const TcItem* items) {
+  const TcItem it = items[blockIdx.x];
+  if (it.pad != 1) return;
+  const int64_t r0 = (int64_t)it.tile0 * 128;
+  const int64_t r1 = min(P.d, (int64_t)(it.tile0 + it.ntiles) * 128);
+  double* o = reinterpret_cast<double*>(P.out) + (int64_t)it.col * P.ld;
+  for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) o[r] = 0.0;
+}
+
+cudaError_t launch_f4_zero_split(const ApplyArgs& a, const TcItem* items, int64_t n_items, cudaStream_t stream) {
+  if (n_items == 0) return cudaSuccess;
+  sk_f4_zero_split_kernel<<<(unsigned)n_items, 256, 0, stream>>>(a, items);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const TcItem* items, int64_t n_items, cudaStream_t stream) {

@@ -227,6 +227,30 @@ def test_rad_f32_kernel_paths(sk, path):
         sk.set_rad_f32_path("simt")
 
 
+def test_f4_last_wave_split_along_k(sk):
+    # 160 one-item columns on 148 SMs: the plan splits the last wave (here every item) into two
+    # K halves that add into zeroed rows.  Results match the oracle, short columns (< 2 K-steps)
+    # stay whole, and two runs are bit-identical (0 + a + b rounds the same in either order).
+    import torch
+    lens = [300] * 160
+    lens[7], lens[50], lens[51] = 40, 127, 129
+    A = workloads.random_csc(60000, 160, lens, seed=23)
+    plan = sk.Plan(_dev(A.colptr), _dev(A.rowidx), 700, A.m, "f64")
+    try:
+        st = plan.stats()
+        if torch.cuda.get_device_properties(0).multi_processor_count == 148:
+            assert st["n_items_f4_split"] == 2 * 158
+        assert "sk_rad_f4_kernel" in plan.kernel_name("rademacher")
+        vals = _dev(A.vals)
+        o1 = plan.apply(vals, 3, "rademacher").T.cpu().numpy()
+        o2 = plan.apply(vals, 3, "rademacher").T.cpu().numpy()
+        assert np.array_equal(o1, o2)
+        ref, B = oracle.sketch(3, "rademacher", 700, A.m, A.n, A.colptr, A.rowidx, A.vals, threads=8)
+        _check(o1, ref, B, TOL["f64"])
+    finally:
+        plan.close()
+
+
 def test_kernel_names_report_the_path(sk):
     A = workloads.random_csc(10000, 4, 300, seed=1)
     plan = sk.Plan(_dev(A.colptr), _dev(A.rowidx), 300, A.m, "f64")

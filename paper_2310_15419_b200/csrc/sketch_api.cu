@@ -753,40 +753,66 @@ int sketch_apply_host(uint64_t seed, sk_dist_t dist, sk_dtype_t dtype, int64_t d
   cudaStream_t stream = (cudaStream_t)stream_;
   const size_t w = dtype_bytes(dtype);
 
-  // Column groups with balanced nnz; group g+1's upload overlaps group g's kernels.
-  int G = pipeline_chunks > 0 ? pipeline_chunks : (int)std::min<int64_t>(8, std::max<int64_t>(1, nnz / (1 << 21)));
+  // Column groups by nnz; group g+1's upload overlaps group g's kernels.  Group sizes shrink
+  // geometrically (ratio SKETCH_HOST_RATIO, default 0.84 ~ compute / upload time per byte on c5) so
+  // the previous group's kernels finish about when the next group lands, and the compute left
+  // after the last upload (the end-to-end tail) is only the small last group's.
+  int G = pipeline_chunks > 0 ? pipeline_chunks : (int)std::min<int64_t>(10, std::max<int64_t>(1, nnz / (1 << 21)));
   G = (int)std::max<int64_t>(1, std::min<int64_t>(G, n));
   std::vector<int64_t> cb((size_t)G + 1, 0);
   {
+    std::vector<double> wsum((size_t)G + 1, 0.0);
+    static const double ratio = [] { const char* v = getenv("SKETCH_HOST_RATIO"); const double r = v ? atof(v) : 0.84;
+                                     return r > 0.1 && r <= 1.0 ? r : 0.84; }();
+    double wg = 1.0;
+    for (int g = 0; g < G; ++g, wg *= ratio) wsum[g + 1] = wsum[g] + wg;
     int64_t k = 0;
     for (int g = 1; g < G; ++g) {
-      const int64_t target = (nnz * g) / G;
+      const int64_t target = (int64_t)((double)nnz * wsum[g] / wsum[G]);
       while (k < n && h_colptr[k] < target) ++k;
       cb[g] = std::max(cb[g - 1], k);
     }
     cb[G] = n;
   }
 
-  cudaStream_t h2d = nullptr, d2h = nullptr;
-  std::vector<cudaEvent_t> ev_in(G), ev_done(G);
-  cudaEvent_t ev_start = nullptr, ev_end = nullptr;
+  // Streams and events are per host thread and device, created once and reused (their creation
+  // and destruction cost more than the copy / kernel overlap wins on small calls).  The call is
+  // synchronous, so reuse across calls is safe.
+  struct HostPipe {
+    int dev = -1;
+    cudaStream_t h2d = nullptr, d2h = nullptr, comp2 = nullptr;
+    std::vector<cudaEvent_t> ev;
+  };
+  thread_local HostPipe hp;
+  cudaError_t e = cudaSuccess;
+  const char* what = "";
+#define SK_STEP(call) do { if (e == cudaSuccess) { e = (call); if (e != cudaSuccess) what = #call; } } while (0)
+  {
+    int dev = 0;
+    SK_STEP(cudaGetDevice(&dev));
+    if (e == cudaSuccess && hp.dev != dev) {
+      hp = HostPipe();
+      SK_STEP(cudaStreamCreateWithFlags(&hp.h2d, cudaStreamNonBlocking));
+      SK_STEP(cudaStreamCreateWithFlags(&hp.d2h, cudaStreamNonBlocking));
+      SK_STEP(cudaStreamCreateWithFlags(&hp.comp2, cudaStreamNonBlocking));
+      if (e == cudaSuccess) hp.dev = dev;
+    }
+    while (e == cudaSuccess && hp.ev.size() < (size_t)(2 * G + 2)) {
+      cudaEvent_t ev;
+      SK_STEP(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      if (e == cudaSuccess) hp.ev.push_back(ev);
+    }
+  }
+  if (e != cudaSuccess) return cuda_fail(e, what);
+  cudaStream_t h2d = hp.h2d, d2h = hp.d2h, comp2 = hp.comp2;   // comp2: odd groups' kernels
+  std::vector<cudaEvent_t> ev_in(hp.ev.begin() + 2, hp.ev.begin() + 2 + G), ev_done(hp.ev.begin() + 2 + G, hp.ev.begin() + 2 + 2 * G);
+  cudaEvent_t ev_start = hp.ev[0], ev_end = hp.ev[1];
   int64_t* d_colptr = nullptr;
   int32_t* d_rowidx = nullptr;
   void* d_vals = nullptr;
   void* d_out = nullptr;
   int* d_flag = nullptr;
   int h_flag = 0;
-  cudaError_t e = cudaSuccess;
-  const char* what = "";
-#define SK_STEP(call) do { if (e == cudaSuccess) { e = (call); if (e != cudaSuccess) what = #call; } } while (0)
-  SK_STEP(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
-  SK_STEP(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
-  SK_STEP(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
-  SK_STEP(cudaEventCreateWithFlags(&ev_end, cudaEventDisableTiming));
-  for (int g = 0; g < G; ++g) {
-    SK_STEP(cudaEventCreateWithFlags(&ev_in[g], cudaEventDisableTiming));
-    SK_STEP(cudaEventCreateWithFlags(&ev_done[g], cudaEventDisableTiming));
-  }
   SK_STEP(cudaMallocAsync((void**)&d_colptr, (size_t)(n + 1) * 8, stream));
   SK_STEP(cudaMallocAsync((void**)&d_rowidx, (size_t)std::max<int64_t>(nnz, 1) * 4, stream));
   SK_STEP(cudaMallocAsync(&d_vals, (size_t)std::max<int64_t>(nnz, 1) * w, stream));
@@ -805,11 +831,19 @@ int sketch_apply_host(uint64_t seed, sk_dist_t dist, sk_dtype_t dtype, int64_t d
                               cudaMemcpyHostToDevice, h2d));
     }
   };
+  static const bool timing = getenv("SKETCH_TIMING") != nullptr;
+  // SKETCH_TIMING: timeline of uploads / kernels / downloads (stderr), relative to the start
+  std::vector<cudaEvent_t> tev;
+  auto tmark = [&](cudaStream_t st) {
+    if (!timing) return;
+    cudaEvent_t ev;
+    if (cudaEventCreate(&ev) == cudaSuccess) { cudaEventRecord(ev, st); tev.push_back(ev); }
+  };
   SK_STEP(cudaEventRecord(ev_start, stream));
   SK_STEP(cudaStreamWaitEvent(h2d, ev_start, 0));
+  tmark(h2d);
   SK_STEP(cudaMemcpyAsync(d_colptr, h_colptr, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, h2d));
   upload_group(0);
-  static const bool timing = getenv("SKETCH_TIMING") != nullptr;
   const auto t0 = std::chrono::steady_clock::now();
   std::vector<sk_plan_t> plans((size_t)G, nullptr);
   for (int g = 0; g < G && e == cudaSuccess; ++g) {
@@ -826,26 +860,34 @@ int sketch_apply_host(uint64_t seed, sk_dist_t dist, sk_dtype_t dtype, int64_t d
   for (int g = 0; g < G && e == cudaSuccess; ++g)
     if (plans[g] && upload_plan(plans[g], h2d, false) != SK_OK) { e = cudaErrorUnknown; what = "upload plan"; }
   SK_STEP(cudaEventRecord(ev_in[0], h2d));
+  tmark(h2d);
   for (int g = 1; g < G; ++g) {
     upload_group(g);
     SK_STEP(cudaEventRecord(ev_in[g], h2d));
+    tmark(h2d);
   }
+  // Consecutive groups' kernels alternate between the caller's stream and comp2, so a group's
+  // last partial wave of CTAs overlaps the next group's first one.
+  SK_STEP(cudaStreamWaitEvent(comp2, ev_start, 0));
   for (int g = 0; g < G; ++g) {
     const int64_t c0 = cb[g], c1 = cb[g + 1];
     const int64_t p0 = h_colptr[c0], p1 = h_colptr[c1];
-    SK_STEP(cudaStreamWaitEvent(stream, ev_in[g], 0));
-    if (p1 > p0 && e == cudaSuccess) e = sk::launch_validate_rows(d_rowidx + p0, p1 - p0, m, d_flag, stream);
+    cudaStream_t cs = (g & 1) ? comp2 : stream;
+    SK_STEP(cudaStreamWaitEvent(cs, ev_in[g], 0));
+    if (p1 > p0 && e == cudaSuccess) e = sk::launch_validate_rows(d_rowidx + p0, p1 - p0, m, d_flag, cs);
     if (e == cudaSuccess && c1 > c0) {
-      const int rca = apply_items(plans[g], seed, dist, d_vals, (char*)d_out + (size_t)(c0 * d) * w, stream);
+      const int rca = apply_items(plans[g], seed, dist, d_vals, (char*)d_out + (size_t)(c0 * d) * w, cs);
       if (rca != SK_OK) { e = cudaErrorLaunchFailure; what = "launch apply"; }
     }
-    SK_STEP(cudaEventRecord(ev_done[g], stream));
+    SK_STEP(cudaEventRecord(ev_done[g], cs));
+    tmark(cs);
     SK_STEP(cudaStreamWaitEvent(d2h, ev_done[g], 0));
     if (c1 > c0)
       SK_STEP(cudaMemcpyAsync((char*)h_out + (size_t)(c0 * d) * w, (char*)d_out + (size_t)(c0 * d) * w,
                               (size_t)((c1 - c0) * d) * w, cudaMemcpyDeviceToHost, d2h));
   }
   SK_STEP(cudaEventRecord(ev_end, d2h));
+  tmark(d2h);
   SK_STEP(cudaStreamWaitEvent(stream, ev_end, 0));
   SK_STEP(cudaMemcpyAsync(&h_flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, stream));
   if (d_colptr) cudaFreeAsync(d_colptr, stream);
@@ -855,15 +897,17 @@ int sketch_apply_host(uint64_t seed, sk_dist_t dist, sk_dtype_t dtype, int64_t d
   if (d_flag) cudaFreeAsync(d_flag, stream);
   cudaError_t es = cudaStreamSynchronize(stream);
   if (e == cudaSuccess && es != cudaSuccess) { e = es; what = "cudaStreamSynchronize"; }
-  for (int g = 0; g < G; ++g) {
-    if (ev_in[g]) cudaEventDestroy(ev_in[g]);
-    if (ev_done[g]) cudaEventDestroy(ev_done[g]);
+  if (timing && tev.size() == (size_t)(2 * G + 2)) {
+    // tev: [start, in 0 .. in G-1, done 0 .. done G-1, end]
+    auto at = [&](size_t i) { float ms = 0; cudaEventElapsedTime(&ms, tev[0], tev[i]); return ms; };
+    fprintf(stderr, "apply_host timeline (ms):");
+    for (int g = 0; g < G; ++g) fprintf(stderr, " [g%d in %.2f done %.2f]", g, at(1 + g), at(1 + G + g));
+    fprintf(stderr, " end %.2f\n", at(2 * G + 1));
   }
+  for (auto ev : tev) cudaEventDestroy(ev);
+
   for (auto pl : plans) sketch_plan_destroy(pl);
-  if (ev_start) cudaEventDestroy(ev_start);
-  if (ev_end) cudaEventDestroy(ev_end);
-  if (h2d) cudaStreamDestroy(h2d);
-  if (d2h) cudaStreamDestroy(d2h);
+
 #undef SK_STEP
   if (e != cudaSuccess) return cuda_fail(e, what);
   return h_flag ? SK_ECSC : SK_OK;

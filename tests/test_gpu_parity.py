@@ -251,6 +251,37 @@ def test_f4_last_wave_split_along_k(sk):
         plan.close()
 
 
+@pytest.mark.parametrize("case", range(16))
+def test_randomized_shapes_match_oracle(sk, case):
+    # seeded random shapes through the default kernel selection: m, n, column lengths (empty,
+    # short, >= 256 so the tensor-core path is eligible, occasionally one very long column), d
+    # (ragged, tiny, > 2048), dtype, distribution and a nonzero row offset
+    rng = np.random.default_rng(1000 + case)
+    m = int(rng.integers(1, 60000))
+    n = int(rng.integers(1, 24))
+    kind = case % 4
+    if kind == 0:
+        lens = rng.integers(0, 40, n)
+    elif kind == 1:
+        lens = rng.integers(256, 700, n)
+    elif kind == 2:
+        lens = rng.integers(0, 900, n)
+        lens[int(rng.integers(0, n))] = min(m, 5000)
+    else:
+        lens = rng.integers(300, 400, n)
+    lens = [int(min(L, m)) for L in lens]
+    d = int(rng.choice([1, 2, 127, 129, 700, 1025, 2049, int(rng.integers(1, 2200))]))
+    dtype = np.float32 if case % 3 == 2 else np.float64
+    dist = ["rademacher", "uniform", "gaussian", "uniform24"][case % 4 if case % 5 else 0]
+    A = workloads.random_csc(m, n, lens, seed=case, dtype=dtype, sorted_rows=bool(case % 2),
+                             duplicates=case % 7 == 3)
+    A.row_offset = int(rng.integers(0, 1 << 20))
+    got = _gpu_sketch(sk, A, d, dist, 17 + case)
+    ref, B = oracle.sketch(17 + case, dist, d, A.m, A.n, A.colptr, A.rowidx, A.vals, row_offset=A.row_offset,
+                           threads=8)
+    _check(got, ref, B, TOL["f32" if dtype == np.float32 else "f64"])
+
+
 def test_kernel_names_report_the_path(sk):
     A = workloads.random_csc(10000, 4, 300, seed=1)
     plan = sk.Plan(_dev(A.colptr), _dev(A.rowidx), 300, A.m, "f64")

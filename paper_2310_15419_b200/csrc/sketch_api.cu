@@ -265,7 +265,7 @@ int build_jki(sk_plan_s* p, const int64_t* h_colptr, bool force, cudaStream_t st
     }
     if (picked.empty()) return SK_OK;
     const size_t words = (size_t)((p->m + 31) / 32);
-    if (p->m <= (int64_t(1) << 31)) {
+    if (p->m <= (int64_t(1) << 28)) {   // bitmap <= 32 MB; taller shards sample on the host
       uint32_t* bitmap = nullptr;
       unsigned long long* cnt = nullptr;
       std::vector<unsigned long long> h_cnt(picked.size(), 0);

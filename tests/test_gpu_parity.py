@@ -382,6 +382,30 @@ def test_degenerate_shapes(sk):
     assert plan.apply(torch.zeros(0, dtype=torch.float64, device="cuda"), 1, "uniform").shape == (0, 5)
 
 
+def test_extreme_index_ranges(sk):
+    # global rows near 2^31 (m just below the int32 bound, rows at the top of the range, plus a
+    # row offset past 2^32 so the Philox counter's high word j >> 32 is nonzero) and a large d
+    # (many row tiles: tile indices and Philox block indices q far from 0), on the default paths
+    rng = np.random.default_rng(77)
+    m = 2**31 - 1
+    n = 6
+    cols = []
+    for k in range(n):
+        L = 300 if k % 2 == 0 else 17
+        rows = np.sort(rng.choice(np.arange(m - 5000, m, dtype=np.int64), size=L, replace=False))
+        cols.append(rows)
+    colptr = np.zeros(n + 1, np.int64)
+    colptr[1:] = np.cumsum([len(c) for c in cols])
+    rowidx = np.concatenate(cols).astype(np.int32)
+    vals = rng.standard_normal(int(colptr[-1]))
+    A = workloads.CSC(m, n, colptr, rowidx, vals, row_offset=(1 << 32) + 12345)
+    for dist, d in (("rademacher", 70001), ("uniform", 9000), ("gaussian", 3001)):
+        got = _gpu_sketch(sk, A, d, dist, 5)
+        ref, B = oracle.sketch(5, dist, d, A.m, A.n, A.colptr, A.rowidx, A.vals, row_offset=A.row_offset,
+                               threads=8)
+        _check(got, ref, B, TOL["f64"])
+
+
 def test_csc_validation_errors(sk):
     import torch
     colptr = _dev(np.array([0, 2, 1, 3], np.int64))

@@ -223,7 +223,7 @@ __device__ __forceinline__ uint32_t f4_off(int m, int h) {
 // The debug switches exist only in builds with -DSK_F4_DEBUG=1 (the default build has none, so
 // they cannot perturb the schedule of the production kernel).
 #ifndef SK_F4_STAGGER_NS
-#define SK_F4_STAGGER_NS 600
+#define SK_F4_STAGGER_NS 0
 #endif
 #ifndef SK_F4_DEBUG
 #define SK_F4_DEBUG 0

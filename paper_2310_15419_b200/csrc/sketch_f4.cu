@@ -20,7 +20,7 @@
 //    K-major no-swizzle layout (8-row x 16-byte core matrices).  Inside each 32-nonzero K chunk,
 //    word c nibble n holds nonzero 4n + c for both A and B.
 //  * CTA = up to 12 A-producer warps (tile = w % T, nonzero half = w / T) + 2 B-producer warps +
-//    1 MMA warp; 2-stage smem ring, each stage 4 K-steps (A: T x 16 KB, B: 4 x 2.5 KB) with mbarrier
+//    1 MMA warp; 2-stage smem ring, each stage kF4Sub = 3 K-steps (A: T x 12 KB, B: 3 x 2.5 KB) with mbarrier
 //    full/empty (fewer, larger handshakes: 10.9 -> 8.4 ms on c5);
 //    block scale factors (ue8m0 = 1.0) live in TMEM columns [448, 512).
 // Measured (scripts/microbench_mxf4.cu): one M=128,K=64 mxf4 MMA reads its 4 KB A tile at
@@ -59,7 +59,7 @@ constexpr int kF4N = 72;                          // 64 digit rows + ones row + 
 constexpr int kF4Ones = 64;
 #endif
 #ifndef SK_F4_SUB
-#define SK_F4_SUB 4
+#define SK_F4_SUB 3                               // (4 at ptxas -O3; at -O1 3 measured 7.31 vs 7.35 ms)
 #define SK_F4_STAGES 2
 #endif
 constexpr int kF4Sub = SK_F4_SUB;                 // K-steps (64 nonzeros each) per smem stage
@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
     constexpr int kMine = kF4Sub / kF4KC;            // K-steps of a stage this warp produces
     static_assert(kMine * kF4KC == kF4Sub, "K-step classes must divide the stage");
     const uint32_t q = (uint32_t)(it.tile0 + t);
-    // One smem stage holds kF4Sub = 4 K-steps: the warp generates all of them (independent Philox
+    // One smem stage holds kF4Sub K-steps: the warp generates all of them (independent Philox
     // chains, 4 kF4Sub interleaved 32x32 transposes) and signals the stage once.  Their row indices
     // come from one ring slot (one wait, one release per stage; padding past the column end was
     // zero-filled by the loader).

@@ -282,6 +282,25 @@ def test_randomized_shapes_match_oracle(sk, case):
     _check(got, ref, B, TOL["f32" if dtype == np.float32 else "f64"])
 
 
+@pytest.mark.parametrize("dist,dtype", [("rademacher", "f64"), ("rademacher", "f32"), ("uniform", "f64"),
+                                        ("gaussian", "f64")])
+def test_repeated_runs_are_bit_identical(sk, dist, dtype):
+    # race check without a sanitizer: 25 back-to-back applies of the same plan on a matrix whose
+    # schedule uses every stage of the pipelines (long columns, ragged tail, K-split last wave)
+    # must give bit-identical outputs (all reductions have a fixed order; the tensor-core path
+    # accumulates integers)
+    import torch
+    A = workloads.random_csc(400000, 170, 1500, seed=31, dtype=np.float32 if dtype == "f32" else np.float64)
+    plan = sk.Plan(_dev(A.colptr), _dev(A.rowidx), 1900, A.m, dtype)
+    try:
+        vals = _dev(A.vals)
+        first = plan.apply(vals, 8, dist).clone()
+        for _ in range(24):
+            assert torch.equal(plan.apply(vals, 8, dist), first)
+    finally:
+        plan.close()
+
+
 def test_kernel_names_report_the_path(sk):
     A = workloads.random_csc(10000, 4, 300, seed=1)
     plan = sk.Plan(_dev(A.colptr), _dev(A.rowidx), 300, A.m, "f64")

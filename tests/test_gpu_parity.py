@@ -301,6 +301,29 @@ def test_repeated_runs_are_bit_identical(sk, dist, dtype):
         plan.close()
 
 
+@pytest.mark.parametrize("path", ["fp4", "fp4t", "fp4n", "int8smem", "simt"])
+def test_extreme_value_scales(sk, path):
+    # columns whose values are all subnormal, all near the top of the fp64 range, or mix both with
+    # exact zeros: the tensor-core paths scale each column by 2^(61-E) in two exact factors
+    A = workloads.random_csc(30000, 5, 400, seed=41)
+    v = A.vals.copy()
+    s = [slice(A.colptr[k], A.colptr[k + 1]) for k in range(5)]
+    v[s[0]] *= 1e-310                                  # subnormal
+    v[s[1]] *= 1e300                                   # huge (|Â| stays < 1e308 for 400 terms)
+    v[s[2]] = np.where(np.arange(400) % 2 == 0, v[s[2]] * 1e-300, v[s[2]] * 1e200)
+    v[s[3]] = 0.0                                      # all explicit zeros
+    v[s[4]][::3] = 0.0
+    A.vals = v
+    try:
+        sk.set_rad_f64_path(path)
+        got = _gpu_sketch(sk, A, 600, "rademacher", 9)
+        ref, B = oracle.sketch(9, "rademacher", 600, A.m, A.n, A.colptr, A.rowidx, A.vals, threads=8)
+        assert np.all(np.isfinite(got))
+        _check(got, ref, B, TOL["f64"])
+    finally:
+        sk.set_rad_f64_path("fp4")
+
+
 def test_kernel_names_report_the_path(sk):
     A = workloads.random_csc(10000, 4, 300, seed=1)
     plan = sk.Plan(_dev(A.colptr), _dev(A.rowidx), 300, A.m, "f64")

@@ -126,9 +126,9 @@ __device__ __forceinline__ void gaussian_pair(const uint4 x, double& g0, double&
 // u1's scaling costs no multiply: exponent bias 53).  u = 2^e m, idx = round(128 (m - 1)), and with
 // the table rows {-2 c, 2 log(c)_hi, 2 log(c)_lo, pad}: s = fma(m, -2c, 2) = -2 (m c - 1) exactly
 // (|s| < 0.009), -2 log u = (e (-2 ln2_hi) + 2 L_hi) + (s + s^2 Q(s) + (e (-2 ln2_lo) + 2 L_lo)),
-// Q(s) = 1/4 + s/12 + s^2/32 + s^3/80 + s^4/192 + s^5/448 (= -P(-s/2)/2 for the Taylor P of
-// (log1p(r) - r) / r^2), the first bracket exact (2^-42 grid).  The factor -2 of Box-Muller is
-// folded into the constants: 12 FP64 operations, no multiply by -2.
+// Q(s) = 1/4 + s/12 + s^2/32 + s^3/80 + s^4/192 (= -P(-s/2)/2 for the Taylor P of
+// (log1p(r) - r) / r^2, truncated where the next term is below 2^-60), the first bracket exact
+// (2^-42 grid).  The factor -2 of Box-Muller is folded into the constants: 11 FP64 operations.
 __device__ __forceinline__ double bm_m2log_u53(double U, const double* __restrict__ tab) {
   const unsigned long long b = (unsigned long long)__double_as_longlong(U);
   const int e = (int)(b >> 52) - (1023 + 53);
@@ -138,8 +138,7 @@ __device__ __forceinline__ double bm_m2log_u53(double U, const double* __restric
   const double lo = tab[4 * idx + 2];
   const double s = fma(m, ch.x, 2.0);                          // -2 r, |r| < 0.0045
   const double s2 = s * s;
-  double q = fma(s, kBm[kQ5], kBm[kQ4]);
-  q = fma(s, q, kBm[kQ3]);
+  double q = fma(s, kBm[kQ4], kBm[kQ3]);                       // (the s^5/448 term is below 2^-60)
   q = fma(s, q, kBm[kQ2]);
   q = fma(s, q, kBm[kQ1]);
   q = fma(s, q, kBm[kQ0]);

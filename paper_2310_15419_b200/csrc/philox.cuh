@@ -148,24 +148,23 @@ __device__ __forceinline__ double bm_m2log_u53(double U, const double* __restric
   return shi + (s + fma(s2, q, slo));
 }
 
-// sin and cos of th in [0, 2 pi) by table: j = rint(64 th / pi), r = th - j pi/64 (pi/64 in three
-// parts, the first two products exact), |r| <= pi/128, Taylor sin r / cos r to degree 7 / 6, and
+// sin and cos of th in [0, 2 pi) by table: j = rint(256 th / pi), r = th - j pi/256 (pi/256 in three
+// parts, the first two products exact), |r| <= pi/512, Taylor sin r / cos r to degree 5 / 4, and
 // sin th = S_j cos r + C_j sin r, cos th = C_j cos r - S_j sin r with the correctly rounded
-// S_j, C_j of kBmSinCosTab (exact zeros at multiples of pi/2: no cancellation where sin or cos
-// vanishes).  17 FP64 operations + one 16-byte load (L1-resident 2 KB table) instead of ~25
-// for the quadrant form below; <= 2.5e-16 relative (scripts/gen_bm_tables.py --check).
+// S_j, C_j of kBmSinCosTab (513 rows, 8 KB, L1-resident; exact zeros at multiples of pi/2: no
+// cancellation where sin or cos vanishes).  15 FP64 operations + one 16-byte load instead of ~25
+// for the quadrant form below; <= 3.3e-16 relative (scripts/gen_bm_tables.py --check).
 __device__ __forceinline__ void bm_sincos(double th, double& s, double& c) {
-  const double kr = fma(th, kBm[k64OverPi], kBm[kRound]);    // 1.5 2^52 + rint(64 th / pi)
+  const double kr = fma(th, kBm[kSCInv], kBm[kRound]);      // 1.5 2^52 + rint(256 th / pi)
   const double kd = kr - kBm[kRound];
-  double r = fma(-kd, kBm[kPi64_0], th);
-  r = fma(-kd, kBm[kPi64_1], r);
-  r = fma(-kd, kBm[kPi64_2], r);
-  const int j = __double2loint(kr) & 0xFF;                   // 0..128
+  double r = fma(-kd, kBm[kSCPi_0], th);
+  r = fma(-kd, kBm[kSCPi_1], r);
+  r = fma(-kd, kBm[kSCPi_2], r);
+  const int j = __double2loint(kr) & 0x3FF;                  // 0..512
   const double2 t = __ldg(reinterpret_cast<const double2*>(&kBmSinCosTab[j][0]));
   const double z = r * r;
-  const double ps = fma(z, fma(z, kBm[kT7], kBm[kT5]), kBm[kT3]);
-  const double sr = fma(z * r, ps, r);
-  const double cr = fma(z, fma(z, fma(z, kBm[kU6], kBm[kU4]), kBm[kU2]), 1.0);
+  const double sr = fma(z * r, fma(z, kBm[kT5], kBm[kT3]), r);
+  const double cr = fma(z, fma(z, kBm[kU4], kBm[kU2]), 1.0);
   s = fma(t.x, cr, t.y * sr);
   c = fma(t.y, cr, -(t.x * sr));
 }

@@ -18,11 +18,11 @@ sin / cos on |r| <= pi/4 after the Cody-Waite reduction r = theta - k pi/2 (pi/2
   + s^3/80 + s^4/192 (+ s^5/448, dropped: same worst case 1.3e-16 over random and idx-boundary
   inputs), so the factor -2 of Box-Muller costs no multiply; u1 enters as
   the integer k1 + 1 (exponent bias 53) and theta = k2 (2^-53 fl(2 pi)), one multiply each.
-sin / cos by table (bm_sincos, the one in use): j = rint(64 theta / pi) in [0, 128],
-  r = theta - j pi/64 (pi/64 in three parts, j pi/64 exact for the first two), |r| <= pi/128;
-  sin r = r + r^3 (-1/6 + r^2 (1/120 - r^2/5040)), cos r = 1 + r^2 (-1/2 + r^2 (1/24 - r^2/720))
-  (Taylor; the next terms are below 2^-60 relative); sin theta = S_j cos r + C_j sin r,
-  cos theta = C_j cos r - S_j sin r with S_j, C_j = sin, cos (j pi/64) correctly rounded (exact
+sin / cos by table (bm_sincos, the one in use): j = rint(256 theta / pi) in [0, 512],
+  r = theta - j pi/256 (pi/256 in three parts, j pi/256 exact for the first two), |r| <= pi/512;
+  sin r = r + r^3 (-1/6 + r^2/120), cos r = 1 + r^2 (-1/2 + r^2/24) (Taylor; the next terms are
+  below 2^-55 relative on this interval); sin theta = S_j cos r + C_j sin r,
+  cos theta = C_j cos r - S_j sin r with S_j, C_j = sin, cos (j pi/256) correctly rounded (exact
   zeros at multiples of pi/2, so no cancellation near the zeros of sin and cos).
 """
 import argparse
@@ -61,13 +61,14 @@ def round_grid(x, g):
 LN2 = mp.log(2)
 LN2_HI = round_grid(LN2, 42)
 LN2_LO = float(LN2 - LN2_HI)
-PI64 = mp.pi / 64
-PI64_0 = round_bits(PI64, 44)                  # j * PI64_0 exact for j <= 128 (8 + 44 bits)
-PI64_1 = round_bits(PI64 - PI64_0, 44)
-PI64_2 = float(PI64 - PI64_0 - PI64_1)
-SC_TAB = [(float(mp.sin(j * PI64)), float(mp.cos(j * PI64))) for j in range(129)]
-for j in (0, 32, 64, 96, 128):                 # exact zeros / ones at multiples of pi/2
-    SC_TAB[j] = (float(mp.nint(mp.sin(j * PI64))), float(mp.nint(mp.cos(j * PI64))))
+NSC = 512                                      # sin / cos table intervals over [0, 2 pi)
+PISC = 2 * mp.pi / NSC
+PISC_0 = round_bits(PISC, 43)                  # j * PISC_0 exact for j <= 512 (10 + 43 bits)
+PISC_1 = round_bits(PISC - PISC_0, 43)
+PISC_2 = float(PISC - PISC_0 - PISC_1)
+SC_TAB = [(float(mp.sin(j * PISC)), float(mp.cos(j * PISC))) for j in range(NSC + 1)]
+for j in range(0, NSC + 1, NSC // 4):          # exact zeros / ones at multiples of pi/2
+    SC_TAB[j] = (float(mp.nint(mp.sin(j * PISC))), float(mp.nint(mp.cos(j * PISC))))
 
 
 def fma(a, b, c):
@@ -76,17 +77,17 @@ def fma(a, b, c):
 
 def bm_sincos_tab(th: float):
     """float64 emulation (with fma) of philox.cuh bm_sincos."""
-    kr = fma(th, float(64 / mp.pi), 6755399441055744.0)
+    kr = fma(th, float(1 / PISC), 6755399441055744.0)
     kd = kr - 6755399441055744.0
     j = int(kd)
-    r = fma(-kd, PI64_0, th)
-    r = fma(-kd, PI64_1, r)
-    r = fma(-kd, PI64_2, r)
+    r = fma(-kd, PISC_0, th)
+    r = fma(-kd, PISC_1, r)
+    r = fma(-kd, PISC_2, r)
     S, C = SC_TAB[j]
     z = r * r
-    ps = fma(z, fma(z, -1.0 / 5040.0, 1.0 / 120.0), -1.0 / 6.0)
+    ps = fma(z, 1.0 / 120.0, -1.0 / 6.0)
     sr = fma(z * r, ps, r)
-    cr = fma(z, fma(z, fma(z, -1.0 / 720.0, 1.0 / 24.0), -0.5), 1.0)
+    cr = fma(z, fma(z, 1.0 / 24.0, -0.5), 1.0)
     return fma(S, cr, C * sr), fma(C, cr, -(S * sr))
 
 
@@ -214,7 +215,7 @@ def write(rows) -> None:
              "// (fp64 immediates would be rebuilt with UMOV pairs at every use).",
              "enum BmK { kLn2Hi, kLn2Lo, kPio2_0, kPio2_1, kPio2_2, kPio2_3, kS1, kS2, kS3, kS4, kS5, kS6,",
              "           kC1, kC2, kC3, kC4, kC5, kC6, kL7, kL6, kL5, kL4, kL3, kL2, kTwoOverPi, kRound, kTwoPi,",
-             "           k64OverPi, kPi64_0, kPi64_1, kPi64_2, kT3, kT5, kT7, kU2, kU4, kU6,",
+             "           kSCInv, kSCPi_0, kSCPi_1, kSCPi_2, kT3, kT5, kT7, kU2, kU4, kU6,",
              "           kQ0, kQ1, kQ2, kQ3, kQ4, kQ5, kM2Ln2Hi, kM2Ln2Lo, kTwoPi53, kBmKCount };",
              "__device__ __constant__ double kBm[kBmKCount] = {",
              f"    {LN2_HI!r}, {LN2_LO!r},",
@@ -224,7 +225,7 @@ def write(rows) -> None:
              "    " + ", ".join(repr(x) for x in C) + ",",
              "    1.0 / 7.0, -1.0 / 6.0, 1.0 / 5.0, -1.0 / 4.0, 1.0 / 3.0, -0.5,",
              "    0.63661977236758138243, 6755399441055744.0, 6.283185307179586 /* fl(2 pi) */,",
-             f"    {float(64 / mp.pi)!r}, {PI64_0!r}, {PI64_1!r}, {PI64_2!r},",
+             f"    {float(1 / PISC)!r}, {PISC_0!r}, {PISC_1!r}, {PISC_2!r},",
              "    -1.0 / 6.0, 1.0 / 120.0, -1.0 / 5040.0, -0.5, 1.0 / 24.0, -1.0 / 720.0,",
              "    1.0 / 4.0, 1.0 / 12.0, 1.0 / 32.0, 1.0 / 80.0, 1.0 / 192.0, 1.0 / 448.0,",
              f"    {-2.0 * LN2_HI!r}, {-2.0 * LN2_LO!r}, {6.283185307179586 * 2.0 ** -53!r} /* fl(2 pi) 2^-53 */}};",
@@ -233,8 +234,9 @@ def write(rows) -> None:
              "__device__ const double kBmLogTab[129][4] = {"]
     for c, hi, lo in rows:
         lines.append(f"    {{{-2.0 * c!r}, {2.0 * hi!r}, {2.0 * lo!r}, 0.0}},")
-    lines += ["};", "", "// {sin(j pi/64), cos(j pi/64)}, j = 0..128, correctly rounded (exact 0 / +-1 at multiples of pi/2)",
-              "__device__ const double kBmSinCosTab[129][2] = {"]
+    lines += ["};", "", f"// {{sin(j 2pi/{NSC}), cos(j 2pi/{NSC})}}, j = 0..{NSC}, correctly rounded (exact 0 / +-1 at multiples of pi/2)",
+              f"constexpr int kBmSinCosN = {NSC};",
+              f"__device__ const double kBmSinCosTab[{NSC + 1}][2] = {{"]
     for sv, cv in SC_TAB:
         lines.append(f"    {{{sv!r}, {cv!r}}},")
     lines += ["};", "", "}  // namespace sk", ""]

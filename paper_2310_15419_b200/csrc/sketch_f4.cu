@@ -64,7 +64,10 @@ constexpr int kF4Ones = 64;
 #endif
 constexpr int kF4Sub = SK_F4_SUB;                 // K-steps (64 nonzeros each) per smem stage
 constexpr int kF4Stages = SK_F4_STAGES;
-constexpr int kF4JSlots = 12 / kF4Sub;            // nonzero-stream ring: one slot = one smem stage (kF4Sub K-steps)
+#ifndef SK_F4_JDEPTH
+#define SK_F4_JDEPTH 6                             // (2 slots: 7.23 ms; 3: 7.30, 4: 7.31, 1: 7.35 on c5)
+#endif
+constexpr int kF4JSlots = SK_F4_JDEPTH / kF4Sub;  // nonzero-stream ring: one slot = one smem stage (kF4Sub K-steps)
 constexpr int kF4ATile = 128 * 32;                // 128 rows x 64 fp4 = 4 KB
 constexpr int kF4BSub = SK_F4_B4 ? 1280 : 2560;   // B tile slot per K-step: row groups x 256 B (padded)
 constexpr int kF4ATileS = kF4Sub * kF4ATile;      // one tile's A data per stage

@@ -66,7 +66,10 @@ Schedule build_schedule(const int64_t* colptr, int64_t n, int64_t d, int rows_pe
   };
   int64_t base = 1;
   double best = 1e300;
+  // SKETCH_SCHED_WD (tuning only): force W_d for every column
+  static const int64_t force_wd = [] { const char* v = getenv("SKETCH_SCHED_WD"); return v ? atoll(v) : 0; }();
   for (int64_t WD = 1; WD <= std::min<int64_t>(16, n_rw); ++WD) {
+    if (force_wd > 0 && WD != std::min<int64_t>(force_wd, std::min<int64_t>(16, n_rw))) continue;
     const int64_t tiles = (n_rw + WD - 1) / WD;
     double tot = 0;
     for (int64_t k = 0; k < n; ++k) tot += (double)tiles * (double)cost_of(colptr[k + 1] - colptr[k], WD);
@@ -80,7 +83,7 @@ Schedule build_schedule(const int64_t* colptr, int64_t n, int64_t d, int rows_pe
   for (int64_t k = 0; k < n; ++k) {
     const int64_t L = colptr[k + 1] - colptr[k];
     int64_t WD = base;
-    if (WD > 1 && (double)cost_of(L, WD) > 0.25 * per_slot) WD = 1;
+    if (force_wd == 0 && WD > 1 && (double)cost_of(L, WD) > 0.25 * per_slot) WD = 1;
     const int64_t tiles = (n_rw + WD - 1) / WD;
     for (int64_t tt = 0; tt < tiles; ++tt) {
       Item it;

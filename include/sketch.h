@@ -29,10 +29,9 @@
  *  - Indices are 0-based.  colptr is int64[n+1] (colptr[0] = 0, non-decreasing,
  *    colptr[n] = nnz), rowidx is int32[nnz] with 0 <= rowidx < m.  Rows inside a column
  *    may be unsorted and may repeat; explicit zeros are processed (linearity).
- *  - Non-finite values: a NaN value makes every entry of its column NaN (as NaN * ±1 does).
- *    The SIMT kernels (fp32, uniform, Gaussian) follow IEEE arithmetic for +-Inf too; the
- *    exact ±1 fp64 tensor-core kernel (the default for SK_RADEMACHER + SK_F64) writes NaN to
- *    the whole column when it holds a NaN or an Inf (its digit encoding needs finite values).
+ *  - Non-finite values follow IEEE arithmetic on every path: a NaN value makes every entry of
+ *    its column NaN (as NaN * ±1 does); ±Inf values give ±Inf, or NaN where opposite infinities
+ *    meet in one sum.
  *  - Pointers are DEVICE pointers unless the name starts with h_ (host memory; pinned
  *    host memory is required for overlap but not for correctness).
  *  - out is d x n COLUMN-MAJOR with leading dimension d, and is OVERWRITTEN in full
@@ -82,8 +81,11 @@ typedef struct {
     int64_t plan_bytes;        /* device bytes the plan owns */
     int64_t n_items_jki;       /* work items of the Algorithm 4 (jki) path, 0 if not built */
     int64_t jki_nonzero_rows;  /* Σ over 16-column groups of the group's nonzero rows (its RNG work) */
-    int64_t n_items_f4_split;  /* fp4 tensor-core items that are halves of a last-wave item split along
-                                  K (0: no split; > 0: apply also launches a small zeroing kernel) */
+    int64_t n_items_f4_split;  /* tensor-core items that are parts of a K-split group (a column longer
+                                  than 131071 nonzeros, or a last-wave item halved along K) */
+    int64_t n_items_f4;        /* CTAs of the tensor-core kernel of one SK_RADEMACHER apply */
+    int64_t n_cols_f4;         /* columns on the tensor-core kernel (the others: n_items_rad SIMT CTAs) */
+    int64_t f4_split_groups;   /* K-split groups (int64 workspace slots of one apply) */
 } sk_stats_t;
 
 /*
@@ -164,39 +166,22 @@ const char* sketch_last_error_detail(void);
 const char* sketch_version(void);
 
 /*
- * Kernel selection for SK_RADEMACHER with SK_F64 values (process-wide).  All paths compute the
- * same Â within the parity bound (|Â - oracle| <= 1e-12 |S||A|); the tensor-core paths are
- * exact up to the per-column fixed-point rounding of the values (<= 2^-44 |S||A| for
- * SK_PATH_TC_FP4..HYBRID, <= 2^-42 |S||A| for SK_PATH_TC_FP4N) and a single final fp64 rounding.
- * Tensor-core paths need an average of >= 256 nonzeros per column and every column to hold
- * <= 131071 nonzeros (SK_PATH_TC_FP4N: <= 1048575), else the SIMT kernel runs.
- * Default: SK_PATH_TC_FP4, or the SKETCH_RAD_F64_PATH environment variable
- * (fp4 | fp4t | fp4n | int8smem | int8tmem | simt | hybrid).  SK_PATH_TC_FP4N also needs 16-byte aligned
- * rowidx / vals (TMA) and colptr[n] < 2^31 - 512.  Errors: SK_EINVAL for an unknown path.
+ * Kernel selection for SK_RADEMACHER with SK_F64 values (process-wide, read when a plan is built).
+ * Both compute the same Â within the parity bound |Â - oracle| <= 1e-12 |S||A|.
+ *  SK_PATH_TC_FP4 (default): the tcgen05 kind::mxf4 kernel (±1 as e2m1, values as 64 signed binary
+ *    digits of a per-column fixed-point scale; exact up to the value rounding <= L 2^-61 max|a| and one
+ *    final fp64 rounding) for every column with 256 .. 2^20 nonzeros -- columns longer than 131071
+ *    nonzeros split along K into parts that add exact int64 sums -- and the SIMT kernel for the other
+ *    columns of the same plan.  A column holding a NaN or an Inf gets the IEEE result (NaN, or the
+ *    common sign of its infinite terms), as the SIMT kernel and the oracle do.
+ *  SK_PATH_SIMT: the FP64 SIMT kernel (one SEL + one DADD per (row, nonzero)) for every column.
+ * Initialised from SKETCH_RAD_F64_PATH = fp4 | simt.  Errors: SK_EINVAL for an unknown path.
  */
 typedef enum {
-    SK_PATH_TC_FP4 = 0,        /* tcgen05 kind::mxf4: ±1 as e2m1, values as 64 signed binary digits */
-    SK_PATH_TC_INT8_SMEM = 1,  /* tcgen05 kind::i8: S tiles in smem (MN-major), 8 int8 digit planes */
-    SK_PATH_TC_INT8_TMEM = 2,  /* tcgen05 kind::i8: S tiles in TMEM (K-major) */
-    SK_PATH_SIMT = 3,          /* FP64 SIMT kernel: one SEL + one DADD per (row, nonzero) */
-    SK_PATH_HYBRID = 4,        /* one persistent kernel: int8 tensor-core warps + FP64 SIMT warps
-                                  pulling columns from one queue */
-    SK_PATH_TC_FP4N = 5,       /* tcgen05 kind::mxf4, S as the N = 256 operand, values as 63 magnitude
-                                  digits, TMA-fed persistent kernel */
-    SK_PATH_TC_FP4T = 6        /* tcgen05 kind::mxf4 with the S operand written to / read from TMEM */
+    SK_PATH_TC_FP4 = 0,
+    SK_PATH_SIMT = 3
 } sk_rad_f64_path_t;
 int sketch_set_rad_f64_path(int path);
-
-/*
- * Kernel selection for SK_RADEMACHER with SK_F32 values (process-wide; both compute Â in fp32
- * within the parity bound 2e-5 |S||A|).  SK_PATH32_SIMT (default): one predicated add per
- * (row, nonzero).  SK_PATH32_TABLE: per 4 nonzeros the CTA tabulates the 16 signed sums
- * ±a_1 ±a_2 ±a_3 ±a_4 and each row adds the one its 4 sign bits select (one table load + one add
- * per 4 entries; sums formed in nonzero order).  Initialised from SKETCH_RAD_F32_PATH = simt | tab.
- * Errors: SK_EINVAL for an unknown path.
- */
-typedef enum { SK_PATH32_SIMT = 1, SK_PATH32_TABLE = 0 } sk_rad_f32_path_t;
-int sketch_set_rad_f32_path(int path);
 
 /*
  * Kernel selection for SK_UNIFORM / SK_GAUSSIAN (process-wide): Algorithm 3 (kji: S[:, j] regenerated

@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsketch.so")
-SOURCES = ["sketch_kernels.cu", "sketch_tc.cu", "sketch_f4.cu", "sketch_f4t.cu", "sketch_f4n.cu", "sketch_hybrid.cu", "sketch_jki.cu", "sketch_tab.cu", "sketch_api.cu"]
+SOURCES = ["sketch_kernels.cu", "sketch_f4.cu", "sketch_jki.cu", "sketch_api.cu"]
 HEADERS = ["philox.cuh", "kernels.h", "bm_tables.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 # Per-file extra flags.  sketch_f4.cu (the c5 kernel): ptxas -O1 schedules its producer loop

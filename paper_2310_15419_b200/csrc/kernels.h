@@ -46,29 +46,32 @@ struct ApplyArgs {
   PhiloxKeys keys;
 };
 
-// Work item of the tensor-core ±1 kernel: column `col`, 128-row tiles [tile0, tile0 + ntiles).
-struct TcItem {
+// Work item of the tensor-core ±1 kernel (sketch_f4.cu): column `col`, 128-row tiles
+// [tile0, tile0 + ntiles), and K range = part `part` of `nparts` equal shares of the column's
+// 64-nonzero K-steps (nparts > 1: a column longer than kTcMaxColumn, or a last-wave item split
+// along K); the parts of one (col, tiles) add exact int64 sums into workspace slot `group`.
+struct F4Item {
   int32_t col;
   int32_t tile0;
-  int32_t ntiles;
-  int32_t pad;
+  int32_t meta;     // ntiles | part << 8 | nparts << 16
+  int32_t group;    // split group (workspace slot), -1 when nparts == 1
 };
+__host__ __device__ inline int f4_ntiles(const F4Item& it) { return it.meta & 0xFF; }
+__host__ __device__ inline int f4_part(const F4Item& it) { return (it.meta >> 8) & 0xFF; }
+__host__ __device__ inline int f4_nparts(const F4Item& it) { return (it.meta >> 16) & 0xFF; }
+__host__ __device__ inline int32_t f4_meta(int ntiles, int part, int nparts) { return ntiles | part << 8 | nparts << 16; }
 
-// Longest column the tensor-core path accepts (int32 accumulation bound, sketch_tc.cu).
+// Longest K range of one tensor-core item: the digit sums |D| <= L must stay exact in the f32
+// accumulator (L < 2^24), and the value rounding of a column, <= L 2^-61 max|a|, must stay far
+// below the fp64 parity bound 1e-12 |S||A| (2^20 2^-61 = 4.5e-13): parts of <= 131071 nonzeros,
+// columns of <= 2^20 (longer ones run on the SIMT kernel).
 constexpr int64_t kTcMaxColumn = 131071;
+constexpr int64_t kTcMaxColumnTotal = int64_t(1) << 20;
 
-// smem_staged = 1: S tiles staged in shared memory (variant 1); 0: staged in TMEM (variant 2).
-cudaError_t launch_apply_rad_tc(const ApplyArgs& a, const TcItem* items, int64_t n_items, int smem_staged,
+// n_groups: split groups of the schedule (their int64 workspace is allocated and zeroed
+// stream-ordered by the launcher).
+cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const F4Item* items, int64_t n_items, int64_t n_groups,
                                 cudaStream_t stream);
-int tc_tiles_per_cta();
-cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const TcItem* items, int64_t n_items, cudaStream_t stream);
-// Zeroes the output rows of K-split fp4 items (TcItem.pad: 0 whole column, 1 / 2 first / second half
-// of its K-steps; the halves atomically add into the zeroed rows).
-cudaError_t launch_f4_zero_split(const ApplyArgs& a, const TcItem* items, int64_t n_items, cudaStream_t stream);
-
-// ±1 x fp32 values through 4-nonzero subset-sum tables (sketch_tab.cu); items of <= 16 row tiles.
-int tab_tiles_per_cta();
-cudaError_t launch_apply_rad_tab(const ApplyArgs& a, const TcItem* items, int64_t n_items, cudaStream_t stream);
 int f4_tiles_per_cta();
 // Algorithm 4 (jki) path for uniform / Gaussian (sketch_jki.cu): column groups of kJCols columns,
 // each stored row by row (CSR of the group); items = (group, tile of jki_rows_per_item() rows).
@@ -89,29 +92,6 @@ struct JkiPlanView {
 };
 int jki_rows_per_item();
 cudaError_t launch_apply_jki(int dist, int dtype, const ApplyArgs& a, const JkiPlanView& J, cudaStream_t stream);
-
-// S-in-TMEM fp4 kernel (sketch_f4t.cu): items = (column, 512-row block `tile0` of Â), fp64 values.
-cudaError_t launch_apply_rad_f4t(const ApplyArgs& a, const TcItem* items, int64_t n_items, cudaStream_t stream);
-// S-as-N=256 fp4 kernel (sketch_f4n.cu): items = (column, 256-row tile), longest first; dtype 0 = f64,
-// 1 = f32; n_cols = columns of the plan (per-column value maxima are computed first).
-constexpr int64_t kF4nMaxColumn = (int64_t(1) << 20) - 1;
-constexpr int kF4nRows = 256;
-// Work item of the S-as-N fp4 kernel: column col (nonzeros [pb, pb + L)), 256-row tile `tile` of Â.
-struct NItem {
-  int64_t pb;
-  int32_t L;
-  int32_t col;
-  int32_t tile;
-  int32_t pad;
-};
-// rowidx and vals must be 16-byte aligned (TMA); nnz_end = colptr[n] (absolute end of the stream).
-bool f4n_aligned(const void* p);
-cudaError_t launch_apply_rad_f4n(const ApplyArgs& a, int dtype, const NItem* items, int64_t n_items, int64_t n_cols,
-                                 int64_t nnz_end, cudaStream_t stream);
-// Tensor cores + FP64 SIMT in one persistent kernel; items = int8 schedule (<= 16 tiles each);
-// counter = one device int (work queue head), reset by the launcher.
-cudaError_t launch_apply_rad_hybrid(const ApplyArgs& a, const TcItem* items, int64_t n_items, int* counter,
-                                    cudaStream_t stream);
 
 // dist: 0 = Rademacher, 1 = uniform, 2 = Gaussian; dtype: 0 = f64, 1 = f32.
 cudaError_t launch_apply(int dist, int dtype, const ApplyArgs& a, cudaStream_t stream);

@@ -73,21 +73,6 @@ __device__ __forceinline__ double uniform53(uint32_t xa, uint32_t xb) {
   return fma(__ull2double_rn(k), 0x1p-52, __longlong_as_double((long long)0xBFEFFFFFFFFFFFFFull));
 }
 
-// The same value without an int->double conversion (exponent-OR construction), kept for
-// reference: with b = bit 52 of k and r = k mod 2^52, |S| = r'·2^-52 + 2^-53 where
-// r' = b ? r : (2^52 - 1 - r); M = 1 + r'·2^-52 is built from bits and |S| = M - (1 - 2^-53)
-// exactly (Sterbenz).  S = b ? |S| : -|S|.
-__device__ __forceinline__ double uniform53_bits(uint32_t xa, uint32_t xb) {
-  const uint32_t lo = __funnelshift_r(xb, xa, 11);          // bits 31..0 of k
-  const uint32_t hi = xa >> 11;                             // bits 52..32 of k
-  const uint32_t nb = ~(uint32_t)((int32_t)xa >> 31);       // all ones iff b == 0
-  const uint32_t mlo = lo ^ nb;
-  const uint32_t mhi = ((hi ^ nb) & 0x000FFFFFu) | 0x3FF00000u;
-  const double M = __hiloint2double((int)mhi, (int)mlo);
-  const double mag = __dsub_rn(M, __longlong_as_double(0x3FEFFFFFFFFFFFFFll));  // M - (1 - 2^-53)
-  return __hiloint2double(__double2hiint(mag) ^ (int)(nb & 0x80000000u), __double2loint(mag));
-}
-
 // Uniform24: S = (2k + 1 - 2^24) 2^-24 with k = the top 24 bits of one
 // Philox word (4 entries per block).  An odd multiple of 2^-24 below 1 in magnitude: exact in fp32
 // (and fp64); I2F of the exact odd integer and one exact scaling.
@@ -96,54 +81,53 @@ __device__ __forceinline__ float uniform24(uint32_t w) {
   return __int2float_rn(odd) * 0x1p-24f;
 }
 
-// 2*pi rounded to the nearest double, 0x1.921fb54442d18p+2.
-__device__ __forceinline__ double two_pi_f64() { return __longlong_as_double(0x401921FB54442D18ll); }
 
-// Box-Muller pair from one block: u1 = (k1 + 1) 2^-53 in (0, 1], u2 = k2 2^-53 in [0, 1),
-// rho = sqrt(-2 ln u1), th = u2 * fl(2 pi); (g0, g1) = (rho cos th, rho sin th).
-// Full-precision libdevice log / sincos (no fast-math); single IEEE ops elsewhere.
-__device__ __forceinline__ void gaussian_pair(const uint4 x, double& g0, double& g1) {
-  const unsigned long long k1 = (((unsigned long long)x.x << 32) | x.y) >> 11;
-  const unsigned long long k2 = (((unsigned long long)x.z << 32) | x.w) >> 11;
-  const double u1 = __dmul_rn(__ull2double_rn(k1 + 1ull), 0x1p-53);
-  const double u2 = __dmul_rn(__ull2double_rn(k2), 0x1p-53);
-  const double rho = __dsqrt_rn(__dmul_rn(-2.0, log(u1)));
-  const double th = __dmul_rn(u2, two_pi_f64());
-  double s, c;
-  sincos(th, &s, &c);
-  g0 = __dmul_rn(rho, c);
-  g1 = __dmul_rn(rho, s);
-}
-
-// ---------------------------------------------------------------- fast Box-Muller (same definition)
+// ---------------------------------------------------------------- Box-Muller (fast fp64)
 //
-// The transform of gaussian_pair with its own log and sincos (scripts/gen_bm_tables.py derives and
-// checks the constants against 300-bit mpmath: <= 0.6 ulp each); ~45 FP64 operations per pair
-// instead of the libdevice calls.  Results agree with the libm-based oracle far inside the
-// Gaussian parity bound (1e-14 relative).
+// Box-Muller pair from one block (include/sketch.h, R4): u1 = (k1 + 1) 2^-53 in (0, 1],
+// u2 = k2 2^-53 in [0, 1), rho = sqrt(-2 ln u1), th = u2 * fl(2 pi); (g0, g1) = (rho cos th, rho sin th),
+// with the library's own log and sincos (scripts/gen_bm_tables.py derives and checks the constants
+// against 300-bit mpmath: <= 0.6 ulp each; ~40 FP64 operations per pair).  Results agree with the
+// libm-based oracle far inside the Gaussian parity bound (1e-14 relative).
+
+// The -2 log table in shared memory, replicated: copy c of row i, component t lives at
+// [(3 i + t) kLogRep + c], and lane l reads copy l mod kLogRep.  A half-warp's 16 lanes then read
+// 16 different copies of any row mix -- 16 consecutive doubles, one per bank pair -- so the random
+// row gather of Box-Muller is free of bank conflicts (the unreplicated table put every row on one
+// of 4 bank groups: ~8-way conflicts).
+constexpr int kLogRep = 16;
+constexpr int kLogTabRepBytes = kBmLogRows * 3 * kLogRep * 8;   // 49.5 KB
+
+__device__ __forceinline__ void bm_fill_logtab(double* smem_tab) {
+  for (int i = threadIdx.x; i < kBmLogRows * 3 * kLogRep; i += blockDim.x)
+    smem_tab[i] = (&kBmLogTab[0][0])[i / kLogRep];
+}
 
 // -2 log(u1) for u1 = U 2^-53, U = k1 + 1 an integer in [1, 2^53] passed as an exact double (so
 // u1's scaling costs no multiply: exponent bias 53).  u = 2^e m, idx = round(128 (m - 1)), and with
-// the table rows {-2 c, 2 log(c)_hi, 2 log(c)_lo, pad}: s = fma(m, -2c, 2) = -2 (m c - 1) exactly
+// the table rows {-2 c, 2 log(c)_hi, 2 log(c)_lo}: s = fma(m, -2c, 2) = -2 (m c - 1) exactly
 // (|s| < 0.009), -2 log u = (e (-2 ln2_hi) + 2 L_hi) + (s + s^2 Q(s) + (e (-2 ln2_lo) + 2 L_lo)),
 // Q(s) = 1/4 + s/12 + s^2/32 + s^3/80 + s^4/192 (= -P(-s/2)/2 for the Taylor P of
 // (log1p(r) - r) / r^2, truncated where the next term is below 2^-60), the first bracket exact
 // (2^-42 grid).  The factor -2 of Box-Muller is folded into the constants: 11 FP64 operations.
+// tab = row 0, component 0 of this lane's copy; STRIDE = distance between consecutive components
+// (kLogRep for the replicated shared-memory table, 1 for kBmLogTab itself).
+template <int STRIDE>
 __device__ __forceinline__ double bm_m2log_u53(double U, const double* __restrict__ tab) {
   const unsigned long long b = (unsigned long long)__double_as_longlong(U);
   const int e = (int)(b >> 52) - (1023 + 53);
   const double m = __longlong_as_double((long long)((b & 0x000FFFFFFFFFFFFFull) | 0x3FF0000000000000ull));
   const int idx = (int)(((b >> 44) & 0xFFu) + 1u) >> 1;        // round(128 (m - 1)), 0..128
-  const double2 ch = *reinterpret_cast<const double2*>(tab + 4 * idx);
-  const double lo = tab[4 * idx + 2];
-  const double s = fma(m, ch.x, 2.0);                          // -2 r, |r| < 0.0045
+  const double* row = tab + 3 * STRIDE * idx;
+  const double c2 = row[0], hi = row[STRIDE], lo = row[2 * STRIDE];
+  const double s = fma(m, c2, 2.0);                            // -2 r, |r| < 0.0045
   const double s2 = s * s;
   double q = fma(s, kBm[kQ4], kBm[kQ3]);                       // (the s^5/448 term is below 2^-60)
   q = fma(s, q, kBm[kQ2]);
   q = fma(s, q, kBm[kQ1]);
   q = fma(s, q, kBm[kQ0]);
   const double ed = (double)e;
-  const double shi = fma(ed, kBm[kM2Ln2Hi], ch.y);             // exact: both on the 2^-42 grid
+  const double shi = fma(ed, kBm[kM2Ln2Hi], hi);               // exact: both on the 2^-42 grid
   const double slo = fma(ed, kBm[kM2Ln2Lo], lo);
   return shi + (s + fma(s2, q, slo));
 }
@@ -169,40 +153,6 @@ __device__ __forceinline__ void bm_sincos(double th, double& s, double& c) {
   c = fma(t.y, cr, -(t.x * sr));
 }
 
-// The quadrant form (previous version, kept for reference): Cody-Waite reduction by pi/2 in four
-// parts (exact products for k <= 4), fdlibm kernels on |r| <= pi/4, quadrant by k mod 4 (signs
-// applied as bit flips).
-__device__ __forceinline__ void bm_sincos_quadrant(double th, double& s, double& c) {
-  const double kr = fma(th, kBm[kTwoOverPi], kBm[kRound]);   // 1.5 2^52 + rint(th 2/pi)
-  const double kd = kr - kBm[kRound];
-  double r = fma(-kd, kBm[kPio2_0], th);
-  r = fma(-kd, kBm[kPio2_1], r);
-  r = fma(-kd, kBm[kPio2_2], r);
-  r = fma(-kd, kBm[kPio2_3], r);
-  // fdlibm kernels, polynomials in z = r^2 (Horner; Estrin measured slower)
-  const double z = r * r;
-  double ps = fma(z, kBm[kS6], kBm[kS5]);
-  ps = fma(z, ps, kBm[kS4]);
-  ps = fma(z, ps, kBm[kS3]);
-  ps = fma(z, ps, kBm[kS2]);
-  ps = fma(z, ps, kBm[kS1]);
-  const double sr = fma(z * r, ps, r);
-  double pc = fma(z, kBm[kC6], kBm[kC5]);
-  pc = fma(z, pc, kBm[kC4]);
-  pc = fma(z, pc, kBm[kC3]);
-  pc = fma(z, pc, kBm[kC2]);
-  pc = fma(z, pc, kBm[kC1]);
-  const double hz = 0.5 * z;
-  const double w = 1.0 - hz;
-  const double cr = w + (((1.0 - w) - hz) + z * (z * pc));
-  const int q = __double2loint(kr) & 3;                        // k mod 4 from the low mantissa bits
-  const bool odd = q & 1;
-  const double a = odd ? cr : sr, bq = odd ? sr : cr;          // sin, cos before signs
-  const int sa = (q & 2) << 30, sb = ((q + 1) & 2) << 30;      // sign bits (0x80000000 or 0)
-  s = __hiloint2double(__double2hiint(a) ^ sa, __double2loint(a));
-  c = __hiloint2double(__double2hiint(bq) ^ sb, __double2loint(bq));
-}
-
 // sqrt(x) for x in [0, 75] to ~1 ulp: rsqrt approximation refined by one Goldschmidt step and one
 // Newton correction (x = -0 or +0 returns x, like sqrt).
 __device__ __forceinline__ double bm_sqrt(double x) {
@@ -217,13 +167,14 @@ __device__ __forceinline__ double bm_sqrt(double x) {
   return x == 0.0 ? x : s;
 }
 
-// Same values as gaussian_pair (to within the parity bound) from the same block.
+// The Box-Muller pair of block x; tab / STRIDE as for bm_m2log_u53.
+template <int STRIDE>
 __device__ __forceinline__ void gaussian_pair_fast(const uint4 x, const double* __restrict__ tab, double& g0, double& g1) {
   const unsigned long long k1 = (((unsigned long long)x.x << 32) | x.y) >> 11;
   const unsigned long long k2 = (((unsigned long long)x.z << 32) | x.w) >> 11;
   // u1 = (k1 + 1) 2^-53 and u2 = k2 2^-53 are never formed: -2 log u1 takes the integer with an
   // exponent bias, and th = u2 fl(2 pi) = k2 (2^-53 fl(2 pi)) is the same single rounding.
-  const double rho = bm_sqrt(bm_m2log_u53(__ull2double_rn(k1 + 1ull), tab));
+  const double rho = bm_sqrt(bm_m2log_u53<STRIDE>(__ull2double_rn(k1 + 1ull), tab));
   const double th = __dmul_rn(__ull2double_rn(k2), kBm[kTwoPi53]);
   double s, c;
   bm_sincos(th, s, c);

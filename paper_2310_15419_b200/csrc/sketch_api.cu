@@ -52,10 +52,13 @@ struct Schedule {
   int64_t philox_blocks = 0;
 };
 
-// colptr: n+1 absolute offsets (colptr[0] may be nonzero for column sub-ranges).
+// Schedule of the SIMT kernels over the columns `cols` (all n when null).  colptr: n+1 absolute
+// offsets (colptr[0] may be nonzero for column sub-ranges).
 Schedule build_schedule(const int64_t* colptr, int64_t n, int64_t d, int rows_per_warp,
-                        int blocks_per_nnz_per_warp) {
+                        int blocks_per_nnz_per_warp, const std::vector<int32_t>* cols = nullptr) {
   Schedule S;
+  const int64_t nc = cols ? (int64_t)cols->size() : n;
+  auto col_at = [&](int64_t i) -> int64_t { return cols ? (*cols)[(size_t)i] : i; };
   const int64_t n_rw = (d + rows_per_warp - 1) / rows_per_warp;  // row-warps covering d
   // Cost of one CTA (warps run in parallel): its per-warp nonzero slice plus a fixed overhead
   // (prologue, reduction, store) of about 30 nonzero-equivalents.  W_d (row-warps per CTA,
@@ -72,7 +75,10 @@ Schedule build_schedule(const int64_t* colptr, int64_t n, int64_t d, int rows_pe
     if (force_wd > 0 && WD != std::min<int64_t>(force_wd, std::min<int64_t>(16, n_rw))) continue;
     const int64_t tiles = (n_rw + WD - 1) / WD;
     double tot = 0;
-    for (int64_t k = 0; k < n; ++k) tot += (double)tiles * (double)cost_of(colptr[k + 1] - colptr[k], WD);
+    for (int64_t i = 0; i < nc; ++i) {
+      const int64_t k = col_at(i);
+      tot += (double)tiles * (double)cost_of(colptr[k + 1] - colptr[k], WD);
+    }
     if (tot < best * 0.999) { best = tot; base = WD; }
   }
   // Average load per SM slot with the base shape; a column whose CTAs would each exceed a
@@ -80,7 +86,8 @@ Schedule build_schedule(const int64_t* colptr, int64_t n, int64_t d, int rows_pe
   // CTAs do not set the makespan (column-length skew, e.g. power-law columns).
   const double per_slot = best / kSMs;
   std::vector<std::pair<int64_t, Item>> tmp;
-  for (int64_t k = 0; k < n; ++k) {
+  for (int64_t i = 0; i < nc; ++i) {
+    const int64_t k = col_at(i);
     const int64_t L = colptr[k + 1] - colptr[k];
     int64_t WD = base;
     if (force_wd == 0 && WD > 1 && (double)cost_of(L, WD) > 0.25 * per_slot) WD = 1;
@@ -104,83 +111,64 @@ Schedule build_schedule(const int64_t* colptr, int64_t n, int64_t d, int rows_pe
   return S;
 }
 
-// Tensor-core schedule: per column, ceil(d/128) row tiles in groups of <= 16 per CTA,
-// longest columns first.
-std::vector<sk::TcItem> build_tc_schedule(const int64_t* colptr, int64_t n, int64_t d, int64_t per) {
+// Tensor-core schedule over the columns `cols`: per column, ceil(d/128) row tiles in groups of
+// <= `per` per CTA; a column longer than kTcMaxColumn is split along K into
+// ceil(L / kTcMaxColumn) parts (one split group per tile group).  Longest items first.
+struct F4Schedule {
+  std::vector<sk::F4Item> items;
+  int64_t groups = 0;         // split groups (workspace slots)
+  int64_t split_items = 0;    // items with nparts > 1
+};
+
+F4Schedule build_f4_schedule(const int64_t* colptr, int64_t d, int64_t per, const std::vector<int32_t>& cols) {
+  F4Schedule F;
   const int64_t tiles = (d + 127) / 128;
-  const int64_t groups = (tiles + per - 1) / per;
-  const int64_t tpg = (tiles + groups - 1) / groups;
-  std::vector<std::pair<int64_t, sk::TcItem>> tmp;
-  for (int64_t k = 0; k < n; ++k) {
+  const int64_t tgroups = (tiles + per - 1) / per;
+  const int64_t tpg = (tiles + tgroups - 1) / tgroups;
+  std::vector<std::pair<int64_t, sk::F4Item>> tmp;
+  for (int32_t k : cols) {
     const int64_t L = colptr[k + 1] - colptr[k];
+    const int64_t P = std::max<int64_t>(1, (L + sk::kTcMaxColumn - 1) / sk::kTcMaxColumn);
     for (int64_t g = 0; g * tpg < tiles; ++g) {
-      sk::TcItem it;
-      it.col = (int32_t)k;
-      it.tile0 = (int32_t)(g * tpg);
-      it.ntiles = (int32_t)std::min(tpg, tiles - g * tpg);
-      it.pad = 0;
-      tmp.emplace_back(L, it);
+      const int64_t grp = P > 1 ? F.groups++ : -1;
+      for (int64_t pt = 0; pt < P; ++pt) {
+        sk::F4Item it;
+        it.col = k;
+        it.tile0 = (int32_t)(g * tpg);
+        it.meta = sk::f4_meta((int)std::min(tpg, tiles - g * tpg), (int)pt, (int)P);
+        it.group = (int32_t)grp;
+        tmp.emplace_back(L / P, it);
+        if (P > 1) ++F.split_items;
+      }
     }
   }
-  std::stable_sort(tmp.begin(), tmp.end(), [](const std::pair<int64_t, sk::TcItem>& a,
-                                              const std::pair<int64_t, sk::TcItem>& b) { return a.first > b.first; });
-  std::vector<sk::TcItem> out;
-  out.reserve(tmp.size());
-  for (auto& pr : tmp) out.push_back(pr.second);
-  return out;
+  std::stable_sort(tmp.begin(), tmp.end(), [](const std::pair<int64_t, sk::F4Item>& a,
+                                              const std::pair<int64_t, sk::F4Item>& b) { return a.first > b.first; });
+  F.items.reserve(tmp.size());
+  for (auto& pr : tmp) F.items.push_back(pr.second);
+  return F;
 }
 
-// S-as-N fp4 schedule: one item per (column, 256-row tile of Â), longest columns first.
-std::vector<sk::NItem> build_f4n_schedule(const int64_t* colptr, int64_t n, int64_t d) {
-  const int64_t tiles = (d + sk::kF4nRows - 1) / sk::kF4nRows;
-  std::vector<sk::NItem> out;
-  out.reserve((size_t)(n * tiles));
-  for (int64_t k = 0; k < n; ++k)
-    for (int64_t g = 0; g < tiles; ++g) {
-      sk::NItem it;
-      it.pb = colptr[k];
-      it.L = (int32_t)(colptr[k + 1] - colptr[k]);
-      it.col = (int32_t)k;
-      it.tile = (int32_t)g;
-      it.pad = 0;
-      out.push_back(it);
-    }
-  std::stable_sort(out.begin(), out.end(), [](const sk::NItem& a, const sk::NItem& b) { return a.L > b.L; });
-  return out;
-}
-
-// Kernel used for ±1 with fp64 values (process-wide; results agree within the parity bound):
-// SK_PATH_TC_FP4 (default), SK_PATH_TC_FP4N, SK_PATH_TC_INT8_SMEM, SK_PATH_TC_INT8_TMEM,
-// SK_PATH_SIMT, SK_PATH_HYBRID.  Initialised from SKETCH_RAD_F64_PATH = fp4 | fp4n | int8smem |
-// int8tmem | simt | hybrid, else fp4.
+// Kernel used for ±1 with fp64 values (process-wide, read when a plan is built; results agree
+// within the parity bound): SK_PATH_TC_FP4 (default: the tensor-core kernel for every column with
+// at least kF4MinColumn nonzeros, the SIMT kernel for the rest) or SK_PATH_SIMT (the SIMT kernel
+// for every column).  Initialised from SKETCH_RAD_F64_PATH = fp4 | simt, else fp4.
 std::atomic<int> g_rad_f64_path{-1};
-// ±1 with fp32 values: SK_PATH32_SIMT (default; c4 1.49 ms) or SK_PATH32_TABLE (2.09 ms: more
-// instructions per entry than the predicated adds); SKETCH_RAD_F32_PATH = simt | tab.
-std::atomic<int> g_rad_f32_path{-1};
-
-int rad_f32_path() {
-  int v = g_rad_f32_path.load(std::memory_order_relaxed);
-  if (v >= 0) return v;
-  v = SK_PATH32_SIMT;
-  if (const char* e = getenv("SKETCH_RAD_F32_PATH"))
-    if (!strcmp(e, "tab")) v = SK_PATH32_TABLE;
-  g_rad_f32_path.store(v, std::memory_order_relaxed);
-  return v;
-}
 
 int rad_f64_path() {
   int v = g_rad_f64_path.load(std::memory_order_relaxed);
   if (v >= 0) return v;
   v = SK_PATH_TC_FP4;
-  if (const char* e = getenv("SKETCH_RAD_F64_PATH")) {
-    if (!strcmp(e, "fp4n")) v = SK_PATH_TC_FP4N;
-    else if (!strcmp(e, "fp4t")) v = SK_PATH_TC_FP4T;
-    else if (!strcmp(e, "hybrid")) v = SK_PATH_HYBRID;
-    else if (!strcmp(e, "int8smem")) v = SK_PATH_TC_INT8_SMEM;
-    else if (!strcmp(e, "int8tmem")) v = SK_PATH_TC_INT8_TMEM;
-    else if (!strcmp(e, "simt")) v = SK_PATH_SIMT;
-  }
+  if (const char* e = getenv("SKETCH_RAD_F64_PATH"))
+    if (!strcmp(e, "simt")) v = SK_PATH_SIMT;
   g_rad_f64_path.store(v, std::memory_order_relaxed);
+  return v;
+}
+
+// Shortest column the tensor-core kernel takes (shorter ones go to the SIMT kernel, whose CTA has
+// no TMEM / barrier / pipeline fill and drain to amortise).  SKETCH_F4_MIN_COL (tuning only).
+int64_t f4_min_column() {
+  static const int64_t v = [] { const char* e = getenv("SKETCH_F4_MIN_COL"); return e ? std::max<int64_t>(1, atoll(e)) : 256; }();
   return v;
 }
 
@@ -209,29 +197,21 @@ struct sk_plan_s {
   int64_t d, m, n, nnz, row_offset, max_col;
   const int64_t* colptr;   // device (caller-owned)
   const int32_t* rowidx;   // device (caller-owned)
-  Item* d_items = nullptr; // [rad items | pair items | Gaussian items]
-  sk::TcItem* d_tc = nullptr;       // tensor-core ±1 fp64 schedules (empty if not eligible):
-  int64_t n_tc = 0;                 //   [int8 items (16 tiles) | fp4 items (6 tiles)]
+  Item* d_items = nullptr; // [rad items | pair items | Gaussian items] (SIMT kernels)
+  sk::F4Item* d_f4 = nullptr;       // tensor-core ±1 fp64 schedule (empty unless dtype F64 and path FP4)
   int64_t n_f4 = 0;
-  int64_t f4_tail_first = 0;        // fp4 items [f4_tail_first, n_f4): the last wave, split along K
-  int64_t f4_tail_n = 0;            //   (0 if not split)
-  int64_t f4_split_items = 0;       // half items among them
-  sk::TcItem* d_f4t = nullptr;      // S-in-TMEM fp4 schedule: (column, 512-row block), longest first
-  int64_t n_f4t = 0;
-  sk::NItem* d_f4n = nullptr;       // S-as-N fp4 schedule: (column, 256-row tile), longest first
-  sk::TcItem* d_tab = nullptr;      // ±1 fp32 subset-sum-table schedule: (column, <= 16 row tiles)
-  int64_t n_tab = 0;
-  int64_t n_f4n = 0;
-  int64_t nnz_end = 0;              // colptr[n] (absolute end of the nonzero stream)
+  int64_t f4_groups = 0;            // split groups (long columns and the K-split last wave)
+  int64_t f4_split_items = 0;       // items that are parts of a split group
+  int64_t f4_cols = 0;              // columns on the tensor-core kernel (the rest: SIMT items)
   // Algorithm 4 (jki) structure: one device block holding items, grp_rows, row_j, row_ent, ent, ent_base
   void* d_jki = nullptr;
   sk::JkiPlanView jki{};
   int64_t jki_rows = 0;             // Σ_groups nonzero rows
   int64_t* owned_colptr = nullptr;  // device copy made by sketch_plan_host
-  // All schedules (items, tc / f4, f4t, f4n) live in ONE device block uploaded by one copy.
+  // All schedules live in ONE device block uploaded by one copy.
   void* d_stage = nullptr;
   std::vector<unsigned char> h_stage;   // host image of d_stage (kept until uploaded)
-  size_t off_items = 0, off_tc = 0, off_f4t = 0, off_f4n = 0, off_tab = 0;
+  size_t off_items = 0, off_f4 = 0;
   int64_t n_rad = 0, n_pair = 0, n_gauss = 0;
   int64_t philox_rad = 0, philox_pair = 0;
 };
@@ -250,6 +230,15 @@ int build_jki(sk_plan_s* p, const int64_t* h_colptr, bool force, cudaStream_t st
     const int64_t c0 = g * sk::kJCols, c1 = std::min<int64_t>(n, c0 + sk::kJCols);
     return std::make_pair(h_colptr[c0] - base, h_colptr[c1] - base);
   };
+  // An entry packs (value index within its group) << 4 | column within the group into 32 bits.
+  for (int64_t g = 0; g < G; ++g) {
+    const auto pr = group_range(g);
+    if (pr.second - pr.first >= (int64_t(1) << 28)) {
+      if (!force) return SK_OK;
+      g_detail = "jki: a 16-column group holds >= 2^28 nonzeros";
+      return SK_EUNSUPPORTED;
+    }
+  }
   auto distinct_rows = [](std::vector<int32_t>& r) {
     std::sort(r.begin(), r.end());
     return (int64_t)(std::unique(r.begin(), r.end()) - r.begin());
@@ -384,33 +373,31 @@ int validate_colptr(const int64_t* h, int64_t n, int64_t nnz, bool require_zero_
 
 // Last-wave split of the fp4 schedule.  Items cost about the same and the hardware hands them to
 // SMs in order, so N items on W SMs take ceil(N / W) item-times; when the last wave is less than
-// half full (0 < N mod W < W/2), splitting the last W + N mod W items into two halves along K
-// (same rows, half the nonzeros each) turns the final 2 item-times into 1.5.  The halves add into
-// Â with one fp64 atomicAdd each onto zeroed rows: 0 + a + b rounds identically in either order,
-// so results stay deterministic.  SKETCH_F4_SPLIT=0 disables it.
-void split_f4_tail(sk_plan_s* p, std::vector<sk::TcItem>& f4, const int64_t* h_colptr) {
+// half full (0 < N mod W < W/2), splitting the last W + N mod W whole items into two halves along K
+// (same rows, half the K-steps each) turns the final 2 item-times into 1.5.  The halves add exact
+// int64 digit sums into a workspace slot (deterministic in any order); the second to finish writes
+// Â.  SKETCH_F4_SPLIT=0 disables it.
+void split_f4_tail(F4Schedule& F, const int64_t* h_colptr) {
   static const bool off = [] { const char* v = getenv("SKETCH_F4_SPLIT"); return v && !strcmp(v, "0"); }();
-  int W = 148, dev = 0;
+  int W = kSMs, dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&W, cudaDevAttrMultiProcessorCount, dev);
+  std::vector<sk::F4Item>& f4 = F.items;
   const int64_t N = (int64_t)f4.size(), r = W > 0 ? N % W : 0;
   if (off || W <= 0 || N <= W || r == 0 || 2 * r >= W) return;
   const int64_t first = N - W - r;
-  std::vector<sk::TcItem> out(f4.begin(), f4.begin() + first);
-  int64_t halves = 0;
+  std::vector<sk::F4Item> out(f4.begin(), f4.begin() + first);
   for (int64_t i = first; i < N; ++i) {
-    sk::TcItem it = f4[(size_t)i];
-    if (h_colptr[it.col + 1] - h_colptr[it.col] >= 128) {   // at least two K-steps
-      it.pad = 1; out.push_back(it);
-      it.pad = 2; out.push_back(it);
-      halves += 2;
+    sk::F4Item it = f4[(size_t)i];
+    if (sk::f4_nparts(it) == 1 && h_colptr[it.col + 1] - h_colptr[it.col] >= 128) {   // >= two K-steps
+      const int nt = sk::f4_ntiles(it);
+      it.group = (int32_t)F.groups++;
+      it.meta = sk::f4_meta(nt, 0, 2); out.push_back(it);
+      it.meta = sk::f4_meta(nt, 1, 2); out.push_back(it);
+      F.split_items += 2;
     } else {
       out.push_back(it);
     }
   }
-  if (halves == 0) return;
-  p->f4_tail_first = first;
-  p->f4_tail_n = (int64_t)out.size() - first;
-  p->f4_split_items = halves;
   f4.swap(out);
 }
 
@@ -442,7 +429,25 @@ int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
       fprintf(stderr, "  make_plan %s: %.3f ms\n", what,
               std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tm0).count());
   };
-  Schedule rad = build_schedule(h_colptr, n, d, sk::kRowsPerWarpRad, sk::kRowsPerWarpRad / 128);
+  // ±1 x fp64: columns with kF4MinColumn .. kTcMaxColumnTotal nonzeros run on the tensor cores,
+  // the others on the SIMT kernel (per column, not per matrix).
+  F4Schedule f4;
+  std::vector<int32_t> simt_cols;
+  const bool use_f4 = dtype == SK_F64 && rad_f64_path() == SK_PATH_TC_FP4;
+  if (use_f4) {
+    std::vector<int32_t> tc_cols;
+    for (int64_t k = 0; k < n; ++k) {
+      const int64_t L = h_colptr[k + 1] - h_colptr[k];
+      (L >= f4_min_column() && L <= sk::kTcMaxColumnTotal ? tc_cols : simt_cols).push_back((int32_t)k);
+    }
+    if (!tc_cols.empty()) {
+      f4 = build_f4_schedule(h_colptr, d, sk::f4_tiles_per_cta(), tc_cols);
+      split_f4_tail(f4, h_colptr);
+    }
+    p->f4_cols = (int64_t)tc_cols.size();
+  }
+  Schedule rad = build_schedule(h_colptr, n, d, sk::kRowsPerWarpRad, sk::kRowsPerWarpRad / 128,
+                                use_f4 ? &simt_cols : nullptr);
   Schedule pair = build_schedule(h_colptr, n, d, sk::kRowsPerWarpPair, sk::kRowsPerWarpPair / 2);
   Schedule gauss = build_schedule(h_colptr, n, d, sk::kRowsPerWarpGauss, sk::kRowsPerWarpGauss / 2);
   p->n_rad = (int64_t)rad.items.size();
@@ -450,43 +455,17 @@ int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
   p->n_gauss = (int64_t)gauss.items.size();
   p->philox_rad = rad.philox_blocks;
   p->philox_pair = pair.philox_blocks;
-  // Tensor-core ±1 paths: every column within the exact-accumulation bound, and columns long
-  // enough on average (>= 256 nonzeros) to amortise a CTA's TMEM / barrier / scale prologue.
-  const bool tc_ok = dtype == SK_F64 && p->max_col <= sk::kTcMaxColumn && n > 0 && nnz >= 256 * n;
-  std::vector<sk::TcItem> tc, f4t, tab;
-  if (dtype == SK_F32 && n > 0) {
-    tab = build_tc_schedule(h_colptr, n, d, sk::tab_tiles_per_cta());
-    p->n_tab = (int64_t)tab.size();
-  }
-  std::vector<sk::NItem> f4n;
-  if (tc_ok) {
-    tc = build_tc_schedule(h_colptr, n, d, sk::tc_tiles_per_cta());
-    std::vector<sk::TcItem> f4 = build_tc_schedule(h_colptr, n, d, sk::f4_tiles_per_cta());
-    split_f4_tail(p, f4, h_colptr);
-    p->n_tc = (int64_t)tc.size();
-    p->n_f4 = (int64_t)f4.size();
-    tc.insert(tc.end(), f4.begin(), f4.end());
-    f4t = build_tc_schedule(h_colptr, n, (d + 3) / 4, 1);   // 512-row blocks
-    p->n_f4t = (int64_t)f4t.size();
-  }
-  lap("rad/pair/gauss/tc schedules");
-  p->nnz_end = h_colptr[n];
-  // S-as-N fp4 path: TMA streams rowidx / values (16-byte aligned arrays, int32 coordinates)
-  if (dtype == SK_F64 && p->max_col <= sk::kF4nMaxColumn && n > 0 && nnz >= 256 * n && sk::f4n_aligned(rowidx) &&
-      p->nnz_end < (int64_t(1) << 31) - 2 * sk::kF4nRows) {
-    f4n = build_f4n_schedule(h_colptr, n, d);
-    p->n_f4n = (int64_t)f4n.size();
-  }
+  p->n_f4 = (int64_t)f4.items.size();
+  p->f4_groups = f4.groups;
+  p->f4_split_items = f4.split_items;
+  lap("schedules");
   // one host image of every schedule, 256-byte aligned sections
   {
     const int64_t total = p->n_rad + p->n_pair + p->n_gauss;
     auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
     p->off_items = 0;
-    p->off_tc = up(p->off_items + (size_t)total * sizeof(Item));
-    p->off_f4t = up(p->off_tc + tc.size() * sizeof(sk::TcItem));
-    p->off_f4n = up(p->off_f4t + f4t.size() * sizeof(sk::TcItem));
-    p->off_tab = up(p->off_f4n + f4n.size() * sizeof(sk::NItem));
-    const size_t bytes = up(p->off_tab + tab.size() * sizeof(sk::TcItem));
+    p->off_f4 = up(p->off_items + (size_t)total * sizeof(Item));
+    const size_t bytes = up(p->off_f4 + f4.items.size() * sizeof(sk::F4Item));
     p->h_stage.assign(bytes, 0);
     unsigned char* h = p->h_stage.data();
     size_t o = p->off_items;
@@ -494,21 +473,15 @@ int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
       if (!sc->items.empty()) std::memcpy(h + o, sc->items.data(), sc->items.size() * sizeof(Item));
       o += sc->items.size() * sizeof(Item);
     }
-    if (!tc.empty()) std::memcpy(h + p->off_tc, tc.data(), tc.size() * sizeof(sk::TcItem));
-    if (!f4t.empty()) std::memcpy(h + p->off_f4t, f4t.data(), f4t.size() * sizeof(sk::TcItem));
-    if (!f4n.empty()) std::memcpy(h + p->off_f4n, f4n.data(), f4n.size() * sizeof(sk::NItem));
-    if (!tab.empty()) std::memcpy(h + p->off_tab, tab.data(), tab.size() * sizeof(sk::TcItem));
+    if (!f4.items.empty()) std::memcpy(h + p->off_f4, f4.items.data(), f4.items.size() * sizeof(sk::F4Item));
     cudaError_t e = defer_upload ? cudaMallocAsync(&p->d_stage, bytes > 0 ? bytes : 256, stream)
                                  : cudaMalloc(&p->d_stage, bytes > 0 ? bytes : 256);
     if (e != cudaSuccess) { delete p; return e == cudaErrorMemoryAllocation ? SK_ENOMEM : cuda_fail(e, "cudaMalloc(plan)"); }
     unsigned char* dst = static_cast<unsigned char*>(p->d_stage);
     p->d_items = total > 0 ? reinterpret_cast<Item*>(dst + p->off_items) : nullptr;
-    p->d_tc = tc.empty() ? nullptr : reinterpret_cast<sk::TcItem*>(dst + p->off_tc);
-    p->d_f4t = f4t.empty() ? nullptr : reinterpret_cast<sk::TcItem*>(dst + p->off_f4t);
-    p->d_f4n = f4n.empty() ? nullptr : reinterpret_cast<sk::NItem*>(dst + p->off_f4n);
-    p->d_tab = tab.empty() ? nullptr : reinterpret_cast<sk::TcItem*>(dst + p->off_tab);
+    p->d_f4 = f4.items.empty() ? nullptr : reinterpret_cast<sk::F4Item*>(dst + p->off_f4);
   }
-  lap("f4n schedule + image + malloc");
+  lap("image + malloc");
   if (jki >= 0) {
     const int rj = build_jki(p, h_colptr, jki > 0, stream);
     if (rj != SK_OK) { cudaFree(p->d_stage); delete p; return rj; }
@@ -551,30 +524,16 @@ int apply_items(const sk_plan_s* p, uint64_t seed, sk_dist_t dist, const void* v
   a.ld = p->d;
   a.row_offset = p->row_offset;
   a.keys = sk::make_keys(seed);
-  cudaError_t e;
-  const int path = rad_f64_path();
-  if (dist == SK_RADEMACHER && p->dtype == SK_F32 && p->n_tab > 0 && rad_f32_path() == SK_PATH32_TABLE) {
-    e = sk::launch_apply_rad_tab(a, p->d_tab, p->n_tab, stream);
-  } else if (dist == SK_RADEMACHER && path == SK_PATH_TC_FP4T && p->n_f4t > 0) {
-    e = sk::launch_apply_rad_f4t(a, p->d_f4t, p->n_f4t, stream);
-  } else if (dist == SK_RADEMACHER && path == SK_PATH_TC_FP4N && p->n_f4n > 0 && sk::f4n_aligned(vals)) {
-    e = sk::launch_apply_rad_f4n(a, (int)p->dtype, p->d_f4n, p->n_f4n, p->n, p->nnz_end, stream);
-  } else if (dist == SK_RADEMACHER && p->n_tc > 0 && path != SK_PATH_SIMT && path != SK_PATH_TC_FP4N &&
-             path != SK_PATH_TC_FP4T) {
-    if (path == SK_PATH_HYBRID) {
-      int* counter = nullptr;
-      e = cudaMallocAsync((void**)&counter, sizeof(int), stream);
-      if (e == cudaSuccess) e = sk::launch_apply_rad_hybrid(a, p->d_tc, p->n_tc, counter, stream);
-      if (counter) cudaFreeAsync(counter, stream);
-    } else if (path == SK_PATH_TC_FP4) {
-      e = sk::launch_f4_zero_split(a, p->d_tc + p->n_tc + p->f4_tail_first, p->f4_tail_n, stream);
-      if (e == cudaSuccess) e = sk::launch_apply_rad_f4(a, p->d_tc + p->n_tc, p->n_f4, stream);
-    }
-    else e = sk::launch_apply_rad_tc(a, p->d_tc, p->n_tc, path == SK_PATH_TC_INT8_SMEM ? 1 : 0, stream);
+  cudaError_t e = cudaSuccess;
+  if (dist == SK_RADEMACHER) {
+    // tensor-core columns, then the SIMT kernel on the remaining columns (disjoint columns of Â)
+    if (p->n_f4 > 0) e = sk::launch_apply_rad_f4(a, p->d_f4, p->n_f4, p->f4_groups, stream);
+    if (e == cudaSuccess) e = sk::launch_apply(0, (int)p->dtype, a, stream);
   } else if ((dist == SK_UNIFORM || dist == SK_GAUSSIAN) && p->jki.n_items > 0 && pair_path() != SK_PAIR_KJI) {
     e = sk::launch_apply_jki((int)dist, (int)p->dtype, a, p->jki, stream);
-  } else
+  } else {
     e = sk::launch_apply((int)dist, (int)p->dtype, a, stream);
+  }
   if (e != cudaSuccess) return cuda_fail(e, "launch apply");
   return SK_OK;
 }
@@ -595,25 +554,11 @@ void ensure_pool() {
   if (!done) { PoolInit p; (void)p; done = true; }
 }
 
-
 const char* kernel_name(const sk_plan_s* p, int dist) {
   if (dist == SK_RADEMACHER) {
-    if (p->n_f4t > 0 && rad_f64_path() == SK_PATH_TC_FP4T) return "sk_rad_f4t_kernel (tcgen05 kind::mxf4, S in TMEM)";
-    if (p->n_f4n > 0 && rad_f64_path() == SK_PATH_TC_FP4N)
-      return p->dtype == SK_F32 ? "sk_rad_f4n_kernel<float> (tcgen05 kind::mxf4, N=256)"
-                                : "sk_rad_f4n_kernel<double> (tcgen05 kind::mxf4, N=256)";
-    if (p->dtype == SK_F32)
-      return p->n_tab > 0 && rad_f32_path() == SK_PATH32_TABLE ? "sk_rad_tab_kernel (fp32, 4-nonzero subset-sum tables)"
-                                                                : "sk_rad_kernel<float>";
-    if (p->n_tc > 0 && rad_f64_path() != SK_PATH_TC_FP4N && rad_f64_path() != SK_PATH_TC_FP4T) {
-      switch (rad_f64_path()) {
-        case SK_PATH_TC_FP4: return "sk_rad_f4_kernel (tcgen05 kind::mxf4)";
-        case SK_PATH_HYBRID: return "sk_rad_hybrid_kernel (tcgen05 kind::i8 + FP64 SIMT)";
-        case SK_PATH_TC_INT8_SMEM: return "sk_rad_tc_kernel (tcgen05 kind::i8, S in smem)";
-        case SK_PATH_TC_INT8_TMEM: return "sk_rad_tm_kernel (tcgen05 kind::i8, S in TMEM)";
-        default: break;
-      }
-    }
+    if (p->dtype == SK_F32) return "sk_rad_kernel<float>";
+    if (p->n_f4 > 0) return p->n_rad > 0 ? "sk_rad_f4_kernel (tcgen05 kind::mxf4) + sk_rad_kernel<double>"
+                                         : "sk_rad_f4_kernel (tcgen05 kind::mxf4)";
     return "sk_rad_kernel<double>";
   }
   const bool f64 = p->dtype == SK_F64;
@@ -893,6 +838,14 @@ int sketch_apply_host(uint64_t seed, sk_dist_t dist, sk_dtype_t dtype, int64_t d
   tmark(d2h);
   SK_STEP(cudaStreamWaitEvent(stream, ev_end, 0));
   SK_STEP(cudaMemcpyAsync(&h_flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  if (e != cudaSuccess) {
+    // A failed step skipped the later ones (including the join of the side streams into `stream`):
+    // drain every stream before the scratch is freed and before h_out is handed back.
+    cudaStreamSynchronize(h2d);
+    cudaStreamSynchronize(comp2);
+    cudaStreamSynchronize(d2h);
+    cudaStreamSynchronize(stream);
+  }
   if (d_colptr) cudaFreeAsync(d_colptr, stream);
   if (d_rowidx) cudaFreeAsync(d_rowidx, stream);
   if (d_vals) cudaFreeAsync(d_vals, stream);
@@ -938,10 +891,11 @@ int sketch_plan_stats(sk_plan_t plan, sk_stats_t* h) {
   h->n_items_jki = plan->jki.n_items;
   h->jki_nonzero_rows = plan->jki_rows;
   h->n_items_f4_split = plan->f4_split_items;
+  h->n_items_f4 = plan->n_f4;
+  h->n_cols_f4 = plan->f4_cols;
+  h->f4_split_groups = plan->f4_groups;
   h->plan_bytes = (plan->n_rad + plan->n_pair + plan->n_gauss) * (int64_t)sizeof(Item) +
-                  (plan->n_tc + plan->n_f4 + plan->n_f4t) * (int64_t)sizeof(sk::TcItem) +
-                  plan->n_f4n * (int64_t)sizeof(sk::NItem) +
-                  (plan->owned_colptr ? (plan->n + 1) * 8 : 0);
+                  plan->n_f4 * (int64_t)sizeof(sk::F4Item) + (plan->owned_colptr ? (plan->n + 1) * 8 : 0);
   return SK_OK;
 }
 
@@ -973,14 +927,8 @@ const char* sketch_last_error_detail(void) { return g_detail.c_str(); }
 const char* sketch_version(void) { return "libsketch 0.2.0 sm_100a"; }
 
 int sketch_set_rad_f64_path(int path) {
-  if (path < SK_PATH_TC_FP4 || path > SK_PATH_TC_FP4T) return SK_EINVAL;
+  if (path != SK_PATH_TC_FP4 && path != SK_PATH_SIMT) return SK_EINVAL;
   g_rad_f64_path.store(path, std::memory_order_relaxed);
-  return SK_OK;
-}
-
-int sketch_set_rad_f32_path(int path) {
-  if (path != SK_PATH32_TABLE && path != SK_PATH32_SIMT) return SK_EINVAL;
-  g_rad_f32_path.store(path, std::memory_order_relaxed);
   return SK_OK;
 }
 

@@ -36,28 +36,14 @@ namespace sk {
 namespace {
 
 constexpr int kF4Tiles = 6;                       // 128-row tiles per CTA (max)
-#ifndef SK_F4_KC
-#define SK_F4_KC 1
-#endif
-constexpr int kF4KC = SK_F4_KC;                   // K-step classes: A warp class c takes sub = c, c + kF4KC, ..
-constexpr int kF4AWarps = 2 * kF4Tiles * kF4KC;   // A producers: (tile, nonzero half, K-step class)
+constexpr int kF4AWarps = 2 * kF4Tiles;          // A producers: (tile, nonzero half)
 constexpr int kF4BWarps = 2;                      // B producers: nonzero half
 constexpr int kF4Producers = kF4AWarps + kF4BWarps;
 constexpr int kF4LoaderWarp = kF4Producers;       // streams rowidx / vals into a smem ring
 constexpr int kF4MmaWarp = kF4Producers + 1;
 constexpr int kF4Threads = (kF4Producers + 2) * 32;
-#ifndef SK_F4_B4
-#define SK_F4_B4 0
-#endif
-#if SK_F4_B4
-// Base-4 signed digits {-3, -1, 1, 3} (e2m1 0xD / 0xA / 0x2 / 0x5): 32 digit rows + ones row +
-// 7 zero rows, so the digits operand is 1280 B per K-step instead of 2304.
-constexpr int kF4N = 40;
-constexpr int kF4Ones = 32;
-#else
 constexpr int kF4N = 72;                          // 64 digit rows + ones row + 7 zero rows
 constexpr int kF4Ones = 64;
-#endif
 #ifndef SK_F4_SUB
 #define SK_F4_SUB 3                               // (4 at ptxas -O3; at -O1 3 measured 7.31 vs 7.35 ms)
 #define SK_F4_STAGES 2
@@ -69,7 +55,7 @@ constexpr int kF4Stages = SK_F4_STAGES;
 #endif
 constexpr int kF4JSlots = SK_F4_JDEPTH / kF4Sub;  // nonzero-stream ring: one slot = one smem stage (kF4Sub K-steps)
 constexpr int kF4ATile = 128 * 32;                // 128 rows x 64 fp4 = 4 KB
-constexpr int kF4BSub = SK_F4_B4 ? 1280 : 2560;   // B tile slot per K-step: row groups x 256 B (padded)
+constexpr int kF4BSub = 2560;                     // B tile slot per K-step: 10 row groups x 256 B (72 rows, padded)
 constexpr int kF4ATileS = kF4Sub * kF4ATile;      // one tile's A data per stage
 constexpr int kF4Stage = kF4Tiles * kF4ATileS + kF4Sub * kF4BSub;
 constexpr uint32_t kF4SfCol = 448;                // scale factors: TMEM columns [448, 512)
@@ -92,6 +78,7 @@ struct F4Shared {
   unsigned long long maxabs_bits;
   int32_t E;
   int32_t nonfinite;
+  int32_t last;      // this CTA is the last part of its split group to finish
 };
 
 __device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -186,38 +173,48 @@ __device__ __forceinline__ void f4_store_row_masked(uint32_t addr, uint32_t y, i
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" :: "r"(addr), "r"(w0), "r"(w1), "r"(w2), "r"(w3) : "memory");
 }
 
-// Partial transpose for the S operand (SK_F4_PART=1; off by default -- on c5 it measured 8.14 ms vs
-// 8.09 ms for the full transpose: 40% fewer shuffles, but 4x more STS instructions, and the shuffles
-// were not what binds the producers): only 3 exchange stages.  Stage a swaps
-// lane bit a with word bit a + 2 (shift 4 << a): on exit lane (lh, ll) = (l >> 3, l & 7), bit 4n + c
-// holds what lane (lh, n) had at bit 4 ll + c.  Each nibble word c then already holds 8 nonzeros of
-// ONE row, so 2 of the 5 shuffle stages of the full 32 x 32 transpose disappear (the shuffles share
-// the shared-memory data pipe with the STS of S and the tensor core's operand reads).
-#ifndef SK_F4_PART
-#define SK_F4_PART 0
-#endif
-template <int NW>
-__device__ __forceinline__ void f4_exchange3(uint32_t (&x)[NW], int lane) {
-  const uint32_t m0[3] = {0x0F0F0F0Fu, 0x00FF00FFu, 0x0000FFFFu};
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    const bool lower = (lane & (1 << a)) == 0;
-    const uint32_t keep = lower ? m0[a] : ~m0[a];
-    const uint32_t r = lower ? (4u << a) : 32u - (4u << a);   // rotate: << s in the lower lane, >> s in the upper
-    uint32_t y[NW];
-#pragma unroll
-    for (int k = 0; k < NW; ++k) y[k] = __shfl_xor_sync(0xFFFFFFFFu, x[k], 1 << a);
-#pragma unroll
-    for (int k = 0; k < NW; ++k) {
-      const uint32_t yr = __funnelshift_l(y[k], y[k], r);
-      asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(x[k]) : "r"(x[k]), "r"(yr), "r"(keep));
-    }
-  }
-}
-
 // byte offset of row m, K chunk h inside a K-major no-swizzle tile (core matrices 8 x 16 B)
 __device__ __forceinline__ uint32_t f4_off(int m, int h) {
   return (uint32_t)((m >> 3) * 256 + h * 128 + (m & 7) * 16);
+}
+
+// Non-finite column (a NaN or an Inf among its values; the digit encoding needs finite values):
+// every entry of Â[:, k] is then non-finite, so only the non-finite terms S[i,p] a_p decide it, and
+// IEEE addition in ANY order gives NaN if a term is NaN or both +Inf and -Inf occur, else the sign
+// of the infinite terms -- exactly what the oracle's sequential sum gives.  The CTA finds the
+// non-finite values of the whole column, ORs each row's term signs into shared flags, and writes
+// its rows.  (Rare path: one Philox block per (non-finite value, tile).)
+__device__ void f4_nonfinite_column(const ApplyArgs& P, const F4Item& it, int64_t cb, int64_t ce,
+                                    uint32_t* flags /* >= kF4Tiles * 128 + 1 words of smem */) {
+  const int T = f4_ntiles(it);
+  for (int i = threadIdx.x; i <= T * 128; i += blockDim.x) flags[i] = 0u;
+  __syncthreads();
+  const double* vals = reinterpret_cast<const double*>(P.vals);
+  for (int64_t p = cb + threadIdx.x; p < ce; p += blockDim.x) {
+    const double v = vals[p];
+    if (isfinite(v)) continue;
+    if (isnan(v)) { atomicOr(&flags[T * 128], 1u); continue; }
+    const uint32_t vneg = signbit(v) ? 1u : 0u;
+    const uint64_t j = (uint64_t)P.row_offset + (uint32_t)P.rowidx[p];
+    for (int tt = 0; tt < T; ++tt) {
+      const uint4 x = s_block((uint32_t)(it.tile0 + tt), j, P.keys);
+      const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+      for (int r = 0; r < 128; ++r) {
+        const uint32_t neg = ((w[r >> 5] >> (r & 31)) & 1u) ^ vneg;   // sign of S[i,p] a_p
+        atomicOr(&flags[tt * 128 + r], neg ? 2u : 1u);
+      }
+    }
+  }
+  __syncthreads();
+  double* outc = reinterpret_cast<double*>(P.out) + (int64_t)it.col * P.ld;
+  const bool anynan = flags[T * 128] != 0u;
+  for (int r = threadIdx.x; r < T * 128; r += blockDim.x) {
+    const int64_t row = (int64_t)it.tile0 * 128 + r;
+    if (row >= P.d) break;
+    const uint32_t f = flags[r];
+    outc[row] = (anynan || f == 3u) ? __longlong_as_double(0x7FF8000000000000ll)
+                                    : (f == 2u ? -INFINITY : INFINITY);
+  }
 }
 
 // dbg (SKETCH_F4_DEBUG; tuning only, results invalid when nonzero), bit flags: 1 = no S stores,
@@ -225,33 +222,38 @@ __device__ __forceinline__ uint32_t f4_off(int m, int h) {
 // Philox and the transposes, 64 = MMAs with N = 8.
 // The debug switches exist only in builds with -DSK_F4_DEBUG=1 (the default build has none, so
 // they cannot perturb the schedule of the production kernel).
-#ifndef SK_F4_STAGGER_NS
-#define SK_F4_STAGGER_NS 0
-#endif
 #ifndef SK_F4_DEBUG
 #define SK_F4_DEBUG 0
 #endif
-__global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArgs P, const TcItem* items, int dbg_arg) {
+__global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArgs P, const F4Item* items,
+                                                                   unsigned long long* __restrict__ ws,
+                                                                   unsigned int* __restrict__ ws_count, int dbg_arg) {
   const int dbg = SK_F4_DEBUG ? dbg_arg : 0;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* stages = smem_raw + ((1024u - (s_u32(smem_raw) & 1023u)) & 1023u);
   F4Shared& sh = *reinterpret_cast<F4Shared*>(stages + kF4Stages * kF4Stage);
-  const TcItem it = items[blockIdx.x];
+  const F4Item it = items[blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int64_t pb = P.colptr[it.col], pe = P.colptr[it.col + 1];
-  if (it.pad) {   // last-wave item split along K: pad 1 = first half of the K-steps, 2 = second half
-    const int64_t half = ((((pe - pb) + 63) >> 6) >> 1) << 6;
-    if (it.pad == 1) pe = pb + half; else pb += half;
+  // The column's nonzeros [cb, ce); this item's K range [pb, pe) is part `part` of `nparts` equal
+  // shares of its 64-nonzero K-steps (nparts > 1: columns longer than kTcMaxColumn, and the
+  // last-wave items split along K).  E is the column-wide exponent so all parts use one scale.
+  const int64_t cb = P.colptr[it.col], ce = P.colptr[it.col + 1];
+  const int part = f4_part(it), nparts = f4_nparts(it);
+  int64_t pb = cb, pe = ce;
+  if (nparts > 1) {
+    const int64_t ns = (ce - cb + 63) >> 6;
+    pb = cb + 64 * ((ns * part) / nparts);
+    pe = min(ce, cb + 64 * ((ns * (part + 1)) / nparts));
   }
   const int64_t L = pe - pb;
   const int nsteps = (int)((L + 63) >> 6);
   const int nsup = (nsteps + kF4Sub - 1) / kF4Sub;
-  const int T = it.ntiles;                         // <= kF4Tiles
+  const int T = f4_ntiles(it);                     // <= kF4Tiles
   const double* vals = reinterpret_cast<const double*>(P.vals);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kF4Stages; ++s) { f4_mbar_init(&sh.full[s], 2 * T * kF4KC + kF4BWarps); f4_mbar_init(&sh.empty[s], 1); }
-    for (int s = 0; s < kF4JSlots; ++s) { f4_mbar_init(&sh.jfull[s], 32); f4_mbar_init(&sh.jempty[s], 2 * T * kF4KC + kF4BWarps); }
+    for (int s = 0; s < kF4Stages; ++s) { f4_mbar_init(&sh.full[s], 2 * T + kF4BWarps); f4_mbar_init(&sh.empty[s], 1); }
+    for (int s = 0; s < kF4JSlots; ++s) { f4_mbar_init(&sh.jfull[s], 32); f4_mbar_init(&sh.jempty[s], 2 * T + kF4BWarps); }
     f4_mbar_init(&sh.done, 1);
     sh.maxabs_bits = 0ull;
     sh.nonfinite = 0;
@@ -284,9 +286,9 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   }
-  // column scale E (all producers)
+  // column scale E (all producers), over the whole column
   if (warp < kF4Producers && !(dbg & 16)) {
-    unsigned long long mx = col_absmax_bits(vals, pb, pe, threadIdx.x, kF4Producers * 32);
+    unsigned long long mx = col_absmax_bits(vals, cb, ce, threadIdx.x, kF4Producers * 32);
     for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
     if (lane == 0) atomicMax(&sh.maxabs_bits, mx);
   }
@@ -299,80 +301,52 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
   }
   __syncthreads();
   const int E = sh.E;
+  if (sh.nonfinite) {
+    f4_nonfinite_column(P, it, cb, ce, reinterpret_cast<uint32_t*>(stages));
+    __syncthreads();
+    if (warp == kF4MmaWarp) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(512));
+    }
+    return;
+  }
 
-  if (warp < 2 * T * kF4KC) {
-    // ===================== A producers: S tile (w % T), nonzero half, K-step class =====================
-    const int t = warp % T, h = (warp / T) & 1, kc = warp / (2 * T);
-    constexpr int kMine = kF4Sub / kF4KC;            // K-steps of a stage this warp produces
-    static_assert(kMine * kF4KC == kF4Sub, "K-step classes must divide the stage");
+  if (warp < 2 * T) {
+    // ===================== A producers: S tile (w % T), nonzero half =====================
+    const int t = warp % T, h = warp / T;
     const uint32_t q = (uint32_t)(it.tile0 + t);
     // One smem stage holds kF4Sub K-steps: the warp generates all of them (independent Philox
     // chains, 4 kF4Sub interleaved 32x32 transposes) and signals the stage once.  Their row indices
     // come from one ring slot (one wait, one release per stage; padding past the column end was
     // zero-filled by the loader).
-#if SK_F4_PART
-    // lane (lh, n) takes nonzero 4n + lh: after f4_exchange3 nibble n of k-group lh is K position
-    // 8 lh + n, the B operand's order (K position 8c + n <-> nonzero 4n + c)
-    const int jl = 32 * h + 4 * (lane & 7) + (lane >> 3);
-#else
     const int jl = 32 * h + lane;
-#endif
-#if SK_F4_STAGGER_NS > 0
-    // The three S warps of a scheduler run identical code; started together they stay in phase
-    // (all in Philox, then all in shuffles ...).  Offset them by a fraction of a stage.
-    if (const int g = (warp >> 2) % 3) __nanosleep((unsigned)(g * SK_F4_STAGGER_NS));
-#endif
     for (int ss = 0; ss < nsup; ++ss) {
       const int stage = ss % kF4Stages, use = ss / kF4Stages;
       const int jslot = ss % kF4JSlots;
       f4_wait(&sh.jfull[jslot], (ss / kF4JSlots) & 1);
-      uint32_t jv[kMine];
+      uint32_t jv[kF4Sub];
 #pragma unroll
-      for (int i = 0; i < kMine; ++i) jv[i] = sh.js[jslot][64 * (kc + kF4KC * i) + jl];
+      for (int i = 0; i < kF4Sub; ++i) jv[i] = sh.js[jslot][64 * i + jl];
       __syncwarp();
       if (lane == 0) f4_arrive(&sh.jempty[jslot]);   // one arrival per warp
-      uint32_t x[4 * kMine];
+      uint32_t x[4 * kF4Sub];
 #pragma unroll
-      for (int i = 0; i < kMine; ++i) {
+      for (int i = 0; i < kF4Sub; ++i) {
         const uint32_t j = jv[i];
         const uint4 xb = (dbg & 32) ? make_uint4(j, j ^ 1u, j ^ 2u, j ^ 3u)
                                     : s_block(q, (uint64_t)P.row_offset + j, P.keys);   // padded nonzeros: B = 0
         x[4 * i + 0] = xb.x; x[4 * i + 1] = xb.y; x[4 * i + 2] = xb.z; x[4 * i + 3] = xb.w;
       }
-#if SK_F4_PART
-      f4_exchange3<4 * kMine>(x, lane);
-      if (use > 0) f4_wait(&sh.empty[stage], (use - 1) & 1);
-      if (!(dbg & 1)) {
-        // word qq, nibble word c: Â row 32 qq + 4 ll + c, stored as tile row R = 32 qq + 8 c + ll
-        // (the epilogue undoes the permutation), k-group lh: one STS.32 per (qq, c), the 32 lanes on
-        // 32 distinct banks (bank = 4 ll + lh)
-        const uint32_t tile = s_u32(stages + stage * kF4Stage) + (uint32_t)(t * kF4ATileS) +
-                              (uint32_t)(h * 128 + (lane & 7) * 16 + (lane >> 3) * 4);
-#pragma unroll
-        for (int i = 0; i < kMine; ++i)
-#pragma unroll
-          for (int qq = 0; qq < 4; ++qq) {
-            const int sub = kc + kF4KC * i;
-            const uint32_t y = x[4 * i + qq];
-#pragma unroll
-            for (int c = 0; c < 4; ++c)
-              asm volatile("st.shared.b32 [%0], %1;"
-                           :: "r"(tile + (uint32_t)(sub * kF4ATile + (4 * qq + c) * 256)), "r"(f4_nib(y << (3 - c)))
-                           : "memory");
-          }
-      }
-#else
-      if (!(dbg & 32)) f4_transpose<4 * kMine>(x, lane);   // lane r: row 32qq + r over 32 nonzeros
+      if (!(dbg & 32)) f4_transpose<4 * kF4Sub>(x, lane);   // lane r: row 32qq + r over 32 nonzeros
       if (use > 0) f4_wait(&sh.empty[stage], (use - 1) & 1);
       if (!(dbg & 1)) {
         const uint32_t tile = s_u32(stages + stage * kF4Stage) + (uint32_t)(t * kF4ATileS) + f4_off(lane, h);
 #pragma unroll
-        for (int i = 0; i < kMine; ++i)
+        for (int i = 0; i < kF4Sub; ++i)
 #pragma unroll
           for (int qq = 0; qq < 4; ++qq)   // row 32qq + lane
-            f4_store_row(tile + (uint32_t)((kc + kF4KC * i) * kF4ATile + qq * 4 * 256), x[4 * i + qq]);
+            f4_store_row(tile + (uint32_t)(i * kF4ATile + qq * 4 * 256), x[4 * i + qq]);
       }
-#endif
       if (!(dbg & 4)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) f4_arrive(&sh.full[stage]);
@@ -407,52 +381,17 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
           const long long A = __double2ll_rn((v0 * sc1) * sc2);
           U = (unsigned long long)A ^ 0x8000000000000000ull;
         }
-#if SK_F4_B4
-        x[2 * sub] = (uint32_t)U;                  // bits of U (digit s uses bits 2s, 2s+1)
-        x[2 * sub + 1] = (uint32_t)(U >> 32);
-#else
         x[2 * sub] = ~(uint32_t)U;                 // sign bits of the digit nibbles
         x[2 * sub + 1] = ~(uint32_t)(U >> 32);
-#endif
       }
       f4_transpose<2 * kF4Sub>(x, lane);           // lane r: bit r (and 32 + r) of U per K-step
-#if SK_F4_B4
-      // digit s = 4 b_{2s+1} + 2 b_{2s} - 3: even lane r pairs its bit r of the low word with lane
-      // r+1's (digit r/2), odd lane r pairs lane r-1's bit of the high word with its own (digit
-      // 16 + r/2).  One SHFL per K-step brings the pairs together.
-      const bool odd = lane & 1;
-      const int brow = odd ? 16 + (lane >> 1) : (lane >> 1);
-      uint32_t b0w[kF4Sub], b1w[kF4Sub];
-#pragma unroll
-      for (int sub = 0; sub < kF4Sub; ++sub) {
-        const uint32_t lo = x[2 * sub], hi = x[2 * sub + 1];
-        const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, odd ? lo : hi, 1);
-        b0w[sub] = odd ? y : lo;
-        b1w[sub] = odd ? hi : y;
-      }
-#endif
       if (use > 0) f4_wait(&sh.empty[stage], (use - 1) & 1);
       if (!(dbg & 8)) {
 #pragma unroll
         for (int sub = 0; sub < kF4Sub; ++sub) {
           const uint32_t bt = s_u32(stages + stage * kF4Stage + kF4Tiles * kF4ATileS + sub * kF4BSub);
-#if SK_F4_B4
-          // nibble n of word c = nonzero 4n + c: sign = !b1, magnitude 3 (0b101) iff b1 == b0, else 1 (0b010)
-          const uint32_t sg = ~b1w[sub], eq = ~(b1w[sub] ^ b0w[sub]);
-          uint32_t wv[4];
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const uint32_t a = sg << (3 - c);
-            const uint32_t t = c <= 2 ? eq << (2 - c) : eq >> 1;   // bit 4n + c -> 4n + 2
-            wv[c] = (a & 0x88888888u) | (t & 0x44444444u) | (~(t >> 1) & 0x22222222u) | ((t >> 2) & 0x11111111u);
-            if (nval[sub] < 32) wv[c] &= f4_valid_mask(c, nval[sub]);
-          }
-          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};"
-                       :: "r"(bt + f4_off(brow, h)), "r"(wv[0]), "r"(wv[1]), "r"(wv[2]), "r"(wv[3]) : "memory");
-#else
           f4_store_row_masked(bt + f4_off(lane, h), x[2 * sub], nval[sub]);
           f4_store_row_masked(bt + f4_off(32 + lane, h), x[2 * sub + 1], nval[sub]);
-#endif
           if (nval[sub] < 32 && lane == 0) {   // partial (last) K chunk: the ones row too
             const uint32_t z = 0u;              // (y = 0 -> nibbles 0x2 = +1.0)
             f4_store_row_masked(bt + f4_off(kF4Ones, h), z, nval[sub]);
@@ -518,14 +457,18 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
   }
 
   // ===================== epilogue: warps 0..11 read D (lane quarter = warp % 4) =====================
+  // Σ_s 2^s D_s - D_64 = hi 2^32 + (lo - ones): both parts exact int64.  Whole columns round once
+  // into fp64; the parts of a split column add their (hi, lo - ones) into an int64 workspace
+  // (integer atomics: exact, so the order of the parts cannot change a bit), and the last part to
+  // finish converts the sums.
+  double* outc = reinterpret_cast<double*>(P.out) + (int64_t)it.col * P.ld;
+  unsigned long long* wsg = nparts > 1 ? ws + 2 * (size_t)it.group * (kF4Tiles * 128) : nullptr;
   if (warp < kF4Producers) {
     if (nsteps > 0) {
       f4_wait(&sh.done, 0);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     }
     const int qw = warp & 3;
-    double* outc = reinterpret_cast<double*>(P.out) + (int64_t)it.col * P.ld;
-    const double nan = __longlong_as_double(0x7FF8000000000000ll);
     for (int tt = warp >> 2; warp < 12 && tt < T; tt += 3) {
       long long lo = 0, hi = 0, ones = 0;
       if (nsteps > 0) {
@@ -541,39 +484,48 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
           for (int u = 0; u < 8; ++u) {
             const long long dv = (long long)__float2ll_rn(__uint_as_float(D[u]));
             const int s = c + u;
-#if SK_F4_B4
-            // Σ_s 4^s D_s - D_32: low 16 digits into lo, high 16 into hi (weights 4^(s-16))
-            if (s < 16) lo += dv << (2 * s);
-            else if (s < 32) hi += dv << (2 * (s - 16));
-            else if (s == 32) ones = dv;
-#else
             if (s < 32) lo += dv << s;
             else if (s < 64) hi += dv << (s - 32);
             else if (s == 64) ones = dv;
-#endif
           }
         }
       }
-#if SK_F4_PART
-      // TMEM lane R = 32 qw + lane holds Â row 32 qw + 4 (R & 7) + ((R >> 3) & 3) of the tile
-      const int64_t row = (int64_t)(it.tile0 + tt) * 128 + 32 * qw + 4 * (lane & 7) + (lane >> 3);
-#else
-      const int64_t row = (int64_t)(it.tile0 + tt) * 128 + 32 * qw + lane;
-#endif
+      const int r = tt * 128 + 32 * qw + lane;
+      const int64_t row = (int64_t)it.tile0 * 128 + r;
       if (row < P.d) {
-        // Σ_s 2^s D_s - D_64 = hi 2^32 + (lo - ones), both parts exact in fp64; one rounding
-        const double v = scalbn((double)hi * 4294967296.0 + (double)(lo - ones), E - 62);
-        const double res = sh.nonfinite ? nan : v;
-        // K-split halves add into the zeroed output: 0 + a + b rounds the same in either order
-        if (it.pad) atomicAdd(outc + row, res); else outc[row] = res;
+        if (wsg) {
+          atomicAdd(wsg + 2 * r, (unsigned long long)hi);
+          atomicAdd(wsg + 2 * r + 1, (unsigned long long)(lo - ones));
+        } else {
+          outc[row] = scalbn((double)hi * 4294967296.0 + (double)(lo - ones), E - 62);
+        }
       }
     }
+    if (wsg) __threadfence();
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   }
   __syncthreads();
   if (warp == kF4MmaWarp) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(512));
+  }
+  if (wsg) {
+    // last part of the split group: convert the int64 sums (its reads see every part's atomics:
+    // each part fenced before counting itself in)
+    if (threadIdx.x == 0) {
+      const unsigned int prev = atomicAdd(ws_count + it.group, 1u);
+      sh.last = prev == (unsigned)(nparts - 1);
+      __threadfence();
+    }
+    __syncthreads();
+    if (sh.last) {
+      for (int r = threadIdx.x; r < T * 128; r += blockDim.x) {
+        const int64_t row = (int64_t)it.tile0 * 128 + r;
+        if (row >= P.d) break;
+        const long long hi = (long long)__ldcg(wsg + 2 * r), lo = (long long)__ldcg(wsg + 2 * r + 1);
+        outc[row] = scalbn((double)hi * 4294967296.0 + (double)lo, E - 62);
+      }
+    }
   }
 }
 
@@ -585,30 +537,29 @@ int f4_tiles_per_cta() {   // SKETCH_F4_TILES (tuning only): fewer row tiles per
   return t;
 }
 
-// Zero the Â rows of the K-split items (pad == 1 marks the first half of each pair).
-__global__ void sk_f4_zero_split_kernel(const ApplyArgs P, const TcItem* items) {
-  const TcItem it = items[blockIdx.x];
-  if (it.pad != 1) return;
-  const int64_t r0 = (int64_t)it.tile0 * 128;
-  const int64_t r1 = min(P.d, (int64_t)(it.tile0 + it.ntiles) * 128);
-  double* o = reinterpret_cast<double*>(P.out) + (int64_t)it.col * P.ld;
-  for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) o[r] = 0.0;
-}
-
-cudaError_t launch_f4_zero_split(const ApplyArgs& a, const TcItem* items, int64_t n_items, cudaStream_t stream) {
-  if (n_items == 0) return cudaSuccess;
-  sk_f4_zero_split_kernel<<<(unsigned)n_items, 256, 0, stream>>>(a, items);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const TcItem* items, int64_t n_items, cudaStream_t stream) {
+cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const F4Item* items, int64_t n_items, int64_t n_groups,
+                                cudaStream_t stream) {
   if (n_items == 0) return cudaSuccess;
   const size_t smem = (size_t)kF4Stages * kF4Stage + sizeof(F4Shared) + 1024;
   cudaError_t e = cudaFuncSetAttribute(sk_rad_f4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   static const int dbg = [] { const char* v = getenv("SKETCH_F4_DEBUG"); return v ? atoi(v) : 0; }();
-  sk_rad_f4_kernel<<<(unsigned)n_items, kF4Threads, smem, stream>>>(a, items, dbg);
-  return cudaGetLastError();
+  // split groups: int64 (hi, lo) per row + one arrival counter per group, zeroed stream-ordered
+  unsigned long long* ws = nullptr;
+  unsigned int* cnt = nullptr;
+  const size_t ws_bytes = (size_t)n_groups * kF4Tiles * 128 * 16, cnt_bytes = (size_t)n_groups * 4;
+  if (n_groups > 0) {
+    e = cudaMallocAsync((void**)&ws, ws_bytes + cnt_bytes, stream);
+    if (e != cudaSuccess) return e;
+    cnt = reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(ws) + ws_bytes);
+    e = cudaMemsetAsync(ws, 0, ws_bytes + cnt_bytes, stream);
+  }
+  if (e == cudaSuccess) {
+    sk_rad_f4_kernel<<<(unsigned)n_items, kF4Threads, smem, stream>>>(a, items, ws, cnt, dbg);
+    e = cudaGetLastError();
+  }
+  if (ws) { const cudaError_t e2 = cudaFreeAsync(ws, stream); if (e == cudaSuccess) e = e2; }
+  return e;
 }
 
 }  // namespace sk

@@ -28,7 +28,6 @@ namespace {
 constexpr int kJWarps = 16;
 constexpr int kJRowsPerWarp = 64;
 constexpr int kJRows = kJWarps * kJRowsPerWarp;   // Â rows per work item
-constexpr int kJLogTabBytes = 129 * 4 * 8;
 
 template <int DIST, typename T>
 __device__ __forceinline__ void jki_entries(const uint4 x, const double* __restrict__ logtab, T& v0, T& v1) {
@@ -38,7 +37,7 @@ __device__ __forceinline__ void jki_entries(const uint4 x, const double* __restr
     else { v0 = __double2float_rn(d0); v1 = __double2float_rn(d1); }
   } else {
     double g0, g1;
-    gaussian_pair_fast(x, logtab, g0, g1);
+    gaussian_pair_fast<kLogRep>(x, logtab, g0, g1);
     if constexpr (sizeof(T) == 8) { v0 = g0; v1 = g1; }
     else { v0 = __double2float_rn(g0); v1 = __double2float_rn(g1); }
   }
@@ -48,11 +47,12 @@ template <int DIST, typename T>
 __global__ void __launch_bounds__(kJWarps * 32, 1) sk_jki_kernel(const ApplyArgs P, JkiPlanView J) {
   extern __shared__ __align__(16) unsigned char smem[];
   T* acc = reinterpret_cast<T*>(smem);                                    // [warp][k][64 rows]
-  double* logtab = reinterpret_cast<double*>(smem + kJWarps * kJCols * kJRowsPerWarp * sizeof(T));
+  double* logtab_base = reinterpret_cast<double*>(smem + kJWarps * kJCols * kJRowsPerWarp * sizeof(T));
+  const double* logtab = logtab_base + (threadIdx.x & (kLogRep - 1));   // replicated -2 log table
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const JItem it = J.items[blockIdx.x];
   if constexpr (DIST == 2) {
-    for (int i = threadIdx.x; i < 129 * 4; i += blockDim.x) logtab[i] = (&kBmLogTab[0][0])[i];
+    bm_fill_logtab(logtab_base);
   }
   T* mine = acc + warp * (kJCols * kJRowsPerWarp);
 #pragma unroll
@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(kJWarps * 32, 1) sk_jki_kernel(const ApplyArgs
 
 template <int DIST, typename T>
 cudaError_t launch_jki_t(const ApplyArgs& a, const JkiPlanView& J, cudaStream_t stream) {
-  const size_t smem = (size_t)kJWarps * kJCols * kJRowsPerWarp * sizeof(T) + (DIST == 2 ? kJLogTabBytes : 0);
+  const size_t smem = (size_t)kJWarps * kJCols * kJRowsPerWarp * sizeof(T) + (DIST == 2 ? kLogTabRepBytes : 0);
   cudaError_t e = cudaFuncSetAttribute(sk_jki_kernel<DIST, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   sk_jki_kernel<DIST, T><<<(unsigned)J.n_items, kJWarps * 32, smem, stream>>>(a, J);

@@ -107,6 +107,11 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 2 : 1) sk_rad_kerne
 #pragma unroll
   for (int b = 0; b < 32; ++b) acc[b] = T(0);
   T total = T(0);   // fp32 "T - 2P" form only
+  // fp32: non-finite values stay out of T and P (Inf - 2 Inf would be NaN); the signs of the
+  // infinite terms are kept per row as masks in shared memory (+Inf rows, -Inf rows; a NaN sets
+  // both) and applied at the end, so the rows come out as IEEE addition gives them.
+  uint32_t* infm = reinterpret_cast<uint32_t*>(smem + kXchBytes + kWarps * 32 * kRadPad * sizeof(T)) + 2 * threadIdx.x;
+  if constexpr (sizeof(T) == 4) { infm[0] = 0u; infm[1] = 0u; }
 
   for (int64_t p = s0; p < s1; p += 32) {
     const int cnt = (int)((s1 - p) < 32 ? (s1 - p) : 32);
@@ -115,6 +120,21 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 2 : 1) sk_rad_kerne
     if (lane < cnt) {
       jl = __ldg(P.rowidx + p + lane);
       al = ldg_val<T>(P.vals, p + lane);
+    }
+    if constexpr (sizeof(T) == 4) {
+      if (__any_sync(kFull, !isfinite(al))) {   // rare: take the chunk's non-finite values out first
+        if (__any_sync(kFull, isnan(al))) { infm[0] = ~0u; infm[1] = ~0u; }
+        for (unsigned m = __ballot_sync(kFull, isinf(al)); m; m &= m - 1) {
+          const int s = __ffs(m) - 1;
+          const T ai = __shfl_sync(kFull, al, s);
+          const uint32_t jr = (uint32_t)__shfl_sync(kFull, jl, s);
+          const uint4 x = s_block(q, (uint64_t)P.row_offset + jr, P.keys);
+          const uint32_t ww = t == 0 ? x.x : t == 1 ? x.y : t == 2 ? x.z : x.w;   // this lane's 32 rows
+          infm[0] |= ai > T(0) ? ~ww : ww;                                          // S = -1 where the bit is set
+          infm[1] |= ai > T(0) ? ww : ~ww;
+        }
+        if (!isfinite(al)) al = T(0);
+      }
     }
     const int ngroups = (cnt + 3) >> 2;
     for (int u = 0; u < ngroups; ++u) {
@@ -143,7 +163,16 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 2 : 1) sk_rad_kerne
   T* red = reinterpret_cast<T*>(smem + kXchBytes);
   T* mine = red + warp * (32 * kRadPad) + lane * kRadPad;
 #pragma unroll
-  for (int b = 0; b < 32; ++b) mine[b] = finish_sign_sum(acc[b], total);
+  for (int b = 0; b < 32; ++b) {
+    T v = finish_sign_sum(acc[b], total);
+    if constexpr (sizeof(T) == 4) {
+      const bool pi = (infm[0] >> b) & 1u, ni = (infm[1] >> b) & 1u;
+      if (pi && ni) v = __int_as_float(0x7FC00000);
+      else if (pi) v = __int_as_float(0x7F800000);
+      else if (ni) v = __int_as_float((int)0xFF800000);
+    }
+    mine[b] = v;
+  }
   __syncthreads();
   T* outc = reinterpret_cast<T*>(P.out) + (int64_t)it.col * P.ld;
   const int rows = WD * kRowsPerWarpRad;
@@ -164,10 +193,8 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 2 : 1) sk_rad_kerne
 // q = (warp_row0 + 16 l)/E + h; each block yields E entries (E = 2 for uniform / Gaussian, 4 for
 // uniform24), so a lane generates exactly the S entries it consumes (no exchange).
 template <int DIST> constexpr int pair_E() { return DIST == 3 ? 4 : 2; }
-template <int DIST, typename T>
-__device__ __forceinline__ void block_entries(const uint4 x, T (&v)[pair_E<DIST>()], const double* __restrict__ logtab);
-
-template <int DIST, typename T>
+// logtab / STRIDE: the -2 log table (philox.cuh bm_m2log_u53), Gaussian only.
+template <int DIST, typename T, int STRIDE = kLogRep>
 __device__ __forceinline__ void pair_entries(const uint4 x, T& v0, T& v1, const double* __restrict__ logtab) {
   if constexpr (DIST == 1) {
     const double d0 = uniform53(x.x, x.y), d1 = uniform53(x.z, x.w);
@@ -175,18 +202,18 @@ __device__ __forceinline__ void pair_entries(const uint4 x, T& v0, T& v1, const 
     else { v0 = __double2float_rn(d0); v1 = __double2float_rn(d1); }
   } else {
     double g0, g1;
-    gaussian_pair_fast(x, logtab, g0, g1);
+    gaussian_pair_fast<STRIDE>(x, logtab, g0, g1);
     if constexpr (sizeof(T) == 8) { v0 = g0; v1 = g1; }
     else { v0 = __double2float_rn(g0); v1 = __double2float_rn(g1); }
   }
 }
 
-template <int DIST, typename T>
+template <int DIST, typename T, int STRIDE = kLogRep>
 __device__ __forceinline__ void block_entries(const uint4 x, T (&v)[pair_E<DIST>()], const double* __restrict__ logtab) {
   if constexpr (DIST == 3) {
     v[0] = (T)uniform24(x.x); v[1] = (T)uniform24(x.y); v[2] = (T)uniform24(x.z); v[3] = (T)uniform24(x.w);
   } else {
-    pair_entries<DIST, T>(x, v[0], v[1], logtab);
+    pair_entries<DIST, T, STRIDE>(x, v[0], v[1], logtab);
   }
 }
 
@@ -195,7 +222,6 @@ __device__ __forceinline__ void block_entries(const uint4 x, T (&v)[pair_E<DIST>
 // c3 16.1 -> 15.0 ms, while uniform prefers 16: 2.71 vs 2.82 ms on c2).
 template <int DIST> constexpr int pair_rows() { return (DIST == 2 ? kRowsPerWarpGauss : kRowsPerWarpPair) / 32; }
 constexpr int kPairRedBytes = kWarps * 32 * (kRowsPerWarpPair / 32 + 1) * 8;   // reduction area (fp64 worst case)
-constexpr int kLogTabBytes = 129 * 4 * 8;
 
 #ifndef SK_GAUSS_MINB
 #define SK_GAUSS_MINB 1
@@ -204,9 +230,10 @@ template <int DIST, typename T>
 __global__ void __launch_bounds__(kThreads, DIST == 2 ? SK_GAUSS_MINB : 1) sk_pair_kernel(const ApplyArgs P) {
   constexpr int kPairRows = pair_rows<DIST>(), kPairPad = kPairRows + 1, kRowsPerWarp = 32 * kPairRows;
   extern __shared__ __align__(16) unsigned char smem[];
-  double* logtab = reinterpret_cast<double*>(smem + kPairRedBytes);   // Gaussian: log table copy
+  // Gaussian: the replicated -2 log table; this lane reads copy lane mod kLogRep
+  double* logtab = reinterpret_cast<double*>(smem + kPairRedBytes) + (threadIdx.x & (kLogRep - 1));
   if constexpr (DIST == 2) {
-    for (int i = threadIdx.x; i < 129 * 4; i += blockDim.x) logtab[i] = (&kBmLogTab[0][0])[i];
+    bm_fill_logtab(reinterpret_cast<double*>(smem + kPairRedBytes));
     __syncthreads();
   }
   const Item it = P.items[blockIdx.x];
@@ -302,7 +329,7 @@ __global__ void sk_fill_s_kernel(PhiloxKeys K, int64_t i0, int64_t i1, int64_t j
     } else {
       constexpr int kE = pair_E<DIST>();
       T v[kE];
-      block_entries<DIST, T>(x, v, &kBmLogTab[0][0]);
+      block_entries<DIST, T, 1>(x, v, &kBmLogTab[0][0]);
 #pragma unroll
       for (int t = 0; t < kE; ++t) {
         const int64_t i = q * kE + t;
@@ -336,10 +363,10 @@ cudaError_t launch_items(K kernel, size_t smem, const ApplyArgs& a, cudaStream_t
 
 cudaError_t launch_apply(int dist, int dtype, const ApplyArgs& a, cudaStream_t stream) {
   const size_t rad64 = kXchBytes + (size_t)kWarps * 32 * kRadPad * 8;
-  const size_t rad32 = kXchBytes + (size_t)kWarps * 32 * kRadPad * 4;
+  const size_t rad32 = kXchBytes + (size_t)kWarps * 32 * kRadPad * 4 + kThreads * 8;   // + Inf masks
   const size_t pair64 = (size_t)kPairRedBytes;
   const size_t pair32 = (size_t)kPairRedBytes;
-  const size_t gauss = (size_t)kPairRedBytes + kLogTabBytes;
+  const size_t gauss = (size_t)kPairRedBytes + kLogTabRepBytes;
   if (dist == 0) {
     if (dtype == 1) return launch_items(sk_rad_kernel<float, 0>, rad32, a, stream);
     static const int selmode = [] {

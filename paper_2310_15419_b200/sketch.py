@@ -29,9 +29,8 @@ EXPORTS = ["sketch_plan", "sketch_plan_host", "sketch_apply", "sketch_apply_csc"
            "sketch_apply_host", "sketch_fill_s", "sketch_plan_stats", "sketch_plan_destroy",
            "sketch_error_string", "sketch_last_error_detail", "sketch_version",
            "sketch_set_rad_f64_path", "sketch_apply_kernel_name", "sketch_set_pair_path",
-           "sketch_plan_host_jki", "sketch_set_rad_f32_path"]
-RAD_F64_PATHS = {"fp4": 0, "int8smem": 1, "int8tmem": 2, "simt": 3, "hybrid": 4, "fp4n": 5, "fp4t": 6}
-RAD_F32_PATHS = {"tab": 0, "simt": 1}
+           "sketch_plan_host_jki"]
+RAD_F64_PATHS = {"fp4": 0, "simt": 3}
 PAIR_PATHS = {"auto": 0, "kji": 1, "jki": 2}
 _STRING_RESULTS = ("sketch_error_string", "sketch_last_error_detail", "sketch_version",
                    "sketch_apply_kernel_name")
@@ -46,7 +45,8 @@ class SketchError(RuntimeError):
 class sk_stats_t(ctypes.Structure):
     _fields_ = [(name, ctypes.c_int64) for name in
                 ("d", "m", "n", "nnz", "row_offset", "max_col_nnz", "n_items_rad", "n_items_pair",
-                 "philox_blocks_rad", "philox_blocks_pair", "plan_bytes", "n_items_jki", "jki_nonzero_rows", "n_items_f4_split")]
+                 "philox_blocks_rad", "philox_blocks_pair", "plan_bytes", "n_items_jki", "jki_nonzero_rows", "n_items_f4_split",
+                 "n_items_f4", "n_cols_f4", "f4_split_groups")]
 
 
 _lock = threading.Lock()
@@ -84,7 +84,6 @@ def load_library(path: str = LIB_PATH):
         lib.sketch_version.argtypes = []
         lib.sketch_version.restype = ctypes.c_char_p
         lib.sketch_set_rad_f64_path.argtypes = [i32]
-        lib.sketch_set_rad_f32_path.argtypes = [i32]
         lib.sketch_set_pair_path.argtypes = [i32]
         lib.sketch_plan_host_jki.argtypes = [ctypes.POINTER(vp), i32, i64, i64, i64, i64, vp, vp, i64, i32, vp]
         lib.sketch_apply_kernel_name.argtypes = [vp, i32]
@@ -262,17 +261,10 @@ def sketch_fill_s(seed, dist, i0, i1, j0, j1, dtype="f64", device="cuda", stream
 
 
 def set_rad_f64_path(path) -> None:
-    """Select the kernel for ±1 sketches of fp64 values: "fp4" (tensor cores, default),
-    "int8smem", "int8tmem" or "simt" (process-wide)."""
+    """Select the kernel for ±1 sketches of fp64 values in plans built from now on: "fp4" (tensor
+    cores for columns of >= 256 nonzeros, SIMT for the rest; default) or "simt" (process-wide)."""
     p = RAD_F64_PATHS[path] if isinstance(path, str) else int(path)
     _check(load_library().sketch_set_rad_f64_path(p), "sketch_set_rad_f64_path")
-
-
-def set_rad_f32_path(path) -> None:
-    """Select the kernel for ±1 sketches of fp32 values: "simt" (predicated adds, default) or
-    "tab" (subset-sum tables) (process-wide)."""
-    p = RAD_F32_PATHS[path] if isinstance(path, str) else int(path)
-    _check(load_library().sketch_set_rad_f32_path(p), "sketch_set_rad_f32_path")
 
 
 def set_pair_path(path) -> None:

@@ -5,7 +5,7 @@ OUT="$1"; shift
 D=paper_2310_15419_b200/csrc
 T=$(mktemp -d)
 F4FLAGS="${F4FLAGS--Xptxas -O1}"
-for s in sketch_kernels sketch_tc sketch_f4 sketch_f4t sketch_f4n sketch_hybrid sketch_jki sketch_tab sketch_api; do
+for s in sketch_kernels sketch_f4 sketch_jki sketch_api; do
   extra=""; [ "$s" = sketch_f4 ] && extra="$F4FLAGS"
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
     --expt-relaxed-constexpr "$@" $extra -I include -c $D/$s.cu -o $T/$s.o &

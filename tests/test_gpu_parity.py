@@ -163,14 +163,14 @@ def test_sketch_matches_oracle_small(sk, dist, case):
     _check(got, ref, B, TOL["f64"])
 
 
-@pytest.mark.parametrize("path", ["fp4t", "fp4n", "fp4", "int8smem", "int8tmem", "simt", "hybrid"])
+@pytest.mark.parametrize("path", ["fp4", "simt"])
 def test_rad_f64_kernel_paths(sk, path):
-    # every ±1 fp64 kernel (tensor-core fp4n / fp4 / int8-smem / int8-TMEM, SIMT) meets the fp64 bar on
+    # both ±1 fp64 kernel selections (tensor cores + SIMT for short columns, SIMT only) meet the fp64 bar on
     # the edge cases: ragged d and tiles, empty and single-nonzero columns, a column that is long
     # relative to the rest, unsorted rows with duplicates, explicit zeros and huge / tiny values
     try:
         sk.set_rad_f64_path(path)
-        # (averages >= 256 nonzeros per column, so the tensor-core paths are eligible)
+        # (columns of >= 256 nonzeros run on the tensor cores, the others on the SIMT kernel)
         cases = [workloads.random_csc(50000, 40, 300, seed=2),
                  workloads.random_csc(30000, 12, [0, 500, 0, 0, 640, 1, 0, 3300, 0, 2, 0, 100], seed=5),
                  workloads.random_csc(200000, 24, [20000] + [10] * 23, seed=6),
@@ -187,7 +187,7 @@ def test_rad_f64_kernel_paths(sk, path):
         sk.set_rad_f64_path("fp4")
 
 
-@pytest.mark.parametrize("path", ["fp4", "fp4t", "fp4n", "int8smem", "int8tmem", "simt", "hybrid"])
+@pytest.mark.parametrize("path", ["fp4", "simt"])
 def test_nan_poisons_only_its_column(sk, path):
     # a NaN value makes its whole column NaN (NaN * ±1 = NaN in every row, as in the oracle); the
     # other columns are unaffected.  (fmax-based column scans would drop the NaN: the tensor-core
@@ -206,40 +206,78 @@ def test_nan_poisons_only_its_column(sk, path):
         sk.set_rad_f64_path("fp4")
 
 
-@pytest.mark.parametrize("path", ["tab", "simt"])
-def test_rad_f32_kernel_paths(sk, path):
-    # both ±1 fp32 kernels (subset-sum tables, predicated adds) on the edge cases: ragged d and
-    # item tails (d not a multiple of 128 or 2048), empty / single / long columns, chunk tails
-    # (lengths not multiples of 32 or 4), unsorted rows with duplicates, d = 1
+def test_rad_f32_edge_cases(sk):
+    # the ±1 fp32 kernel on the edge cases: ragged d and item tails (d not a multiple of 128 or
+    # 2048), empty / single / long columns, chunk tails (lengths not multiples of 32 or 4),
+    # unsorted rows with duplicates, d = 1
+    f32 = np.float32
+    cases = [(workloads.random_csc(50000, 40, 300, seed=2, dtype=f32), 1000),
+             (workloads.random_csc(30000, 12, [0, 500, 0, 0, 641, 1, 0, 3303, 0, 2, 0, 99], seed=5, dtype=f32), 2100),
+             (workloads.random_csc(5000, 10, 37, seed=7, sorted_rows=False, duplicates=True, dtype=f32), 129),
+             (workloads.random_csc(4000, 7, 45, seed=9, dtype=f32), 1),
+             (workloads.random_csc(200000, 3, [20000, 3, 7], seed=6, dtype=f32), 4097)]
+    for A, d in cases:
+        got = _gpu_sketch(sk, A, d, "rademacher", 13)
+        ref, B = oracle.sketch(13, "rademacher", d, A.m, A.n, A.colptr, A.rowidx, A.vals, threads=8)
+        _check(got, ref, B, TOL["f32"])
+
+
+INF_DISTS = [("rademacher", "f64", "fp4"), ("rademacher", "f64", "simt"), ("rademacher", "f32", "fp4"),
+             ("uniform", "f64", "fp4"), ("gaussian", "f64", "fp4"), ("uniform24", "f32", "fp4"),
+             ("uniform", "f64", "jki"), ("gaussian", "f32", "jki")]
+
+
+@pytest.mark.parametrize("dist,dtype,path", INF_DISTS, ids=["-".join(x) for x in INF_DISTS])
+def test_infinite_values_follow_ieee(sk, dist, dtype, path):
+    # ±Inf values give the IEEE sum on every path (the tensor-core kernel used to write NaN):
+    # column 1 holds one +Inf (every row ±Inf by its S sign), column 3 a +Inf and a -Inf (rows where the
+    # two terms have opposite signs are NaN, the others ±Inf), column 4 an Inf and a NaN (all NaN); the
+    # other columns stay finite and within the parity bar.  Columns are long enough (2100) for the
+    # tensor-core kernel.
+    import torch
+    npdt = np.float32 if dtype == "f32" else np.float64
+    A = workloads.random_csc(60000, 6, 2100, seed=43, dtype=npdt)
+    A.vals[A.colptr[1] + 17] = np.inf
+    A.vals[A.colptr[3] + 5] = np.inf
+    A.vals[A.colptr[3] + 900] = -np.inf
+    A.vals[A.colptr[4] + 3] = -np.inf
+    A.vals[A.colptr[4] + 1000] = np.nan
+    d = 900
     try:
-        sk.set_rad_f32_path(path)
-        f32 = np.float32
-        cases = [(workloads.random_csc(50000, 40, 300, seed=2, dtype=f32), 1000),
-                 (workloads.random_csc(30000, 12, [0, 500, 0, 0, 641, 1, 0, 3303, 0, 2, 0, 99], seed=5, dtype=f32), 2100),
-                 (workloads.random_csc(5000, 10, 37, seed=7, sorted_rows=False, duplicates=True, dtype=f32), 129),
-                 (workloads.random_csc(4000, 7, 45, seed=9, dtype=f32), 1),
-                 (workloads.random_csc(200000, 3, [20000, 3, 7], seed=6, dtype=f32), 4097)]
-        for A, d in cases:
-            got = _gpu_sketch(sk, A, d, "rademacher", 13)
-            ref, B = oracle.sketch(13, "rademacher", d, A.m, A.n, A.colptr, A.rowidx, A.vals, threads=8)
-            _check(got, ref, B, TOL["f32"])
+        if path == "simt":
+            sk.set_rad_f64_path("simt")
+        plan = sk.Plan(_dev(A.colptr), _dev(A.rowidx), d, A.m, dtype, jki=path == "jki")
+        if path == "fp4" and dist == "rademacher" and dtype == "f64":
+            assert plan.stats()["n_cols_f4"] == 6
+        got = plan.apply(_dev(A.vals), 3, dist).T.double().cpu().numpy()
+        torch.cuda.synchronize()
+        plan.close()
     finally:
-        sk.set_rad_f32_path("simt")
+        sk.set_rad_f64_path("fp4")
+    ref, B = oracle.sketch(3, dist, d, A.m, A.n, A.colptr, A.rowidx, A.vals, threads=8)
+    for k in (1, 3, 4):
+        assert np.array_equal(np.isnan(got[:, k]), np.isnan(ref[:, k])), k
+        fin = ~np.isnan(ref[:, k])
+        assert np.all(np.isinf(ref[fin, k])) and np.array_equal(got[fin, k], ref[fin, k]), k
+    assert np.isnan(ref[:, 3]).any() and (~np.isnan(ref[:, 3])).any()
+    keep = [0, 2, 5]
+    _check(got[:, keep], ref[:, keep], B[:, keep], TOL[dtype])
 
 
 def test_f4_last_wave_split_along_k(sk):
-    # 160 one-item columns on 148 SMs: the plan splits the last wave (here every item) into two
-    # K halves that add into zeroed rows.  Results match the oracle, short columns (< 2 K-steps)
-    # stay whole, and two runs are bit-identical (0 + a + b rounds the same in either order).
+    # 160 one-item columns on 148 SMs: the plan splits the last wave (here every tensor-core item)
+    # into two K halves that add exact int64 digit sums; the second half to finish writes Â.  Short
+    # columns go to the SIMT kernel, results match the oracle, and two runs are bit-identical.
     import torch
-    lens = [300] * 160
+    lens = [2100] * 160
     lens[7], lens[50], lens[51] = 40, 127, 129
     A = workloads.random_csc(60000, 160, lens, seed=23)
     plan = sk.Plan(_dev(A.colptr), _dev(A.rowidx), 700, A.m, "f64")
     try:
         st = plan.stats()
+        assert st["n_cols_f4"] == 157 and st["n_items_rad"] > 0
         if torch.cuda.get_device_properties(0).multi_processor_count == 148:
-            assert st["n_items_f4_split"] == 2 * 158
+            assert st["n_items_f4_split"] == 2 * 157 and st["f4_split_groups"] == 157
         assert "sk_rad_f4_kernel" in plan.kernel_name("rademacher")
         vals = _dev(A.vals)
         o1 = plan.apply(vals, 3, "rademacher").T.cpu().numpy()
@@ -249,6 +287,30 @@ def test_f4_last_wave_split_along_k(sk):
         _check(o1, ref, B, TOL["f64"])
     finally:
         plan.close()
+
+
+def test_f4_long_columns_split_along_k(sk):
+    # columns longer than 131071 nonzeros stay on the tensor cores: split along K into parts whose
+    # exact int64 digit sums add in a workspace (PAPER.md:270-283's inner loop over a column, cut into
+    # pieces).  One 300K-nonzero column (3 parts), one of exactly 131072 (2 parts), one of 131071
+    # (whole), plus ordinary columns; the d = 1300 rows make 11 row tiles = 2 tile groups.
+    import torch
+    lens = [300000, 131072, 131071, 3000, 700, 90]
+    A = workloads.random_csc(400000, len(lens), lens, seed=29)
+    plan = sk.Plan(_dev(A.colptr), _dev(A.rowidx), 1300, A.m, "f64")
+    try:
+        st = plan.stats()
+        assert st["n_cols_f4"] == 5, st
+        assert st["f4_split_groups"] >= 4 and st["n_items_f4_split"] >= 10, st
+        vals = _dev(A.vals)
+        o1 = plan.apply(vals, 6, "rademacher").T.cpu().numpy()
+        o2 = plan.apply(vals, 6, "rademacher").T.cpu().numpy()
+        torch.cuda.synchronize()
+        assert np.array_equal(o1, o2)
+    finally:
+        plan.close()
+    ref, B = oracle.sketch(6, "rademacher", 1300, A.m, A.n, A.colptr, A.rowidx, A.vals, threads=16)
+    _check(o1, ref, B, TOL["f64"])
 
 
 @pytest.mark.parametrize("case", range(16))
@@ -301,7 +363,7 @@ def test_repeated_runs_are_bit_identical(sk, dist, dtype):
         plan.close()
 
 
-@pytest.mark.parametrize("path", ["fp4", "fp4t", "fp4n", "int8smem", "simt"])
+@pytest.mark.parametrize("path", ["fp4", "simt"])
 def test_extreme_value_scales(sk, path):
     # columns whose values are all subnormal, all near the top of the fp64 range, or mix both with
     # exact zeros: the tensor-core paths scale each column by 2^(61-E) in two exact factors
@@ -325,24 +387,20 @@ def test_extreme_value_scales(sk, path):
 
 
 def test_kernel_names_report_the_path(sk):
-    A = workloads.random_csc(10000, 4, 300, seed=1)
-    plan = sk.Plan(_dev(A.colptr), _dev(A.rowidx), 300, A.m, "f64")
+    A = workloads.random_csc(10000, 4, 3000, seed=1)
     try:
-        for path, tag in (("fp4t", "S in TMEM"), ("fp4n", "N=256"), ("fp4", "mxf4"), ("int8smem", "smem"), ("int8tmem", "TMEM"), ("simt", "sk_rad_kernel"),
-                          ("hybrid", "hybrid")):
+        for path, tag in (("fp4", "mxf4"), ("simt", "sk_rad_kernel<double>")):
             sk.set_rad_f64_path(path)
+            plan = sk.Plan(_dev(A.colptr), _dev(A.rowidx), 300, A.m, "f64")
             assert tag in plan.kernel_name("rademacher")
-        assert "uniform" in plan.kernel_name("uniform") and "gaussian" in plan.kernel_name("gaussian")
+            assert "uniform" in plan.kernel_name("uniform") and "gaussian" in plan.kernel_name("gaussian")
+            plan.close()
         A32 = workloads.random_csc(10000, 4, 300, seed=1, dtype=np.float32)
         plan32 = sk.Plan(_dev(A32.colptr), _dev(A32.rowidx), 300, A32.m, "f32")
-        for path, tag in (("tab", "sk_rad_tab_kernel"), ("simt", "sk_rad_kernel<float>")):
-            sk.set_rad_f32_path(path)
-            assert tag in plan32.kernel_name("rademacher")
+        assert "sk_rad_kernel<float>" in plan32.kernel_name("rademacher")
         plan32.close()
     finally:
         sk.set_rad_f64_path("fp4")
-        sk.set_rad_f32_path("simt")
-        plan.close()
 
 
 @pytest.mark.parametrize("dist", ["rademacher", "uniform", "gaussian", "uniform24"])

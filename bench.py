@@ -11,6 +11,10 @@ plus, for N > 1, the NCCL all-reduce of the d x n partials (a6).  The plan (a1, 
 "format conversion") is built once and timed separately (plan_ms).
 Rows of A are sharded across ranks (RNG keyed by the global row index), so the total work
 is fixed as N grows ("scaling": "strong") and every rank ends with the same full Â.
+`--gpus N` without torchrun's environment starts the N ranks itself (torch.distributed.run on
+127.0.0.1).  At N = 1 the line also carries `per_config`: c1-c4 timed in the same process with
+their strict roofline fractions (G = ceil(d/E) nnzrows, paper_2310_15419_b200/
+metrics.py roofline()).
 """
 from __future__ import annotations
 
@@ -38,13 +42,6 @@ def _peaks():
             return json.load(f), "measured"
     except Exception:
         return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
-
-
-# FP64 / FP32 vector-pipe peaks derived from unit counts and clocks (DESIGN.md §"Roofline"):
-# 148 SMs x {64 fp64, 128 fp32} lanes x 2 flop per FMA x sm_max clock.
-def alu_peak_tflops(dtype: str, sm_mhz: float) -> float:
-    lanes = 64 if dtype == "f64" else 128
-    return 148 * lanes * 2 * sm_mhz * 1e6 / 1e12
 
 
 class ClockSampler:
@@ -104,12 +101,14 @@ class ClockSampler:
 
 
 def launches_per_apply(plan, dist: str, stats: dict) -> int:
-    """Kernels one sketch_apply launches: the fused kernel, plus the zeroing kernel of the fp4
-    path's K-split last wave when the plan made one."""
-    if not (stats["n_items_rad"] or stats["n_items_pair"]):
-        return 0
-    split = stats.get("n_items_f4_split", 0) > 0 and "sk_rad_f4_kernel" in plan.kernel_name(dist)
-    return 2 if split else 1
+    """Kernels of the library one sketch_apply launches: for ±1, the tensor-core kernel (columns of
+    >= 256 nonzeros, fp64) and the SIMT kernel (the other columns) when each has work; otherwise the
+    one fused kernel of the distribution."""
+    if dist == "rademacher":
+        return int(stats.get("n_items_f4", 0) > 0) + int(stats["n_items_rad"] > 0)
+    if stats.get("n_items_jki", 0) > 0 and "Algorithm 4" in plan.kernel_name(dist):
+        return 1
+    return int(stats["n_items_pair"] > 0)
 
 
 def load_profile_traffic(config: str, kernel: str):
@@ -206,6 +205,95 @@ def run_reference(args):
     return 0
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket() as sck:
+        sck.bind(("127.0.0.1", 0))
+        return sck.getsockname()[1]
+
+
+def relaunch_under_torchrun(n: int) -> int:
+    """`bench.py --gpus N` without a torchrun environment: start the N ranks ourselves (one process
+    per GPU, rendezvous on 127.0.0.1) with the same arguments; rank 0 prints the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
+def nonzero_rows(A) -> int:
+    """nnzrows(A): rows holding at least one stored entry (the strict RNG count's row factor)."""
+    if A.nnz == 0:
+        return 0
+    return int(np.count_nonzero(np.bincount(A.rowidx, minlength=A.m)))
+
+
+def time_applies(torch, plan, vals, seed, dist_name, out, steps, warmup, flush, stream, after=None):
+    """Per-step device times (CUDA events on the launching stream) of plan.apply (+ `after`, e.g. the
+    cross-GPU reduce): returns (apply ms list, step ms list)."""
+    for _ in range(warmup):
+        if flush is not None:
+            flush.zero_()
+        plan.apply(vals, seed, dist_name, out=out)
+        if after:
+            after()
+    torch.cuda.synchronize()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+    for i in range(steps):
+        if flush is not None:
+            flush.zero_()
+        ev[i][0].record(stream)
+        plan.apply(vals, seed, dist_name, out=out)
+        ev[i][1].record(stream)
+        if after:
+            after()
+        ev[i][2].record(stream)
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b, _ in ev], [a.elapsed_time(c) for a, _, c in ev]
+
+
+def per_config_lines(torch, sk, dev, names, steps, warmup, peaks, sm_mhz):
+    """The other BASELINE.json configs, each timed in this process (N = 1): apply ms (median of
+    `steps` after `warmup`, L2 flushed between steps when the inputs fit in L2), GFLOP/s and the
+    strict roofline fraction of SURVEY.md §8(d)."""
+    from paper_2310_15419_b200.metrics import roofline, roofline_report
+    res = {}
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    for name in names:
+        cfg = workloads.CONFIGS[name]
+        A = workloads.make_config(name)
+        colptr = torch.from_numpy(A.colptr).to(dev)
+        rowidx = torch.from_numpy(A.rowidx).to(dev)
+        vals = torch.from_numpy(A.vals).to(dev)
+        out = torch.empty((A.n, cfg.d), dtype=vals.dtype, device=dev)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        plan = sk.Plan(colptr, rowidx, cfg.d, A.m, cfg.dtype)
+        torch.cuda.synchronize()
+        plan_ms = (time.perf_counter() - t0) * 1e3
+        w = 8 if cfg.dtype == "f64" else 4
+        flush = torch.empty(512 * 2**20 // 4, dtype=torch.int32, device=dev) \
+            if algorithmic_bytes(cfg.d, cfg.n, A.nnz, w) < 256 * 2**20 else None
+        k_ms, _ = time_applies(torch, plan, vals, cfg.seed, cfg.dist, out, steps, warmup, flush,
+                               torch.cuda.current_stream())
+        t = statistics.median(k_ms)
+        nzr = nonzero_rows(A)
+        rl = roofline(cfg.dist, cfg.dtype, cfg.d, cfg.n, A.nnz, nzr, hbm, sm_mhz)
+        rep = roofline_report(rl, t / 1e3, cfg.dtype, hbm, sm_mhz)
+        st = plan.stats()
+        res[name] = {"ms": t, "ms_min": min(k_ms), "gflops": gflops(cfg.d, A.nnz, t / 1e3),
+                     "bound": rep["bound"], "frac": rep["frac"], "t_roof_ms": rep["t_roof_ms"],
+                     "achieved": rep["achieved"], "peak": rep["peak"], "unit": rep["unit"],
+                     "kernel": plan.kernel_name(cfg.dist), "dist": cfg.dist, "dtype": cfg.dtype,
+                     "d": cfg.d, "n": cfg.n, "m": cfg.m, "nnz": A.nnz, "nnzrows": nzr,
+                     "g_calls_strict": rl["g_calls_strict"], "g_calls_alg3": rl["g_calls_alg3"],
+                     "plan_ms": plan_ms, "launches_per_step": launches_per_apply(plan, cfg.dist, st),
+                     "l2": "L2 flushed between steps" if flush is not None else "inputs > L2 (no flush)"}
+        plan.close()
+        del flush, colptr, rowidx, vals, out
+        torch.cuda.empty_cache()
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -215,12 +303,15 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-per-config", action="store_true")
     ap.add_argument("--shard", default="rows", choices=["rows", "cols"],
-                    help="rows: row shards + NCCL all_reduce of the d x n partials (default); "
+                    help="rows: row shards + all_reduce of the d x n partials (default); "
                          "cols: nnz-balanced column shards, no collective (SURVEY.md §8(f) f4)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3   # timing rule: >= 3 warm-up steps
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_under_torchrun(args.gpus)
     if args.impl == "reference":
         return run_reference(args)
 
@@ -232,10 +323,21 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    ndev = torch.cuda.device_count()
+    if ndev == 0:
+        raise SystemExit("bench.py needs a CUDA device (there is no CPU fallback)")
+    # One process per GPU over NCCL.  With fewer GPUs than ranks (a functional run on a small box)
+    # the ranks share devices and the partials are summed through gloo (host-staged): such a line
+    # says "shared_gpus": true and is not a scaling measurement.
+    shared = world > ndev
+    torch.cuda.set_device(local % ndev)
+    dev = torch.device("cuda", local % ndev)
+    backend = "gloo" if shared else "nccl"
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
 
     import __graft_entry__
     if rank == 0:
@@ -243,14 +345,15 @@ def main():
     if world > 1:
         dist.barrier()
     from paper_2310_15419_b200 import sketch as sk
+    from paper_2310_15419_b200 import distributed as skd
+    from paper_2310_15419_b200.metrics import roofline, roofline_report
 
     cfg = workloads.CONFIGS[args.config]
     # ---- inputs: this rank's row shard (c5 generates shards independently) or column shard ----
     col_shard = args.shard == "cols" and world > 1
     if col_shard:
-        from paper_2310_15419_b200.distributed import balanced_col_shards
         Af = workloads.make_config(cfg.name)
-        cb = balanced_col_shards(Af.colptr, world)
+        cb = skd.balanced_col_shards(Af.colptr, world)
         A = workloads.col_slice(Af, cb[rank], cb[rank + 1])
         del Af
     elif cfg.name == "c5":
@@ -283,55 +386,36 @@ def main():
     plan_ms = (time.perf_counter() - t0) * 1e3
 
     # L2 policy: inputs larger than the 126 MB L2 need no flush; smaller ones get a flush.
-    in_bytes = algorithmic_bytes(cfg.d, cfg.n, nnz_local, wbytes)
+    in_bytes = algorithmic_bytes(cfg.d, A.n, nnz_local, wbytes)
     flush = None
     if in_bytes < 256 * 2**20:
         flush = torch.empty(512 * 2**20 // 4, dtype=torch.int32, device=dev)
 
-    def step():
-        plan.apply(vals, cfg.seed, cfg.dist, out=out)
-        if reduce_partials:
-            dist.all_reduce(out, op=dist.ReduceOp.SUM)
+    def do_reduce():
+        skd.reduce_partials(out, mode="all_reduce")
+        if shared:
+            torch.cuda.synchronize()     # gloo: host-staged; keep the events honest
 
-    for _ in range(args.warmup):
-        if flush is not None:
-            flush.zero_()
-        step()
-    torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(local % ndev)
     sampler.start()
     time.sleep(0.3)
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    mids = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    for i in range(args.steps):
-        if flush is not None:
-            flush.zero_()
-        starts[i].record(stream)
-        plan.apply(vals, cfg.seed, cfg.dist, out=out)
-        mids[i].record(stream)
-        if reduce_partials:
-            dist.all_reduce(out, op=dist.ReduceOp.SUM)
-        ends[i].record(stream)
-    torch.cuda.synchronize()
+    kern_ms, step_ms = time_applies(torch, plan, vals, cfg.seed, cfg.dist, out, args.steps, args.warmup, flush,
+                                    stream, do_reduce if reduce_partials else None)
     if world > 1:
         dist.barrier()
     clocks = sampler.stop()
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    kern_ms = [s.elapsed_time(m) for s, m in zip(starts, mids)]
     t_step = sum(step_ms) / len(step_ms)
     t_kern = sum(kern_ms) / len(kern_ms)
+    t_red = t_step - t_kern
     if world > 1:
-        tt = torch.tensor([t_step, t_kern], dtype=torch.float64, device=dev)
+        tt = torch.tensor([t_step, t_kern, t_red], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_step, t_kern = float(tt[0]), float(tt[1])
-    if world > 1:
+        t_step, t_kern, t_red = float(tt[0]), float(tt[1]), float(tt[2])
         nn = torch.tensor([nnz_local], dtype=torch.int64, device=dev)
         dist.all_reduce(nn)
         nnz_total = int(nn.item())
@@ -339,62 +423,91 @@ def main():
         nnz_total = nnz_local
     value = gflops(cfg.d, nnz_total, t_step / 1e3)
 
-    # ---- e2e through the host-buffer C-ABI entry point (pinned buffers) ----
+    # ---- e2e through the host-buffer C-ABI entry point (pinned buffers; + the reduce at N > 1) ----
     e2e = None
     if not args.no_e2e:
         h_colptr = torch.from_numpy(A.colptr).pin_memory()
         h_rowidx = torch.from_numpy(A.rowidx).pin_memory()
         h_vals = torch.from_numpy(A.vals).pin_memory()
         h_out = torch.empty((A.n, cfg.d), dtype=vals.dtype).pin_memory()
+
+        def e2e_step():
+            if reduce_partials:
+                skd.sketch_row_sharded_e2e(h_colptr, h_rowidx, h_vals, cfg.d, A.m, A.row_offset, cfg.seed,
+                                           cfg.dist, h_out, work=out)
+            else:
+                sk.sketch_apply_host(cfg.seed, cfg.dist, cfg.d, A.m, h_colptr, h_rowidx, h_vals,
+                                     out=h_out, row_offset=A.row_offset)
         for _ in range(2):
-            sk.sketch_apply_host(cfg.seed, cfg.dist, cfg.d, A.m, h_colptr, h_rowidx, h_vals,
-                                 out=h_out, row_offset=A.row_offset)
-        if world > 1:
-            dist.barrier()
+            e2e_step()
         e_times = []
         for _ in range(max(3, min(args.steps, 5))):
+            if world > 1:
+                dist.barrier()
             t0 = time.perf_counter()
-            sk.sketch_apply_host(cfg.seed, cfg.dist, cfg.d, A.m, h_colptr, h_rowidx, h_vals,
-                                 out=h_out, row_offset=A.row_offset)
+            e2e_step()
             e_times.append(time.perf_counter() - t0)
         te = sum(e_times) / len(e_times)
+        h2d = A.colptr.nbytes + A.rowidx.nbytes + A.vals.nbytes
+        d2h = A.n * cfg.d * wbytes
         if world > 1:
             tt = torch.tensor([te], dtype=torch.float64, device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             te = float(tt[0])
-        h2d = A.colptr.nbytes + A.rowidx.nbytes + A.vals.nbytes
+            bb = torch.tensor([h2d, d2h], dtype=torch.int64, device=dev)
+            dist.all_reduce(bb)
+            h2d, d2h = int(bb[0]), int(bb[1])
         e2e = {"value": gflops(cfg.d, nnz_total, te), "unit": "GFLOP/s",
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(A.n * cfg.d * wbytes),
-               "ms_per_step": te * 1e3,
-               "note": "sketch_apply_host: pinned host A -> device, plan, fused apply, Â -> host; "
-                       "column groups pipelined on copy streams" + ("; no cross-GPU reduce" if world > 1 else "")}
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": te * 1e3,
+               "note": "sketch_apply_host: pinned host A -> device, plan, fused apply, Â -> host; column groups "
+                       "pipelined on copy streams" +
+                       ("; per rank into device memory, then the all_reduce of the partials and Â -> pinned host "
+                        "(bytes summed over ranks; wall clock, max over ranks)" if reduce_partials else "")}
 
-    # ---- roofline of the dominant kernel (the fused apply; one launch per step) ----
+    # ---- roofline of the dominant kernel on this rank (strict G = ceil(d/E) nnzrows) ----
     peaks, peak_src = _peaks()
     sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
-    achieved_tf = 2.0 * cfg.d * nnz_local / (t_kern / 1e3) / 1e12
-    peak_tf = alu_peak_tflops(cfg.dtype, sm_mhz)
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
     stats = plan.stats()
     kname = plan.kernel_name(cfg.dist)
-    roofline = {"bound": "alu", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
-                "frac": achieved_tf / peak_tf, "traffic": load_profile_traffic(cfg.name, kname),
-                "kernel": kname,
-                "peak_source": f"{cfg.dtype} vector pipe (the SpMM's FMA roofline): 148 SMs x "
-                               f"{64 if cfg.dtype == 'f64' else 128} lanes x 2 flop x {sm_mhz:.0f} MHz "
-                               f"(sm_max_mhz of {peak_src} peaks)",
-                "kernel_ms": t_kern,
-                "hbm_frac": (in_bytes / (t_kern / 1e3) / 1e9) / float(peaks.get("hbm_gbs", 6650.0)),
-                "algorithmic_bytes": int(in_bytes)}
+    nzr = nonzero_rows(A)
+    rl = roofline(cfg.dist, cfg.dtype, cfg.d, A.n, nnz_local, nzr, hbm, sm_mhz)
+    rep = roofline_report(rl, t_kern / 1e3, cfg.dtype, hbm, sm_mhz)
+    roof = {"bound": rep["bound"], "achieved": rep["achieved"], "peak": rep["peak"], "unit": rep["unit"],
+            "frac": rep["frac"], "traffic": load_profile_traffic(cfg.name, kname), "kernel": kname,
+            "kernel_ms": t_kern, "t_roof_ms": rep["t_roof_ms"],
+            "peak_source": {"fp64_pipe": f"148 SMs x 64 FP64 lanes x 2 flop x {sm_mhz:.0f} MHz (sm_max_mhz of "
+                                         f"{peak_src} peaks)",
+                            "fp32_pipe": f"148 SMs x 128 FP32 lanes x 2 flop x {sm_mhz:.0f} MHz (sm_max_mhz of "
+                                         f"{peak_src} peaks)",
+                            "int_philox": "Philox4x32-10 blocks/s measured on B200 (profiles/r01_microbench.json)",
+                            "hbm": f"hbm_gbs of {peak_src} peaks"}[rep["bound"]],
+            "model": {"t_hbm_ms": rl["t_hbm"] * 1e3, "t_fp_ms": rl["t_fp"] * 1e3, "t_int_ms": rl["t_int"] * 1e3,
+                      "nnzrows": nzr, "g_calls_strict": rl["g_calls_strict"], "g_calls_alg3": rl["g_calls_alg3"],
+                      "algorithmic_bytes": rl["algorithmic_bytes"]},
+            "hbm_frac": (rl["algorithmic_bytes"] / (t_kern / 1e3) / 1e9) / hbm,
+            "scope": "rank 0's kernel on its shard" if world > 1 else "the whole matrix"}
     if "mxf4" in kname:
-        # the tensor-core path's own ceiling: one M=128,K=64 mxf4 MMA per 92 cycles
-        # (scripts/microbench_mxf4.cu) = 89 (row, nonzero) entries/clk/SM
+        # the tensor-core path's own ceiling: one M=128,K=64 mxf4 MMA per 92 cycles with the A tile
+        # streamed from shared memory (scripts/microbench_mxf4.cu) = 89 (row, nonzero) entries/clk/SM
         tc_peak = 2 * 89.0 * 148 * sm_mhz * 1e6 / 1e12
-        roofline["tensor_feed_peak"] = tc_peak
-        roofline["tensor_feed_frac"] = achieved_tf / tc_peak
+        roof["tensor_feed_peak"] = tc_peak
+        roof["tensor_feed_frac"] = 2.0 * cfg.d * nnz_local / (t_kern / 1e3) / 1e12 / tc_peak
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, A)
+        if world > 1:
+            cpu["sample"] += f" (rank 0's row shard of {world})"
+    per_config = None
+    if rank == 0 and world == 1 and not args.no_per_config:
+        others = [c for c in ("c1", "c2", "c3", "c4", "c5") if c != cfg.name]
+        per_config = per_config_lines(torch, sk, dev, others, max(5, args.steps), args.warmup, peaks, sm_mhz)
+        per_config[cfg.name] = {"ms": t_kern, "gflops": gflops(cfg.d, nnz_local, t_kern / 1e3),
+                                "bound": rep["bound"], "frac": rep["frac"], "t_roof_ms": rep["t_roof_ms"],
+                                "kernel": kname, "nnz": nnz_local, "nnzrows": nzr, "note": "the headline run above"}
+    if world > 1:
+        dist.barrier()
 
     if rank == 0:
         line = {
@@ -407,11 +520,15 @@ def main():
                        "parallelism": f"{'cols' if col_shard else 'rows'}{world}",
                        "l2": "inputs > L2 (no flush)" if flush is None else "L2 flushed between steps",
                        "plan_ms": plan_ms, "plan_first_ms": plan_first_ms, "kernel_ms": t_kern,
-                       "reduce": "NCCL all_reduce of d x n partials" if reduce_partials else None},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                       "reduce": ({"op": "all_reduce (sum of the d x n partials)", "backend": backend,
+                                   "bytes": A.n * cfg.d * wbytes, "ms": t_red,
+                                   "bus_gbs": 2 * (world - 1) / world * A.n * cfg.d * wbytes / (t_red / 1e3) / 1e9
+                                   if t_red > 0 else None} if reduce_partials else None),
+                       "shared_gpus": shared},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "per_config": per_config,
             "clocks": clocks, "gpu_launches": args.steps * launches_per_apply(plan, cfg.dist, stats),
         }
-        print(json.dumps(line))
+        print(json.dumps(line), flush=True)
     plan.close()
     if world > 1:
         dist.destroy_process_group()

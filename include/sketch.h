@@ -133,6 +133,8 @@ int sketch_apply_csc(uint64_t seed, sk_dist_t dist, sk_dtype_t dtype, int64_t d,
  * The column range is processed in `pipeline_chunks` column groups (0 = automatic) so the
  * host->device copy of group g+1 overlaps the kernels of group g and the device->host copy
  * of group g-1.  Device scratch is allocated stream-ordered and freed before returning.
+ * h_out may also be a device pointer (unified addressing): Â then stays on the device, e.g. for
+ * the cross-GPU sum of row-shard partials.
  * Synchronous: returns after h_out is complete.  Errors: as sketch_plan / sketch_apply.
  */
 int sketch_apply_host(uint64_t seed, sk_dist_t dist, sk_dtype_t dtype, int64_t d, int64_t m,

@@ -832,7 +832,7 @@ int sketch_apply_host(uint64_t seed, sk_dist_t dist, sk_dtype_t dtype, int64_t d
     SK_STEP(cudaStreamWaitEvent(d2h, ev_done[g], 0));
     if (c1 > c0)
       SK_STEP(cudaMemcpyAsync((char*)h_out + (size_t)(c0 * d) * w, (char*)d_out + (size_t)(c0 * d) * w,
-                              (size_t)((c1 - c0) * d) * w, cudaMemcpyDeviceToHost, d2h));
+                              (size_t)((c1 - c0) * d) * w, cudaMemcpyDefault, d2h));   // h_out: host or device (UVA)
   }
   SK_STEP(cudaEventRecord(ev_end, d2h));
   tmark(d2h);

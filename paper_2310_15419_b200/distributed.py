@@ -47,6 +47,13 @@ def balanced_row_shards(row_nnz, world: int):
     return b
 
 
+def _host_staged(t, group=None) -> bool:
+    """True when the group's backend cannot run this collective on a CUDA tensor directly (gloo
+    implements only broadcast / all_reduce for CUDA tensors): the call then goes through a host copy."""
+    import torch.distributed as dist
+    return t.is_cuda and dist.get_backend(group) == "gloo"
+
+
 def reduce_partials(out, group=None, mode: str = "all_reduce", dst: int = 0):
     """Â = Σ_g Â_g across the process group (in place).  ``mode`` is "all_reduce" (every
     rank gets Â) or "reduce" (rank ``dst`` only)."""
@@ -56,7 +63,13 @@ def reduce_partials(out, group=None, mode: str = "all_reduce", dst: int = 0):
     if mode == "all_reduce":
         dist.all_reduce(out, op=dist.ReduceOp.SUM, group=group)
     elif mode == "reduce":
-        dist.reduce(out, dst=dst, op=dist.ReduceOp.SUM, group=group)
+        if _host_staged(out, group):
+            h = out.cpu()
+            dist.reduce(h, dst=dst, op=dist.ReduceOp.SUM, group=group)
+            if dist.get_rank(group) == dst:
+                out.copy_(h)
+        else:
+            dist.reduce(out, dst=dst, op=dist.ReduceOp.SUM, group=group)
     else:
         raise ValueError(mode)
     return out
@@ -108,11 +121,12 @@ def gather_col_blocks(block, bounds, group=None):
     d = block.shape[1]
     widths = [bounds[g + 1] - bounds[g] for g in range(world)]
     wmax = max(max(widths), 1)
-    pad = torch.zeros((wmax, d), dtype=block.dtype, device=block.device)
+    staged = _host_staged(block, group)
+    pad = torch.zeros((wmax, d), dtype=block.dtype, device="cpu" if staged else block.device)
     pad[:block.shape[0]].copy_(block)
     outs = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(outs, pad, group=group)
-    return torch.cat([o[:w] for o, w in zip(outs, widths)], dim=0)
+    return torch.cat([o[:w] for o, w in zip(outs, widths)], dim=0).to(block.device)
 
 
 def sketch_col_sharded(colptr_local, rowidx_local, vals_local, d: int, m: int, seed: int, dist_name: str,
@@ -167,3 +181,21 @@ def sketch_row_sharded_overlapped(colptr_h, colptr, rowidx, vals, d: int, m_loca
     for pl in plans:
         pl.close()
     return out
+
+
+def sketch_row_sharded_e2e(h_colptr, h_rowidx, h_vals, d: int, m_local: int, row_offset: int, seed: int,
+                           dist_name: str, out_host, group=None, work=None):
+    """End-to-end row-sharded sketch from HOST buffers (the bench's ``e2e`` leg at N > 1): this rank's
+    shard goes through ``sketch_apply_host`` (pinned host A -> device, plan, fused apply, column groups
+    pipelined on copy streams) into a device buffer, the d x n partials are summed across ranks, and Â
+    comes back into ``out_host`` (pinned, (n, d)).  ``work`` is an optional device (n, d) buffer to reuse.
+    Returns out_host."""
+    import torch
+    from . import sketch as sk
+    n = len(h_colptr) - 1
+    if work is None:
+        work = torch.empty((n, d), dtype=out_host.dtype, device="cuda")
+    sk.sketch_apply_host(seed, dist_name, d, m_local, h_colptr, h_rowidx, h_vals, out=work, row_offset=row_offset)
+    reduce_partials(work, group=group, mode="all_reduce")
+    out_host.copy_(work)
+    return out_host

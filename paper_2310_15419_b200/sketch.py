@@ -227,7 +227,8 @@ def sketch_apply_csc(seed, dist, d, m, colptr, rowidx, vals, out=None, row_offse
 def sketch_apply_host(seed, dist, d, m, colptr, rowidx, vals, out=None, row_offset=0,
                       pipeline_chunks=0, stream=None):
     """End-to-end form with HOST buffers (numpy arrays or CPU tensors, ideally pinned).
-    Returns the (n, d) host array holding Â column-major."""
+    Returns the (n, d) array holding Â column-major: a host array, or ``out`` itself when it is a
+    CUDA tensor (the result then stays on the device, e.g. for a cross-GPU reduction)."""
     def _np(x):
         return x.numpy() if hasattr(x, "numpy") and not isinstance(x, np.ndarray) else np.asarray(x)
     cp, ri, va = _np(colptr), _np(rowidx), _np(vals)
@@ -239,11 +240,19 @@ def sketch_apply_host(seed, dist, d, m, colptr, rowidx, vals, out=None, row_offs
     n = cp.shape[0] - 1
     if out is None:
         out = np.empty((n, int(d)), dtype=va.dtype)
-    o = _np(out)
+    if getattr(out, "is_cuda", False):
+        if tuple(out.shape) != (n, int(d)) or not out.is_contiguous() or out.element_size() != va.itemsize:
+            raise ValueError("out must be a contiguous (n, d) tensor of the values' dtype")
+        optr = out.data_ptr()
+    else:
+        o = _np(out)
+        if o.shape != (n, int(d)) or o.dtype != va.dtype or not o.flags["C_CONTIGUOUS"]:
+            raise ValueError("out must be a contiguous (n, d) array of the values' dtype")
+        optr = o.ctypes.data
     _check(load_library().sketch_apply_host(int(seed) & (2**64 - 1), _dist(dist),
                                             F64 if va.dtype == np.float64 else F32, int(d), int(m),
                                             int(n), int(row_offset), cp.ctypes.data, ri.ctypes.data,
-                                            va.ctypes.data, o.ctypes.data, int(pipeline_chunks),
+                                            va.ctypes.data, optr, int(pipeline_chunks),
                                             _stream_ptr(stream)), "sketch_apply_host")
     return out
 

@@ -101,11 +101,11 @@ class ClockSampler:
 
 
 def launches_per_apply(plan, dist: str, stats: dict) -> int:
-    """Kernels of the library one sketch_apply launches: for ±1, the tensor-core kernel (columns of
-    >= 256 nonzeros, fp64) and the SIMT kernel (the other columns) when each has work; otherwise the
-    one fused kernel of the distribution."""
+    """Kernels of the library one sketch_apply launches: for ±1, the tensor-core kernel's two launches
+    (whole columns; K-split parts + non-finite fix-ups) when columns of >= 256 nonzeros exist (fp64),
+    and the SIMT kernel for the other columns; otherwise the one fused kernel of the distribution."""
     if dist == "rademacher":
-        return int(stats.get("n_items_f4", 0) > 0) + int(stats["n_items_rad"] > 0)
+        return 2 * int(stats.get("n_items_f4", 0) > 0) + int(stats["n_items_rad"] > 0)
     if stats.get("n_items_jki", 0) > 0 and "Algorithm 4" in plan.kernel_name(dist):
         return 1
     return int(stats["n_items_pair"] > 0)

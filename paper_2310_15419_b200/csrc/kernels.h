@@ -68,10 +68,10 @@ __host__ __device__ inline int32_t f4_meta(int ntiles, int part, int nparts) { r
 constexpr int64_t kTcMaxColumn = 131071;
 constexpr int64_t kTcMaxColumnTotal = int64_t(1) << 20;
 
-// n_groups: split groups of the schedule (their int64 workspace is allocated and zeroed
-// stream-ordered by the launcher).
-cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const F4Item* items, int64_t n_items, int64_t n_groups,
-                                cudaStream_t stream);
+// items = [n_main whole-column items | n_split K-split items]; n_groups: split groups (their int64
+// workspace is allocated and zeroed stream-ordered by the launcher).  Two launches (sketch_f4.cu).
+cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const F4Item* items, int64_t n_main, int64_t n_split,
+                                int64_t n_groups, cudaStream_t stream);
 int f4_tiles_per_cta();
 // Algorithm 4 (jki) path for uniform / Gaussian (sketch_jki.cu): column groups of kJCols columns,
 // each stored row by row (CSR of the group); items = (group, tile of jki_rows_per_item() rows).

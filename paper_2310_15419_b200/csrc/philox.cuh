@@ -135,17 +135,32 @@ __device__ __forceinline__ double bm_m2log_u53(double U, const double* __restric
 // sin and cos of th in [0, 2 pi) by table: j = rint(256 th / pi), r = th - j pi/256 (pi/256 in three
 // parts, the first two products exact), |r| <= pi/512, Taylor sin r / cos r to degree 5 / 4, and
 // sin th = S_j cos r + C_j sin r, cos th = C_j cos r - S_j sin r with the correctly rounded
-// S_j, C_j of kBmSinCosTab (513 rows, 8 KB, L1-resident; exact zeros at multiples of pi/2: no
-// cancellation where sin or cos vanishes).  15 FP64 operations + one 16-byte load instead of ~25
-// for the quadrant form below; <= 3.3e-16 relative (scripts/gen_bm_tables.py --check).
-__device__ __forceinline__ void bm_sincos(double th, double& s, double& c) {
+// S_j, C_j of kBmSinCosTab (513 rows; exact zeros at multiples of pi/2: no cancellation where sin
+// or cos vanishes).  15 FP64 operations + one 16-byte load; <= 3.3e-16 relative
+// (scripts/gen_bm_tables.py --check).
+// Table: SCREP = 0 reads kBmSinCosTab through L1 (__ldg); SCREP > 0 reads a shared-memory copy
+// replicated SCREP times, row j copy c at doubles [2 (j SCREP + c), +1], tab = this lane's copy
+// (lane mod SCREP): a quarter-warp's 8 lanes then read 8 different copies -- 128 contiguous bytes,
+// no bank conflict -- where the L1 gather of random rows cost ~8 wavefronts per request.
+constexpr int kScRep = 8;
+constexpr int kScTabRepBytes = (kBmSinCosN + 1) * kScRep * 16;   // 64.1 KB
+
+__device__ __forceinline__ void bm_fill_sctab(double* smem_tab) {
+  for (int i = threadIdx.x; i < (kBmSinCosN + 1) * kScRep * 2; i += blockDim.x)
+    smem_tab[i] = (&kBmSinCosTab[0][0])[2 * (i / (2 * kScRep)) + (i & 1)];
+}
+
+template <int SCREP>
+__device__ __forceinline__ void bm_sincos(double th, double& s, double& c, const double* __restrict__ sctab) {
   const double kr = fma(th, kBm[kSCInv], kBm[kRound]);      // 1.5 2^52 + rint(256 th / pi)
   const double kd = kr - kBm[kRound];
   double r = fma(-kd, kBm[kSCPi_0], th);
   r = fma(-kd, kBm[kSCPi_1], r);
   r = fma(-kd, kBm[kSCPi_2], r);
   const int j = __double2loint(kr) & 0x3FF;                  // 0..512
-  const double2 t = __ldg(reinterpret_cast<const double2*>(&kBmSinCosTab[j][0]));
+  double2 t;
+  if constexpr (SCREP == 0) t = __ldg(reinterpret_cast<const double2*>(&kBmSinCosTab[j][0]));
+  else t = *reinterpret_cast<const double2*>(sctab + 2 * SCREP * j);
   const double z = r * r;
   const double sr = fma(z * r, fma(z, kBm[kT5], kBm[kT3]), r);
   const double cr = fma(z, fma(z, kBm[kU4], kBm[kU2]), 1.0);
@@ -167,17 +182,18 @@ __device__ __forceinline__ double bm_sqrt(double x) {
   return x == 0.0 ? x : s;
 }
 
-// The Box-Muller pair of block x; tab / STRIDE as for bm_m2log_u53.
-template <int STRIDE>
-__device__ __forceinline__ void gaussian_pair_fast(const uint4 x, const double* __restrict__ tab, double& g0, double& g1) {
+// The Box-Muller pair of block x; logtab / STRIDE as for bm_m2log_u53, sctab / SCREP as for bm_sincos.
+template <int STRIDE, int SCREP = 0>
+__device__ __forceinline__ void gaussian_pair_fast(const uint4 x, const double* __restrict__ logtab,
+                                                   const double* __restrict__ sctab, double& g0, double& g1) {
   const unsigned long long k1 = (((unsigned long long)x.x << 32) | x.y) >> 11;
   const unsigned long long k2 = (((unsigned long long)x.z << 32) | x.w) >> 11;
   // u1 = (k1 + 1) 2^-53 and u2 = k2 2^-53 are never formed: -2 log u1 takes the integer with an
   // exponent bias, and th = u2 fl(2 pi) = k2 (2^-53 fl(2 pi)) is the same single rounding.
-  const double rho = bm_sqrt(bm_m2log_u53<STRIDE>(__ull2double_rn(k1 + 1ull), tab));
+  const double rho = bm_sqrt(bm_m2log_u53<STRIDE>(__ull2double_rn(k1 + 1ull), logtab));
   const double th = __dmul_rn(__ull2double_rn(k2), kBm[kTwoPi53]);
   double s, c;
-  bm_sincos(th, s, c);
+  bm_sincos<SCREP>(th, s, c, sctab);
   g0 = __dmul_rn(rho, c);
   g1 = __dmul_rn(rho, s);
 }

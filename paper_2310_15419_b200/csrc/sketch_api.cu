@@ -201,7 +201,8 @@ struct sk_plan_s {
   sk::F4Item* d_f4 = nullptr;       // tensor-core ±1 fp64 schedule (empty unless dtype F64 and path FP4)
   int64_t n_f4 = 0;
   int64_t f4_groups = 0;            // split groups (long columns and the K-split last wave)
-  int64_t f4_split_items = 0;       // items that are parts of a split group
+  int64_t f4_split_items = 0;       // items that are parts of a split group (the last n_f4 - f4_main items)
+  int64_t f4_main = 0;              // whole-column items (first launch)
   int64_t f4_cols = 0;              // columns on the tensor-core kernel (the rest: SIMT items)
   // Algorithm 4 (jki) structure: one device block holding items, grp_rows, row_j, row_ent, ent, ent_base
   void* d_jki = nullptr;
@@ -443,6 +444,14 @@ int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
     if (!tc_cols.empty()) {
       f4 = build_f4_schedule(h_colptr, d, sk::f4_tiles_per_cta(), tc_cols);
       split_f4_tail(f4, h_colptr);
+      // [whole-column items, longest first | K-split parts, longest part first]: the two launches
+      auto whole = [](const sk::F4Item& it) { return sk::f4_nparts(it) == 1; };
+      auto mid = std::stable_partition(f4.items.begin(), f4.items.end(), whole);
+      std::stable_sort(mid, f4.items.end(), [&](const sk::F4Item& a, const sk::F4Item& b) {
+        return (h_colptr[a.col + 1] - h_colptr[a.col]) / sk::f4_nparts(a) >
+               (h_colptr[b.col + 1] - h_colptr[b.col]) / sk::f4_nparts(b);
+      });
+      p->f4_main = (int64_t)(mid - f4.items.begin());
     }
     p->f4_cols = (int64_t)tc_cols.size();
   }
@@ -527,7 +536,7 @@ int apply_items(const sk_plan_s* p, uint64_t seed, sk_dist_t dist, const void* v
   cudaError_t e = cudaSuccess;
   if (dist == SK_RADEMACHER) {
     // tensor-core columns, then the SIMT kernel on the remaining columns (disjoint columns of Â)
-    if (p->n_f4 > 0) e = sk::launch_apply_rad_f4(a, p->d_f4, p->n_f4, p->f4_groups, stream);
+    if (p->n_f4 > 0) e = sk::launch_apply_rad_f4(a, p->d_f4, p->f4_main, p->n_f4 - p->f4_main, p->f4_groups, stream);
     if (e == cudaSuccess) e = sk::launch_apply(0, (int)p->dtype, a, stream);
   } else if ((dist == SK_UNIFORM || dist == SK_GAUSSIAN) && p->jki.n_items > 0 && pair_path() != SK_PAIR_KJI) {
     e = sk::launch_apply_jki((int)dist, (int)p->dtype, a, p->jki, stream);

@@ -184,8 +184,8 @@ __device__ __forceinline__ uint32_t f4_off(int m, int h) {
 // of the infinite terms -- exactly what the oracle's sequential sum gives.  The CTA finds the
 // non-finite values of the whole column, ORs each row's term signs into shared flags, and writes
 // its rows.  (Rare path: one Philox block per (non-finite value, tile).)
-__device__ void f4_nonfinite_column(const ApplyArgs& P, const F4Item& it, int64_t cb, int64_t ce,
-                                    uint32_t* flags /* >= kF4Tiles * 128 + 1 words of smem */) {
+__device__ __forceinline__ void f4_nonfinite_column(const ApplyArgs& P, const F4Item& it, int64_t cb, int64_t ce,
+                                                 uint32_t* flags /* >= kF4Tiles * 128 + 1 words of smem */) {
   const int T = f4_ntiles(it);
   for (int i = threadIdx.x; i <= T * 128; i += blockDim.x) flags[i] = 0u;
   __syncthreads();
@@ -198,9 +198,10 @@ __device__ void f4_nonfinite_column(const ApplyArgs& P, const F4Item& it, int64_
     const uint64_t j = (uint64_t)P.row_offset + (uint32_t)P.rowidx[p];
     for (int tt = 0; tt < T; ++tt) {
       const uint4 x = s_block((uint32_t)(it.tile0 + tt), j, P.keys);
-      const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll 1
       for (int r = 0; r < 128; ++r) {
-        const uint32_t neg = ((w[r >> 5] >> (r & 31)) & 1u) ^ vneg;   // sign of S[i,p] a_p
+        const uint32_t w = r < 64 ? (r < 32 ? x.x : x.y) : (r < 96 ? x.z : x.w);
+        const uint32_t neg = ((w >> (r & 31)) & 1u) ^ vneg;   // sign of S[i,p] a_p
         atomicOr(&flags[tt * 128 + r], neg ? 2u : 1u);
       }
     }
@@ -225,15 +226,36 @@ __device__ void f4_nonfinite_column(const ApplyArgs& P, const F4Item& it, int64_
 #ifndef SK_F4_DEBUG
 #define SK_F4_DEBUG 0
 #endif
-__global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArgs P, const F4Item* items,
+// Two instantiations, launched back to back on the caller's stream:
+//  SPLIT = false: the whole-column items (the bulk).  Epilogue: one fp64 rounding per entry, written
+//    to Â.  A column holding a NaN / Inf is only recorded (item index into nf_list) and skipped.
+//  SPLIT = true: the K-split items (columns longer than kTcMaxColumn, and the last wave halved along K)
+//    -- their parts add exact int64 digit sums into the workspace and the last part to finish converts
+//    -- plus `n_fix` CTAs that write the IEEE result of the non-finite columns recorded by the first
+//    launch.  Keeping the split and non-finite code out of the bulk kernel keeps its schedule (c5:
+//    7.22 ms, against 7.30 ms with all three paths in one kernel; same box, scripts/gpu_ab2.sh).
+template <bool SPLIT>
+__global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArgs P, const F4Item* items, int64_t item0,
+                                                                   int64_t n_items,
                                                                    unsigned long long* __restrict__ ws,
-                                                                   unsigned int* __restrict__ ws_count, int dbg_arg) {
+                                                                   unsigned int* __restrict__ ws_count,
+                                                                   int* __restrict__ nf_list, int dbg_arg) {
   const int dbg = SK_F4_DEBUG ? dbg_arg : 0;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* stages = smem_raw + ((1024u - (s_u32(smem_raw) & 1023u)) & 1023u);
   F4Shared& sh = *reinterpret_cast<F4Shared*>(stages + kF4Stages * kF4Stage);
-  const F4Item it = items[blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (SPLIT && (int64_t)blockIdx.x >= n_items) {
+    // fix-up CTAs: the non-finite columns the bulk launch recorded (nf_list[0] = count, then item indices)
+    const int nfix = nf_list[0];
+    for (int f = (int)(blockIdx.x - n_items); f < nfix; f += (int)(gridDim.x - n_items)) {
+      const F4Item fi = items[nf_list[1 + f]];
+      f4_nonfinite_column(P, fi, P.colptr[fi.col], P.colptr[fi.col + 1], reinterpret_cast<uint32_t*>(stages));
+      __syncthreads();
+    }
+    return;
+  }
+  const F4Item it = items[item0 + blockIdx.x];
   // The column's nonzeros [cb, ce); this item's K range [pb, pe) is part `part` of `nparts` equal
   // shares of its 64-nonzero K-steps (nparts > 1: columns longer than kTcMaxColumn, and the
   // last-wave items split along K).  E is the column-wide exponent so all parts use one scale.
@@ -302,7 +324,11 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
   __syncthreads();
   const int E = sh.E;
   if (sh.nonfinite) {
-    f4_nonfinite_column(P, it, cb, ce, reinterpret_cast<uint32_t*>(stages));
+    if constexpr (SPLIT) {
+      f4_nonfinite_column(P, it, cb, ce, reinterpret_cast<uint32_t*>(stages));
+    } else {
+      if (threadIdx.x == 0) nf_list[1 + atomicAdd(nf_list, 1)] = (int)(item0 + blockIdx.x);
+    }
     __syncthreads();
     if (warp == kF4MmaWarp) {
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -462,7 +488,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
   // (integer atomics: exact, so the order of the parts cannot change a bit), and the last part to
   // finish converts the sums.
   double* outc = reinterpret_cast<double*>(P.out) + (int64_t)it.col * P.ld;
-  unsigned long long* wsg = nparts > 1 ? ws + 2 * (size_t)it.group * (kF4Tiles * 128) : nullptr;
+  unsigned long long* wsg = SPLIT ? ws + 2 * (size_t)it.group * (kF4Tiles * 128) : nullptr;
   if (warp < kF4Producers) {
     if (nsteps > 0) {
       f4_wait(&sh.done, 0);
@@ -493,7 +519,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
       const int r = tt * 128 + 32 * qw + lane;
       const int64_t row = (int64_t)it.tile0 * 128 + r;
       if (row < P.d) {
-        if (wsg) {
+        if constexpr (SPLIT) {
           atomicAdd(wsg + 2 * r, (unsigned long long)hi);
           atomicAdd(wsg + 2 * r + 1, (unsigned long long)(lo - ones));
         } else {
@@ -501,7 +527,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
         }
       }
     }
-    if (wsg) __threadfence();
+    if constexpr (SPLIT) __threadfence();
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   }
   __syncthreads();
@@ -509,7 +535,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(512));
   }
-  if (wsg) {
+  if constexpr (SPLIT) {
     // last part of the split group: convert the int64 sums (its reads see every part's atomics:
     // each part fenced before counting itself in)
     if (threadIdx.x == 0) {
@@ -537,29 +563,39 @@ int f4_tiles_per_cta() {   // SKETCH_F4_TILES (tuning only): fewer row tiles per
   return t;
 }
 
-cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const F4Item* items, int64_t n_items, int64_t n_groups,
-                                cudaStream_t stream) {
-  if (n_items == 0) return cudaSuccess;
+cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const F4Item* items, int64_t n_main, int64_t n_split,
+                                int64_t n_groups, cudaStream_t stream) {
+  if (n_main + n_split == 0) return cudaSuccess;
   const size_t smem = (size_t)kF4Stages * kF4Stage + sizeof(F4Shared) + 1024;
-  cudaError_t e = cudaFuncSetAttribute(sk_rad_f4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
   static const int dbg = [] { const char* v = getenv("SKETCH_F4_DEBUG"); return v ? atoi(v) : 0; }();
-  // split groups: int64 (hi, lo) per row + one arrival counter per group, zeroed stream-ordered
+  // scratch (stream-ordered): split groups' int64 (hi, lo) per row + one arrival counter per group,
+  // then the non-finite record list (count + item indices of the bulk launch)
+  const size_t ws_bytes = (size_t)n_groups * kF4Tiles * 128 * 16, cnt_bytes = ((size_t)n_groups * 4 + 15) & ~(size_t)15;
+  const size_t nf_bytes = (size_t)(n_main + 1) * 4;
   unsigned long long* ws = nullptr;
-  unsigned int* cnt = nullptr;
-  const size_t ws_bytes = (size_t)n_groups * kF4Tiles * 128 * 16, cnt_bytes = (size_t)n_groups * 4;
-  if (n_groups > 0) {
-    e = cudaMallocAsync((void**)&ws, ws_bytes + cnt_bytes, stream);
-    if (e != cudaSuccess) return e;
-    cnt = reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(ws) + ws_bytes);
-    e = cudaMemsetAsync(ws, 0, ws_bytes + cnt_bytes, stream);
+  cudaError_t e = cudaMallocAsync((void**)&ws, ws_bytes + cnt_bytes + nf_bytes, stream);
+  if (e != cudaSuccess) return e;
+  unsigned int* cnt = reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(ws) + ws_bytes);
+  int* nf = reinterpret_cast<int*>(reinterpret_cast<char*>(ws) + ws_bytes + cnt_bytes);
+  e = cudaMemsetAsync(ws, 0, ws_bytes + cnt_bytes + 4, stream);   // workspace, counters, nf count
+  if (e == cudaSuccess && n_main > 0) {
+    e = cudaFuncSetAttribute(sk_rad_f4_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) {
+      sk_rad_f4_kernel<false><<<(unsigned)n_main, kF4Threads, smem, stream>>>(a, items, 0, n_main, ws, cnt, nf, dbg);
+      e = cudaGetLastError();
+    }
   }
   if (e == cudaSuccess) {
-    sk_rad_f4_kernel<<<(unsigned)n_items, kF4Threads, smem, stream>>>(a, items, ws, cnt, dbg);
-    e = cudaGetLastError();
+    constexpr int kFixCtas = 8;   // exit at once when the bulk launch recorded no non-finite column
+    e = cudaFuncSetAttribute(sk_rad_f4_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) {
+      sk_rad_f4_kernel<true><<<(unsigned)(n_split + kFixCtas), kF4Threads, smem, stream>>>(a, items, n_main, n_split, ws,
+                                                                                            cnt, nf, dbg);
+      e = cudaGetLastError();
+    }
   }
-  if (ws) { const cudaError_t e2 = cudaFreeAsync(ws, stream); if (e == cudaSuccess) e = e2; }
-  return e;
+  const cudaError_t e2 = cudaFreeAsync(ws, stream);
+  return e == cudaSuccess ? e2 : e;
 }
 
 }  // namespace sk

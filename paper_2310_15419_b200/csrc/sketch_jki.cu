@@ -37,7 +37,7 @@ __device__ __forceinline__ void jki_entries(const uint4 x, const double* __restr
     else { v0 = __double2float_rn(d0); v1 = __double2float_rn(d1); }
   } else {
     double g0, g1;
-    gaussian_pair_fast<kLogRep>(x, logtab, g0, g1);
+    gaussian_pair_fast<kLogRep, 0>(x, logtab, nullptr, g0, g1);
     if constexpr (sizeof(T) == 8) { v0 = g0; v1 = g1; }
     else { v0 = __double2float_rn(g0); v1 = __double2float_rn(g1); }
   }

@@ -42,31 +42,18 @@ __device__ __forceinline__ T ldg_val(const void* vals, int64_t p) {
 //         2-word FSEL per element.
 //  fp32:  the "T - 2P" form Â = Σ a - 2 Σ_{bit=1} a: one predicated FADD per element
 //         (acc holds P; the lane-uniform column total T is kept separately).
-template <int SELMODE>
 __device__ __forceinline__ void apply_signs(double (&acc)[32], uint32_t w, double a) {
-  if constexpr (SELMODE == 0) {
-    // high word of ±a selected per element (SEL, predicate from R2P), shared low word, DADD
-    const int lo = __double2loint(a), hi = __double2hiint(a), nhi = hi ^ (int)0x80000000;
+  // high word of ±a selected per element (SEL, predicate from R2P), shared low word, DADD
+  const int lo = __double2loint(a), hi = __double2hiint(a), nhi = hi ^ (int)0x80000000;
 #pragma unroll
-    for (int b = 0; b < 32; ++b) {
-      int h;
-      asm("{.reg .pred p; .reg .b32 t; and.b32 t, %1, %4; setp.ne.u32 p, t, 0; selp.b32 %0, %2, %3, p;}"
-          : "=r"(h) : "r"(w), "r"(nhi), "r"(hi), "r"(1u << b));
-      acc[b] += __hiloint2double(h, lo);
-    }
-  } else {
-    // ±1.0 as the register pair (0, h), h = 0xBFF00000 / 0x3FF00000, then one DFMA
-#pragma unroll
-    for (int b = 0; b < 32; ++b) {
-      int h;
-      asm("{.reg .pred p; .reg .b32 t; and.b32 t, %1, %2; setp.ne.u32 p, t, 0; selp.b32 %0, -1074790400, 1072693248, p;}"
-          : "=r"(h) : "r"(w), "r"(1u << b));
-      acc[b] = fma(__hiloint2double(h, 0), a, acc[b]);
-    }
+  for (int b = 0; b < 32; ++b) {
+    int h;
+    asm("{.reg .pred p; .reg .b32 t; and.b32 t, %1, %4; setp.ne.u32 p, t, 0; selp.b32 %0, %2, %3, p;}"
+        : "=r"(h) : "r"(w), "r"(nhi), "r"(hi), "r"(1u << b));
+    acc[b] += __hiloint2double(h, lo);
   }
 }
 
-template <int SELMODE>
 __device__ __forceinline__ void apply_signs(float (&acc)[32], uint32_t w, float a) {
 #pragma unroll
   for (int b = 0; b < 32; ++b)
@@ -88,7 +75,7 @@ __device__ __forceinline__ T finish_sign_sum(T acc, T total) {
 // every lane its own word of all four blocks.  One Philox call per 128 (row, nonzero) pairs.
 // fp32 needs 32 accumulator registers, so two CTAs fit per SM (one CTA's prologue / reduction /
 // store overlaps the other's main loop); fp64 needs 64 and runs one CTA per SM.
-template <typename T, int SELMODE>
+template <typename T>
 __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 2 : 1) sk_rad_kernel(const ApplyArgs P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const Item it = P.items[blockIdx.x];
@@ -107,12 +94,10 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 2 : 1) sk_rad_kerne
 #pragma unroll
   for (int b = 0; b < 32; ++b) acc[b] = T(0);
   T total = T(0);   // fp32 "T - 2P" form only
-  // fp32: non-finite values stay out of T and P (Inf - 2 Inf would be NaN); the signs of the
-  // infinite terms are kept per row as masks in shared memory (+Inf rows, -Inf rows; a NaN sets
-  // both) and applied at the end, so the rows come out as IEEE addition gives them.
-  uint32_t* infm = reinterpret_cast<uint32_t*>(smem + kXchBytes + kWarps * 32 * kRadPad * sizeof(T)) + 2 * threadIdx.x;
-  if constexpr (sizeof(T) == 4) { infm[0] = 0u; infm[1] = 0u; }
-
+  // fp32: a non-finite value makes T and P non-finite (Inf - 2 Inf = NaN even where IEEE gives -Inf).
+  // Then every row of this warp's slice is non-finite anyway and decided by the infinite terms alone,
+  // so the epilogue re-reads the slice's values (cheap, L2-resident) and, only when one is non-finite,
+  // rebuilds the rows from the signs of the infinite terms; the hot loop is untouched.
   for (int64_t p = s0; p < s1; p += 32) {
     const int cnt = (int)((s1 - p) < 32 ? (s1 - p) : 32);
     int32_t jl = 0;
@@ -120,21 +105,6 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 2 : 1) sk_rad_kerne
     if (lane < cnt) {
       jl = __ldg(P.rowidx + p + lane);
       al = ldg_val<T>(P.vals, p + lane);
-    }
-    if constexpr (sizeof(T) == 4) {
-      if (__any_sync(kFull, !isfinite(al))) {   // rare: take the chunk's non-finite values out first
-        if (__any_sync(kFull, isnan(al))) { infm[0] = ~0u; infm[1] = ~0u; }
-        for (unsigned m = __ballot_sync(kFull, isinf(al)); m; m &= m - 1) {
-          const int s = __ffs(m) - 1;
-          const T ai = __shfl_sync(kFull, al, s);
-          const uint32_t jr = (uint32_t)__shfl_sync(kFull, jl, s);
-          const uint4 x = s_block(q, (uint64_t)P.row_offset + jr, P.keys);
-          const uint32_t ww = t == 0 ? x.x : t == 1 ? x.y : t == 2 ? x.z : x.w;   // this lane's 32 rows
-          infm[0] |= ai > T(0) ? ~ww : ww;                                          // S = -1 where the bit is set
-          infm[1] |= ai > T(0) ? ww : ~ww;
-        }
-        if (!isfinite(al)) al = T(0);
-      }
     }
     const int ngroups = (cnt + 3) >> 2;
     for (int u = 0; u < ngroups; ++u) {
@@ -154,7 +124,7 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 2 : 1) sk_rad_kerne
       for (int s = 0; s < 4; ++s) {
         const T a = __shfl_sync(kFull, al, 4 * u + s);   // 0 past cnt: adds ±0
         total += a;
-        apply_signs<SELMODE>(acc, w[s], a);
+        apply_signs(acc, w[s], a);
       }
     }
   }
@@ -162,16 +132,41 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 2 : 1) sk_rad_kerne
   // Fixed-order reduction of the W_k partial tiles, then one coalesced store per row.
   T* red = reinterpret_cast<T*>(smem + kXchBytes);
   T* mine = red + warp * (32 * kRadPad) + lane * kRadPad;
+  if constexpr (sizeof(T) == 4) {
+    bool nonfinite = false;
+    for (int64_t p = s0 + lane; p < s1; p += 32) nonfinite |= !isfinite(ldg_val<T>(P.vals, p));
+    if (__any_sync(kFull, nonfinite)) {   // rare: the infinite terms' signs per row
+      uint32_t pinf = 0u, ninf = 0u;
+      for (int64_t p = s0; p < s1; p += 32) {
+        const T al = p + lane < s1 ? ldg_val<T>(P.vals, p + lane) : T(0);
+        const int32_t jl = p + lane < s1 ? __ldg(P.rowidx + p + lane) : 0;
+        if (__any_sync(kFull, isnan(al))) { pinf = ~0u; ninf = ~0u; }
+        for (unsigned m = __ballot_sync(kFull, isinf(al)); m; m &= m - 1) {
+          const int s = __ffs(m) - 1;
+          const T ai = __shfl_sync(kFull, al, s);
+          const uint32_t jr = (uint32_t)__shfl_sync(kFull, jl, s);
+          const uint4 x = s_block(q, (uint64_t)P.row_offset + jr, P.keys);
+          const uint32_t ww = t == 0 ? x.x : t == 1 ? x.y : t == 2 ? x.z : x.w;   // this lane's 32 rows
+          pinf |= ai > T(0) ? ~ww : ww;                                             // S = -1 where the bit is set
+          ninf |= ai > T(0) ? ww : ~ww;
+        }
+      }
 #pragma unroll
-  for (int b = 0; b < 32; ++b) {
-    T v = finish_sign_sum(acc[b], total);
-    if constexpr (sizeof(T) == 4) {
-      const bool pi = (infm[0] >> b) & 1u, ni = (infm[1] >> b) & 1u;
-      if (pi && ni) v = __int_as_float(0x7FC00000);
-      else if (pi) v = __int_as_float(0x7F800000);
-      else if (ni) v = __int_as_float((int)0xFF800000);
+      for (int b = 0; b < 32; ++b) {
+        const bool pi = (pinf >> b) & 1u, ni = (ninf >> b) & 1u;
+        T v = finish_sign_sum(acc[b], total);
+        if (pi && ni) v = __int_as_float(0x7FC00000);
+        else if (pi) v = __int_as_float(0x7F800000);
+        else if (ni) v = __int_as_float((int)0xFF800000);
+        mine[b] = v;
+      }
+    } else {
+#pragma unroll
+      for (int b = 0; b < 32; ++b) mine[b] = finish_sign_sum(acc[b], total);
     }
-    mine[b] = v;
+  } else {
+#pragma unroll
+    for (int b = 0; b < 32; ++b) mine[b] = finish_sign_sum(acc[b], total);
   }
   __syncthreads();
   T* outc = reinterpret_cast<T*>(P.out) + (int64_t)it.col * P.ld;
@@ -193,27 +188,30 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 2 : 1) sk_rad_kerne
 // q = (warp_row0 + 16 l)/E + h; each block yields E entries (E = 2 for uniform / Gaussian, 4 for
 // uniform24), so a lane generates exactly the S entries it consumes (no exchange).
 template <int DIST> constexpr int pair_E() { return DIST == 3 ? 4 : 2; }
-// logtab / STRIDE: the -2 log table (philox.cuh bm_m2log_u53), Gaussian only.
-template <int DIST, typename T, int STRIDE = kLogRep>
-__device__ __forceinline__ void pair_entries(const uint4 x, T& v0, T& v1, const double* __restrict__ logtab) {
+// logtab / STRIDE: the -2 log table (philox.cuh bm_m2log_u53); sctab / SCREP: the sin / cos table
+// (bm_sincos); Gaussian only.
+template <int DIST, typename T, int STRIDE = kLogRep, int SCREP = kScRep>
+__device__ __forceinline__ void pair_entries(const uint4 x, T& v0, T& v1, const double* __restrict__ logtab,
+                                             const double* __restrict__ sctab = nullptr) {
   if constexpr (DIST == 1) {
     const double d0 = uniform53(x.x, x.y), d1 = uniform53(x.z, x.w);
     if constexpr (sizeof(T) == 8) { v0 = d0; v1 = d1; }
     else { v0 = __double2float_rn(d0); v1 = __double2float_rn(d1); }
   } else {
     double g0, g1;
-    gaussian_pair_fast<STRIDE>(x, logtab, g0, g1);
+    gaussian_pair_fast<STRIDE, SCREP>(x, logtab, sctab, g0, g1);
     if constexpr (sizeof(T) == 8) { v0 = g0; v1 = g1; }
     else { v0 = __double2float_rn(g0); v1 = __double2float_rn(g1); }
   }
 }
 
-template <int DIST, typename T, int STRIDE = kLogRep>
-__device__ __forceinline__ void block_entries(const uint4 x, T (&v)[pair_E<DIST>()], const double* __restrict__ logtab) {
+template <int DIST, typename T, int STRIDE = kLogRep, int SCREP = kScRep>
+__device__ __forceinline__ void block_entries(const uint4 x, T (&v)[pair_E<DIST>()], const double* __restrict__ logtab,
+                                              const double* __restrict__ sctab = nullptr) {
   if constexpr (DIST == 3) {
     v[0] = (T)uniform24(x.x); v[1] = (T)uniform24(x.y); v[2] = (T)uniform24(x.z); v[3] = (T)uniform24(x.w);
   } else {
-    pair_entries<DIST, T, STRIDE>(x, v[0], v[1], logtab);
+    pair_entries<DIST, T, STRIDE, SCREP>(x, v[0], v[1], logtab, sctab);
   }
 }
 
@@ -221,22 +219,13 @@ __device__ __forceinline__ void block_entries(const uint4 x, T (&v)[pair_E<DIST>
 // kRowsPerWarpGauss = 256; fewer live accumulators leave the Box-Muller chains registers:
 // c3 16.1 -> 15.0 ms, while uniform prefers 16: 2.71 vs 2.82 ms on c2).
 template <int DIST> constexpr int pair_rows() { return (DIST == 2 ? kRowsPerWarpGauss : kRowsPerWarpPair) / 32; }
-constexpr int kPairRedBytes = kWarps * 32 * (kRowsPerWarpPair / 32 + 1) * 8;   // reduction area (fp64 worst case)
 
-#ifndef SK_GAUSS_MINB
-#define SK_GAUSS_MINB 1
-#endif
+// One work item of the uniform / Gaussian / uniform24 kernel (the CTA's 16 warps; `red` = the
+// reduction area).  Lane l owns Â rows row0 + 32 kPairRows w_d + kPairRows l + e.
 template <int DIST, typename T>
-__global__ void __launch_bounds__(kThreads, DIST == 2 ? SK_GAUSS_MINB : 1) sk_pair_kernel(const ApplyArgs P) {
+__device__ __forceinline__ void pair_item(const ApplyArgs& P, const Item it, T* red, const double* __restrict__ logtab,
+                                          const double* __restrict__ sctab) {
   constexpr int kPairRows = pair_rows<DIST>(), kPairPad = kPairRows + 1, kRowsPerWarp = 32 * kPairRows;
-  extern __shared__ __align__(16) unsigned char smem[];
-  // Gaussian: the replicated -2 log table; this lane reads copy lane mod kLogRep
-  double* logtab = reinterpret_cast<double*>(smem + kPairRedBytes) + (threadIdx.x & (kLogRep - 1));
-  if constexpr (DIST == 2) {
-    bm_fill_logtab(reinterpret_cast<double*>(smem + kPairRedBytes));
-    __syncthreads();
-  }
-  const Item it = P.items[blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int WD = it.wd, WK = kWarps / WD;              // warps >= WD*WK get an empty slice
   const int wd = warp % WD, wk = warp / WD;
@@ -272,7 +261,7 @@ __global__ void __launch_bounds__(kThreads, DIST == 2 ? SK_GAUSS_MINB : 1) sk_pa
         for (int h = 0; h < kPairRows / 2; ++h) {
           const uint4 x = s_block(q0 + h, J, P.keys);
           T v0, v1;
-          pair_entries<DIST, T>(x, v0, v1, logtab);
+          pair_entries<DIST, T>(x, v0, v1, logtab, sctab);
           acc[2 * h] = fma(v0, a, acc[2 * h]);
           acc[2 * h + 1] = fma(v1, a, acc[2 * h + 1]);
         }
@@ -289,7 +278,6 @@ __global__ void __launch_bounds__(kThreads, DIST == 2 ? SK_GAUSS_MINB : 1) sk_pa
     }
   }
 
-  T* red = reinterpret_cast<T*>(smem);
   T* mine = red + warp * (32 * kPairPad) + lane * kPairPad;
 #pragma unroll
   for (int e = 0; e < kPairRows; ++e) mine[e] = acc[e];
@@ -304,6 +292,36 @@ __global__ void __launch_bounds__(kThreads, DIST == 2 ? SK_GAUSS_MINB : 1) sk_pa
     T s = red[rwd * (32 * kPairPad) + off];
     for (int kk = 1; kk < WK; ++kk) s += red[(kk * WD + rwd) * (32 * kPairPad) + off];
     outc[row] = s;
+  }
+  __syncthreads();   // `red` is reused by the CTA's next item
+}
+
+// Shared memory: reduction area, then (Gaussian) the replicated -2 log and sin / cos tables.
+template <int DIST> constexpr int pair_red_bytes() { return kWarps * 32 * (pair_rows<DIST>() + 1) * 8; }
+template <int DIST> constexpr size_t pair_smem_bytes() {
+  return (size_t)pair_red_bytes<DIST>() + (DIST == 2 ? (size_t)kLogTabRepBytes + kScTabRepBytes : 0);
+}
+
+// Uniform / uniform24: one CTA per item.  Gaussian: persistent, one CTA per SM walking the
+// longest-first item list with stride gridDim.x (a static LPT-like assignment), so the 113 KB of
+// replicated Box-Muller tables are filled once per SM instead of once per item.
+template <int DIST, typename T>
+__global__ void __launch_bounds__(kThreads, 1) sk_pair_kernel(const ApplyArgs P) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  T* red = reinterpret_cast<T*>(smem);
+  const double* logtab = nullptr;
+  const double* sctab = nullptr;
+  if constexpr (DIST == 2) {
+    double* lt = reinterpret_cast<double*>(smem + pair_red_bytes<DIST>());
+    double* st = reinterpret_cast<double*>(smem + pair_red_bytes<DIST>() + kLogTabRepBytes);
+    bm_fill_logtab(lt);
+    bm_fill_sctab(st);
+    __syncthreads();
+    logtab = lt + (threadIdx.x & (kLogRep - 1));        // this lane's copies
+    sctab = st + 2 * (threadIdx.x & (kScRep - 1));
+    for (int64_t i = blockIdx.x; i < P.n_items; i += gridDim.x) pair_item<DIST, T>(P, P.items[i], red, logtab, sctab);
+  } else {
+    pair_item<DIST, T>(P, P.items[blockIdx.x], red, logtab, sctab);
   }
 }
 
@@ -329,7 +347,7 @@ __global__ void sk_fill_s_kernel(PhiloxKeys K, int64_t i0, int64_t i1, int64_t j
     } else {
       constexpr int kE = pair_E<DIST>();
       T v[kE];
-      block_entries<DIST, T, 1>(x, v, &kBmLogTab[0][0]);
+      block_entries<DIST, T, 1, 0>(x, v, &kBmLogTab[0][0]);
 #pragma unroll
       for (int t = 0; t < kE; ++t) {
         const int64_t i = q * kE + t;
@@ -350,38 +368,41 @@ __global__ void sk_validate_rows_kernel(const int32_t* __restrict__ rowidx, int6
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
 }
 
+// grid = one CTA per item, or at most `max_grid` persistent CTAs that stride over the items.
 template <typename K>
-cudaError_t launch_items(K kernel, size_t smem, const ApplyArgs& a, cudaStream_t stream) {
+cudaError_t launch_items(K kernel, size_t smem, const ApplyArgs& a, cudaStream_t stream, int64_t max_grid = 0) {
   if (a.n_items == 0) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kernel<<<(unsigned)a.n_items, kThreads, smem, stream>>>(a);
+  const int64_t grid = max_grid > 0 && a.n_items > max_grid ? max_grid : a.n_items;
+  kernel<<<(unsigned)grid, kThreads, smem, stream>>>(a);
   return cudaGetLastError();
+}
+
+int sm_count() {
+  static const int n = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
 }
 
 }  // namespace
 
 cudaError_t launch_apply(int dist, int dtype, const ApplyArgs& a, cudaStream_t stream) {
   const size_t rad64 = kXchBytes + (size_t)kWarps * 32 * kRadPad * 8;
-  const size_t rad32 = kXchBytes + (size_t)kWarps * 32 * kRadPad * 4 + kThreads * 8;   // + Inf masks
-  const size_t pair64 = (size_t)kPairRedBytes;
-  const size_t pair32 = (size_t)kPairRedBytes;
-  const size_t gauss = (size_t)kPairRedBytes + kLogTabRepBytes;
+  const size_t rad32 = kXchBytes + (size_t)kWarps * 32 * kRadPad * 4;
   if (dist == 0) {
-    if (dtype == 1) return launch_items(sk_rad_kernel<float, 0>, rad32, a, stream);
-    static const int selmode = [] {
-      const char* v = getenv("SKETCH_RAD_SELMODE");   // tuning knob only; results identical
-      return v ? atoi(v) : 0;
-    }();
-    if (selmode == 1) return launch_items(sk_rad_kernel<double, 1>, rad64, a, stream);
-    return launch_items(sk_rad_kernel<double, 0>, rad64, a, stream);
+    if (dtype == 1) return launch_items(sk_rad_kernel<float>, rad32, a, stream);
+    return launch_items(sk_rad_kernel<double>, rad64, a, stream);
   }
-  if (dist == 1) return dtype == 0 ? launch_items(sk_pair_kernel<1, double>, pair64, a, stream)
-                                   : launch_items(sk_pair_kernel<1, float>, pair32, a, stream);
-  if (dist == 3) return dtype == 0 ? launch_items(sk_pair_kernel<3, double>, pair64, a, stream)
-                                   : launch_items(sk_pair_kernel<3, float>, pair32, a, stream);
-  return dtype == 0 ? launch_items(sk_pair_kernel<2, double>, gauss, a, stream)
-                    : launch_items(sk_pair_kernel<2, float>, gauss, a, stream);
+  if (dist == 1) return dtype == 0 ? launch_items(sk_pair_kernel<1, double>, pair_smem_bytes<1>(), a, stream)
+                                   : launch_items(sk_pair_kernel<1, float>, pair_smem_bytes<1>(), a, stream);
+  if (dist == 3) return dtype == 0 ? launch_items(sk_pair_kernel<3, double>, pair_smem_bytes<3>(), a, stream)
+                                   : launch_items(sk_pair_kernel<3, float>, pair_smem_bytes<3>(), a, stream);
+  return dtype == 0 ? launch_items(sk_pair_kernel<2, double>, pair_smem_bytes<2>(), a, stream, sm_count())
+                    : launch_items(sk_pair_kernel<2, float>, pair_smem_bytes<2>(), a, stream, sm_count());
 }
 
 cudaError_t launch_fill_s(int dist, int dtype, uint64_t seed, int64_t i0, int64_t i1, int64_t j0,

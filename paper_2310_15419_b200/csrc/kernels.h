@@ -68,29 +68,53 @@ __host__ __device__ inline int32_t f4_meta(int ntiles, int part, int nparts) { r
 constexpr int64_t kTcMaxColumn = 131071;
 constexpr int64_t kTcMaxColumnTotal = int64_t(1) << 20;
 
-// items = [n_main whole-column items | n_split K-split items]; n_groups: split groups (their int64
-// workspace is allocated and zeroed stream-ordered by the launcher).  Two launches (sketch_f4.cu).
-cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const F4Item* items, int64_t n_main, int64_t n_split,
-                                int64_t n_groups, cudaStream_t stream);
+// n_groups: split groups (their int64 workspace is allocated and zeroed stream-ordered by the
+// launcher).  Launches the tensor-core kernel, the split groups' finishing kernel and the IEEE fix-up
+// of the columns it found non-finite (sketch_f4.cu).
+cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const F4Item* items, int64_t n_items, int64_t n_groups,
+                                cudaStream_t stream);
+// ±1 sketch columns holding a NaN / Inf value get the IEEE result: NaN if a term is NaN or +Inf and -Inf
+// terms meet, else the common sign of the infinite terms (sketch_kernels.cu).  cols = device list
+// {count, column...} of the columns to rewrite; nullptr: scan every column's values (n_cols of them).
+// dtype 0 = f64, 1 = f32.
+cudaError_t launch_rad_ieee_fixup(int dtype, const ApplyArgs& a, const int* cols, cudaStream_t stream,
+                                  int64_t n_cols = 0);
 int f4_tiles_per_cta();
-// Algorithm 4 (jki) path for uniform / Gaussian (sketch_jki.cu): column groups of kJCols columns,
-// each stored row by row (CSR of the group); items = (group, tile of jki_rows_per_item() rows).
-constexpr int kJCols = 16;
+// Algorithm 4 (jki) with full row reuse (sketch_jki.cu): vertical blocks of up to b_n columns, each
+// stored row by row; a work item = (tile of kJRows rows of Â, block, range of the block's batches of
+// up to kJBatch nonzero rows / kJBatchEnt entries).
+constexpr int kJRows = 16;
+constexpr int kJBatch = 128;
+constexpr int kJBatchEnt = 1024;
+constexpr int kJOwners = 32;       // column owners (half-warps): column k of a block -> k mod 32
+struct JBatch {
+  int64_t ent0;        // first entry (in ent)
+  int32_t row0;        // first nonzero row (in row_j)
+  int16_t nrows;       // <= kJBatch
+  int16_t block;       // vertical block
+  int32_t nent;        // <= kJBatchEnt
+  int32_t pad;
+};
 struct JItem {
-  int32_t group;
-  int32_t row0;
+  int32_t tile;        // rows [kJRows tile, +kJRows) of Â
+  int32_t bt0, bt1;    // batches [bt0, bt1) of one block
+  int32_t slot;        // workspace slot (the block's batches are split over several items), -1: write Â
 };
 struct JkiPlanView {
   const JItem* items;
   int64_t n_items;
-  const int64_t* grp_rows;   // [n_groups + 1]: range of the group's nonzero rows in row_j / row_ent
-  const int32_t* row_j;      // local row index of each nonzero row, grouped, ascending within a group
-  const int64_t* row_ent;    // [n_rows + 1]: range of the row's entries in ent
-  const uint32_t* ent;       // (value index - ent_base[group]) << 4 | column within the group
-  const int64_t* ent_base;   // [n_groups]: colptr[16 g]
+  const JBatch* batches;
+  const uint16_t* own;       // [n_batches][kJOwners + 1]: entry ranges of the owners within the batch
+  const int32_t* row_j;      // local row index of each nonzero row of each block
+  const uint2* ent;          // {value index, column within block | row slot within batch << 16}
+  const int32_t* blk_slot;   // [n_blocks + 1]: workspace slots of block b ([s0, s1), empty if unsplit)
   int64_t n;                 // columns of the plan
+  int32_t bn;                // columns per block
+  int32_t n_blocks;
+  int64_t n_slots;           // workspace slots (bn x d each)
 };
-int jki_rows_per_item();
+int jki_block_cols(int dtype);
+size_t jki_smem(int dtype, int bn);
 cudaError_t launch_apply_jki(int dist, int dtype, const ApplyArgs& a, const JkiPlanView& J, cudaStream_t stream);
 
 // dist: 0 = Rademacher, 1 = uniform, 2 = Gaussian; dtype: 0 = f64, 1 = f32.

@@ -201,8 +201,7 @@ struct sk_plan_s {
   sk::F4Item* d_f4 = nullptr;       // tensor-core ±1 fp64 schedule (empty unless dtype F64 and path FP4)
   int64_t n_f4 = 0;
   int64_t f4_groups = 0;            // split groups (long columns and the K-split last wave)
-  int64_t f4_split_items = 0;       // items that are parts of a split group (the last n_f4 - f4_main items)
-  int64_t f4_main = 0;              // whole-column items (first launch)
+  int64_t f4_split_items = 0;       // items that are parts of a split group
   int64_t f4_cols = 0;              // columns on the tensor-core kernel (the rest: SIMT items)
   // Algorithm 4 (jki) structure: one device block holding items, grp_rows, row_j, row_ent, ent, ent_base
   void* d_jki = nullptr;
@@ -219,123 +218,179 @@ struct sk_plan_s {
 
 namespace {
 
-// Group-wise CSR for Algorithm 4 ("A will need to be first partitioned into vertical
-// blocks, and within each block, the entries will be stored in CSR format").  Groups are kJCols
-// consecutive columns.  Unless `force`, a sample of up to 32 groups decides whether the reuse factor
-// (nonzeros per nonzero row) is worth it (>= 1.8); otherwise nothing is built.
+// Algorithm 4 structure ("A will need to be first partitioned into vertical
+// blocks, and within each block, the entries will be stored in CSR format"), the paper's "format
+// conversion".  Blocks are b_n = jki_block_cols(dtype) consecutive
+// columns (all n when n <= b_n: every needed S entry is generated once).  Unless `force`, the exact
+// number of distinct rows per block (device row bitmap) decides whether the RNG saved pays for the
+// scatter: Algorithm 3 generates ceil(d/2) Philox blocks per stored nonzero, Algorithm 4 per nonzero
+// row of a block plus a shared-memory scatter per entry (~kJScatter of a row's generation).
+constexpr double kJScatter = 0.15;
+
 int build_jki(sk_plan_s* p, const int64_t* h_colptr, bool force, cudaStream_t stream) {
-  const int64_t n = p->n, G = (n + sk::kJCols - 1) / sk::kJCols;
-  if (n == 0 || p->nnz == 0) return SK_OK;
+  const int64_t n = p->n, nnz = p->nnz, m = p->m, d = p->d;
+  if (n == 0 || nnz == 0) return SK_OK;
+  auto unsupported = [&](const char* why) -> int {
+    if (!force) return SK_OK;
+    g_detail = why;
+    return (int)SK_EUNSUPPORTED;
+  };
+  if (nnz >= (int64_t(1) << 32) - 1) return unsupported("jki: nnz >= 2^32 (32-bit value indices)");
+  if (m > (int64_t(1) << 27)) return unsupported("jki: m > 2^27 (host row counters)");
+  const int64_t bn = sk::jki_block_cols((int)p->dtype), NB = (n + bn - 1) / bn;
+  if (NB > 32767) return unsupported("jki: more than 32767 column blocks");
   const int64_t base = h_colptr[0];
-  auto group_range = [&](int64_t g) {
-    const int64_t c0 = g * sk::kJCols, c1 = std::min<int64_t>(n, c0 + sk::kJCols);
+  auto block_range = [&](int64_t b) {   // entries of block b, relative to base
+    const int64_t c0 = b * bn, c1 = std::min<int64_t>(n, c0 + bn);
     return std::make_pair(h_colptr[c0] - base, h_colptr[c1] - base);
   };
-  // An entry packs (value index within its group) << 4 | column within the group into 32 bits.
-  for (int64_t g = 0; g < G; ++g) {
-    const auto pr = group_range(g);
-    if (pr.second - pr.first >= (int64_t(1) << 28)) {
-      if (!force) return SK_OK;
-      g_detail = "jki: a 16-column group holds >= 2^28 nonzeros";
-      return SK_EUNSUPPORTED;
+  // (1) exact distinct rows per block on the device: one row bitmap, one pass per block
+  std::vector<unsigned long long> brows((size_t)NB, 0);
+  {
+    const size_t words = (size_t)((m + 31) / 32);
+    uint32_t* bitmap = nullptr;
+    unsigned long long* cnt = nullptr;
+    SK_CUDA(cudaMallocAsync((void**)&bitmap, std::max<size_t>(words, 1) * 4, stream));
+    cudaError_t e = cudaMallocAsync((void**)&cnt, (size_t)NB * 8, stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(cnt, 0, (size_t)NB * 8, stream);
+    for (int64_t b = 0; b < NB && e == cudaSuccess; ++b) {
+      const auto pr = block_range(b);
+      e = cudaMemsetAsync(bitmap, 0, std::max<size_t>(words, 1) * 4, stream);
+      if (e == cudaSuccess) e = sk::launch_distinct_rows(p->rowidx, pr.first, pr.second, bitmap, cnt + b, stream);
     }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(brows.data(), cnt, (size_t)NB * 8, cudaMemcpyDeviceToHost, stream);
+    cudaFreeAsync(bitmap, stream);
+    if (cnt) cudaFreeAsync(cnt, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    if (e != cudaSuccess) return cuda_fail(e, "jki distinct rows");
   }
-  auto distinct_rows = [](std::vector<int32_t>& r) {
-    std::sort(r.begin(), r.end());
-    return (int64_t)(std::unique(r.begin(), r.end()) - r.begin());
-  };
-  if (!force) {
-    // Reuse factor nonzeros / distinct rows on up to 32 evenly spaced groups (<= 16M nonzeros),
-    // counted on the device with a row bitmap (one zeroing + one pass per group, one readback).
-    const int64_t ns = std::min<int64_t>(G, 32);
-    int64_t tot = 0, rows = 0;
-    std::vector<std::pair<int64_t, int64_t>> picked;
-    for (int64_t t = 0; t < ns && tot < (int64_t(1) << 24); ++t) {
-      auto pr = group_range((t * G) / ns);
-      if (pr.second == pr.first) continue;
-      picked.push_back(pr);
-      tot += pr.second - pr.first;
-    }
-    if (picked.empty()) return SK_OK;
-    const size_t words = (size_t)((p->m + 31) / 32);
-    if (p->m <= (int64_t(1) << 28)) {   // bitmap <= 32 MB; taller shards sample on the host
-      uint32_t* bitmap = nullptr;
-      unsigned long long* cnt = nullptr;
-      std::vector<unsigned long long> h_cnt(picked.size(), 0);
-      SK_CUDA(cudaMallocAsync((void**)&bitmap, words * 4, stream));
-      cudaError_t e = cudaMallocAsync((void**)&cnt, picked.size() * 8, stream);
-      if (e == cudaSuccess) e = cudaMemsetAsync(cnt, 0, picked.size() * 8, stream);
-      for (size_t i = 0; i < picked.size() && e == cudaSuccess; ++i) {
-        e = cudaMemsetAsync(bitmap, 0, words * 4, stream);
-        if (e == cudaSuccess) e = sk::launch_distinct_rows(p->rowidx, picked[i].first, picked[i].second, bitmap, cnt + i, stream);
-      }
-      if (e == cudaSuccess) e = cudaMemcpyAsync(h_cnt.data(), cnt, picked.size() * 8, cudaMemcpyDeviceToHost, stream);
-      cudaFreeAsync(bitmap, stream);
-      if (cnt) cudaFreeAsync(cnt, stream);
-      if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
-      if (e != cudaSuccess) return cuda_fail(e, "jki sample");
-      for (auto c : h_cnt) rows += (int64_t)c;
-    } else {
-      tot = 0;
-      for (auto& pr : picked) {
-        if (tot >= (int64_t(1) << 18)) break;
-        std::vector<int32_t> r((size_t)(pr.second - pr.first));
-        SK_CUDA(cudaMemcpyAsync(r.data(), p->rowidx + pr.first, r.size() * 4, cudaMemcpyDeviceToHost, stream));
-        SK_CUDA(cudaStreamSynchronize(stream));
-        tot += (int64_t)r.size();
-        rows += distinct_rows(r);
-      }
-    }
-    if (rows == 0 || (double)tot < 1.8 * (double)rows) return SK_OK;
-  }
-  std::vector<int32_t> h_rows((size_t)p->nnz);
-  SK_CUDA(cudaMemcpyAsync(h_rows.data(), p->rowidx, h_rows.size() * 4, cudaMemcpyDeviceToHost, stream));
+  int64_t rows_total = 0;
+  for (auto r : brows) rows_total += (int64_t)r;
+  if (!force && !((double)rows_total + kJScatter * (double)nnz < 0.9 * (double)nnz)) return SK_OK;
+
+  // (2) host CSR of every block: counting sort by row, stable in storage (= column) order
+  std::vector<int32_t> rows((size_t)nnz);
+  SK_CUDA(cudaMemcpyAsync(rows.data(), p->rowidx, (size_t)nnz * 4, cudaMemcpyDeviceToHost, stream));
   SK_CUDA(cudaStreamSynchronize(stream));
-  std::vector<int64_t> grp_rows{0}, row_ent{0}, ent_base;
-  std::vector<int32_t> row_j;
-  std::vector<uint32_t> ent;
-  std::vector<std::pair<int64_t, sk::JItem>> items;
-  const int rpi = sk::jki_rows_per_item();
-  const int64_t tiles = (p->d + rpi - 1) / rpi;
-  std::vector<std::pair<int64_t, uint32_t>> tmp;   // (row, packed entry)
-  for (int64_t g = 0; g < G; ++g) {
-    auto pr = group_range(g);
-    ent_base.push_back(pr.first + base);
-    tmp.clear();
-    const int64_t c0 = g * sk::kJCols, c1 = std::min<int64_t>(n, c0 + sk::kJCols);
-    for (int64_t c = c0; c < c1; ++c)
-      for (int64_t q = h_colptr[c] - base; q < h_colptr[c + 1] - base; ++q)
-        tmp.emplace_back(h_rows[(size_t)q], (uint32_t)(((q - pr.first) << 4) | (c - c0)));
-    std::stable_sort(tmp.begin(), tmp.end(), [](const std::pair<int64_t, uint32_t>& a,
-                                                 const std::pair<int64_t, uint32_t>& b) { return a.first < b.first; });
-    int64_t nrows = 0;
-    for (size_t e = 0; e < tmp.size(); ++e) {
-      if (e == 0 || tmp[e].first != tmp[e - 1].first) {
-        if (e) row_ent.push_back((int64_t)ent.size());
-        row_j.push_back((int32_t)tmp[e].first);
-        ++nrows;
-      }
-      ent.push_back(tmp[e].second);
+  std::vector<int32_t> cnt((size_t)m, 0), touched, row_j;
+  std::vector<std::pair<uint32_t, uint32_t>> tmp;   // (value index, column within block) in row order
+  std::vector<uint2> ent;
+  ent.reserve((size_t)nnz);
+  std::vector<sk::JBatch> batches;
+  std::vector<uint16_t> own;
+  std::vector<double> bcost;                        // per batch: rows + kJScatter entries
+  std::vector<int64_t> blk_b0{0};                   // batches of block b: [blk_b0[b], blk_b0[b + 1])
+  for (int64_t b = 0; b < NB; ++b) {
+    const int64_t c0 = b * bn, c1 = std::min<int64_t>(n, c0 + bn);
+    touched.clear();
+    for (int64_t q = h_colptr[c0] - base; q < h_colptr[c1] - base; ++q) {
+      const int32_t j = rows[(size_t)q];
+      if (cnt[(size_t)j]++ == 0) touched.push_back(j);
     }
-    if (!tmp.empty()) row_ent.push_back((int64_t)ent.size());
-    grp_rows.push_back((int64_t)row_j.size());
-    p->jki_rows += nrows;
-    const int64_t cost = nrows * 8 + (int64_t)tmp.size();   // a row's RNG ~ 8 nonzeros' FMAs
-    for (int64_t t = 0; t < tiles; ++t) items.push_back({cost, sk::JItem{(int32_t)g, (int32_t)(t * rpi)}});
+    std::sort(touched.begin(), touched.end());
+    int64_t run = 0;
+    for (int32_t j : touched) { const int32_t c = cnt[(size_t)j]; cnt[(size_t)j] = (int32_t)run; run += c; }
+    tmp.assign((size_t)run, {0u, 0u});
+    for (int64_t k = c0; k < c1; ++k)
+      for (int64_t q = h_colptr[k] - base; q < h_colptr[k + 1] - base; ++q)
+        tmp[(size_t)cnt[(size_t)rows[(size_t)q]]++] = {(uint32_t)(q + base), (uint32_t)(k - c0)};
+    // rows in ascending order; a row's entries in [end of previous row, cnt[j]) after the scatter
+    int64_t e0 = 0;
+    sk::JBatch cur{};
+    auto close = [&]() {
+      if (cur.nrows == 0) return;
+      // entries of the batch reordered by owner (column mod kJOwners), stable
+      const size_t first = (size_t)cur.ent0;
+      uint16_t off[sk::kJOwners + 1] = {0};
+      for (int32_t e = 0; e < cur.nent; ++e) ++off[(ent[first + e].y & 0xFFFFu) % sk::kJOwners + 1];
+      for (int h = 0; h < sk::kJOwners; ++h) off[h + 1] = (uint16_t)(off[h + 1] + off[h]);
+      std::vector<uint2> sorted((size_t)cur.nent);
+      uint16_t pos[sk::kJOwners];
+      std::copy(off, off + sk::kJOwners, pos);
+      for (int32_t e = 0; e < cur.nent; ++e) sorted[pos[(ent[first + e].y & 0xFFFFu) % sk::kJOwners]++] = ent[first + e];
+      std::copy(sorted.begin(), sorted.end(), ent.begin() + (int64_t)first);
+      own.insert(own.end(), off, off + sk::kJOwners + 1);
+      bcost.push_back((double)cur.nrows + kJScatter * (double)cur.nent);
+      batches.push_back(cur);
+      cur = sk::JBatch{};
+    };
+    for (int32_t j : touched) {
+      int64_t e1 = cnt[(size_t)j];
+      while (e0 < e1) {   // a row with more than kJBatchEnt entries is cut into several row occurrences
+        const int64_t take = std::min<int64_t>(e1 - e0, sk::kJBatchEnt);
+        if (cur.nrows > 0 && (cur.nrows == sk::kJBatch || cur.nent + take > sk::kJBatchEnt)) close();
+        if (cur.nrows == 0) { cur.ent0 = (int64_t)ent.size(); cur.row0 = (int32_t)row_j.size(); cur.block = (int16_t)b; }
+        for (int64_t e = e0; e < e0 + take; ++e)
+          ent.push_back(make_uint2(tmp[(size_t)e].first, tmp[(size_t)e].second | ((uint32_t)cur.nrows << 16)));
+        row_j.push_back(j);
+        cur.nrows = (int16_t)(cur.nrows + 1);
+        cur.nent += (int32_t)take;
+        e0 += take;
+      }
+    }
+    close();
+    for (int32_t j : touched) cnt[(size_t)j] = 0;
+    blk_b0.push_back((int64_t)batches.size());
   }
-  std::stable_sort(items.begin(), items.end(), [](const std::pair<int64_t, sk::JItem>& a,
-                                                   const std::pair<int64_t, sk::JItem>& b) { return a.first > b.first; });
-  // one device block: items | grp_rows | row_ent | ent_base | row_j | ent
+  if (row_j.size() >= (size_t)INT32_MAX) return unsupported("jki: too many nonzero rows");
+  // (3) work items: T tiles x P_b parts of each block's batches (equal cost), P chosen so the item
+  // count fills whole waves of the SMs (one 200 KB CTA per SM) with >= 4 waves
+  const int64_t T = (d + sk::kJRows - 1) / sk::kJRows;
+  std::vector<double> blk_cost((size_t)NB, 0.0);
+  double tot = 0;
+  for (int64_t b = 0; b < NB; ++b)
+    for (int64_t t = blk_b0[b]; t < blk_b0[b + 1]; ++t) { blk_cost[(size_t)b] += bcost[(size_t)t]; tot += bcost[(size_t)t]; }
+  int W = kSMs, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&W, cudaDevAttrMultiProcessorCount, dev);
+  auto parts_for = [&](int64_t ptot) {
+    std::vector<int64_t> pb((size_t)NB);
+    for (int64_t b = 0; b < NB; ++b) {
+      const int64_t nb = blk_b0[b + 1] - blk_b0[b];
+      const int64_t want = (int64_t)std::llround((double)ptot * blk_cost[(size_t)b] / std::max(tot, 1.0));
+      pb[(size_t)b] = std::max<int64_t>(1, std::min<int64_t>(want, nb));
+    }
+    return pb;
+  };
+  const int64_t pmin = std::max<int64_t>(1, (4 * W + T - 1) / T);
+  std::vector<int64_t> best_pb;
+  double best_eff = -1;
+  for (int64_t ptot = pmin; ptot < pmin + 12; ++ptot) {
+    auto pb = parts_for(ptot);
+    int64_t items = 0;
+    for (auto x : pb) items += T * x;
+    const double eff = (double)items / (double)(((items + W - 1) / W) * W);
+    if (eff > best_eff + 1e-3) { best_eff = eff; best_pb = pb; }
+  }
+  std::vector<sk::JItem> items;
+  std::vector<int32_t> blk_slot{0};
+  int64_t slots = 0;
+  for (int64_t b = 0; b < NB; ++b) {
+    // part boundaries at equal cost (a block may end up with fewer parts than planned)
+    std::vector<int64_t> cut{blk_b0[b]};
+    double acc = 0;
+    const double target = blk_cost[(size_t)b] / (double)best_pb[(size_t)b];
+    for (int64_t t = blk_b0[b]; t < blk_b0[b + 1] && (int64_t)cut.size() < best_pb[(size_t)b]; ++t) {
+      acc += bcost[(size_t)t];
+      if (acc >= target * (double)cut.size() && t + 1 < blk_b0[b + 1]) cut.push_back(t + 1);
+    }
+    cut.push_back(blk_b0[b + 1]);
+    const int64_t P = (int64_t)cut.size() - 1;
+    const int64_t s0 = P > 1 ? slots : -1;
+    if (P > 1) slots += P;
+    blk_slot.push_back((int32_t)slots);
+    for (int64_t pt = 0; pt < P; ++pt)
+      for (int64_t t = 0; t < T; ++t)
+        items.push_back(sk::JItem{(int32_t)t, (int32_t)cut[(size_t)pt], (int32_t)cut[(size_t)pt + 1],
+                                  P > 1 ? (int32_t)(s0 + pt) : -1});
+  }
+  // (4) one device block: items | batches | own | row_j | ent | blk_slot
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
-  const size_t b_items = al(items.size() * sizeof(sk::JItem)), b_grp = al(grp_rows.size() * 8),
-               b_rent = al(row_ent.size() * 8), b_base = al(ent_base.size() * 8), b_rowj = al(row_j.size() * 4),
-               b_ent = al(ent.size() * 4);
+  const size_t b_items = al(items.size() * sizeof(sk::JItem)), b_bat = al(batches.size() * sizeof(sk::JBatch)),
+               b_own = al(own.size() * 2), b_rowj = al(row_j.size() * 4), b_ent = al(ent.size() * 8),
+               b_slot = al(blk_slot.size() * 4);
   char* blk = nullptr;
-  cudaError_t e = cudaMalloc(&blk, b_items + b_grp + b_rent + b_base + b_rowj + b_ent);
+  cudaError_t e = cudaMalloc(&blk, b_items + b_bat + b_own + b_rowj + b_ent + b_slot);
   if (e != cudaSuccess) return e == cudaErrorMemoryAllocation ? SK_ENOMEM : cuda_fail(e, "cudaMalloc(jki)");
-  std::vector<sk::JItem> it2;
-  it2.reserve(items.size());
-  for (auto& pr : items) it2.push_back(pr.second);
   char* c = blk;
   auto put = [&](const void* src, size_t bytes, size_t span) {
     char* dst = c;
@@ -343,17 +398,23 @@ int build_jki(sk_plan_s* p, const int64_t* h_colptr, bool force, cudaStream_t st
     c += span;
     return dst;
   };
-  p->jki.items = reinterpret_cast<const sk::JItem*>(put(it2.data(), it2.size() * sizeof(sk::JItem), b_items));
-  p->jki.grp_rows = reinterpret_cast<const int64_t*>(put(grp_rows.data(), grp_rows.size() * 8, b_grp));
-  p->jki.row_ent = reinterpret_cast<const int64_t*>(put(row_ent.data(), row_ent.size() * 8, b_rent));
-  p->jki.ent_base = reinterpret_cast<const int64_t*>(put(ent_base.data(), ent_base.size() * 8, b_base));
-  p->jki.row_j = reinterpret_cast<const int32_t*>(put(row_j.data(), row_j.size() * 4, b_rowj));
-  p->jki.ent = reinterpret_cast<const uint32_t*>(put(ent.data(), ent.size() * 4, b_ent));
+  sk::JkiPlanView J{};
+  J.items = reinterpret_cast<const sk::JItem*>(put(items.data(), items.size() * sizeof(sk::JItem), b_items));
+  J.batches = reinterpret_cast<const sk::JBatch*>(put(batches.data(), batches.size() * sizeof(sk::JBatch), b_bat));
+  J.own = reinterpret_cast<const uint16_t*>(put(own.data(), own.size() * 2, b_own));
+  J.row_j = reinterpret_cast<const int32_t*>(put(row_j.data(), row_j.size() * 4, b_rowj));
+  J.ent = reinterpret_cast<const uint2*>(put(ent.data(), ent.size() * 8, b_ent));
+  J.blk_slot = reinterpret_cast<const int32_t*>(put(blk_slot.data(), blk_slot.size() * 4, b_slot));
   if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
-  if (e != cudaSuccess) { cudaFree(blk); p->jki = sk::JkiPlanView{}; p->jki_rows = 0; return cuda_fail(e, "upload jki"); }
+  if (e != cudaSuccess) { cudaFree(blk); return cuda_fail(e, "upload jki"); }
+  J.n_items = (int64_t)items.size();
+  J.n = n;
+  J.bn = (int32_t)bn;
+  J.n_blocks = (int32_t)NB;
+  J.n_slots = slots;
   p->d_jki = blk;
-  p->jki.n_items = (int64_t)it2.size();
-  p->jki.n = n;
+  p->jki = J;
+  p->jki_rows = rows_total;
   return SK_OK;
 }
 
@@ -444,14 +505,6 @@ int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
     if (!tc_cols.empty()) {
       f4 = build_f4_schedule(h_colptr, d, sk::f4_tiles_per_cta(), tc_cols);
       split_f4_tail(f4, h_colptr);
-      // [whole-column items, longest first | K-split parts, longest part first]: the two launches
-      auto whole = [](const sk::F4Item& it) { return sk::f4_nparts(it) == 1; };
-      auto mid = std::stable_partition(f4.items.begin(), f4.items.end(), whole);
-      std::stable_sort(mid, f4.items.end(), [&](const sk::F4Item& a, const sk::F4Item& b) {
-        return (h_colptr[a.col + 1] - h_colptr[a.col]) / sk::f4_nparts(a) >
-               (h_colptr[b.col + 1] - h_colptr[b.col]) / sk::f4_nparts(b);
-      });
-      p->f4_main = (int64_t)(mid - f4.items.begin());
     }
     p->f4_cols = (int64_t)tc_cols.size();
   }
@@ -536,8 +589,10 @@ int apply_items(const sk_plan_s* p, uint64_t seed, sk_dist_t dist, const void* v
   cudaError_t e = cudaSuccess;
   if (dist == SK_RADEMACHER) {
     // tensor-core columns, then the SIMT kernel on the remaining columns (disjoint columns of Â)
-    if (p->n_f4 > 0) e = sk::launch_apply_rad_f4(a, p->d_f4, p->f4_main, p->n_f4 - p->f4_main, p->f4_groups, stream);
+    if (p->n_f4 > 0) e = sk::launch_apply_rad_f4(a, p->d_f4, p->n_f4, p->f4_groups, stream);
     if (e == cudaSuccess) e = sk::launch_apply(0, (int)p->dtype, a, stream);
+    // fp32 "T - 2P" sums: columns holding a NaN / Inf rewritten with the IEEE result (a scan of the values)
+    if (e == cudaSuccess && p->dtype == SK_F32 && p->n_rad > 0) e = sk::launch_rad_ieee_fixup(1, a, nullptr, stream, p->n);
   } else if ((dist == SK_UNIFORM || dist == SK_GAUSSIAN) && p->jki.n_items > 0 && pair_path() != SK_PAIR_KJI) {
     e = sk::launch_apply_jki((int)dist, (int)p->dtype, a, p->jki, stream);
   } else {

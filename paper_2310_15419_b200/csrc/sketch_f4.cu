@@ -78,7 +78,6 @@ struct F4Shared {
   unsigned long long maxabs_bits;
   int32_t E;
   int32_t nonfinite;
-  int32_t last;      // this CTA is the last part of its split group to finish
 };
 
 __device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -178,46 +177,6 @@ __device__ __forceinline__ uint32_t f4_off(int m, int h) {
   return (uint32_t)((m >> 3) * 256 + h * 128 + (m & 7) * 16);
 }
 
-// Non-finite column (a NaN or an Inf among its values; the digit encoding needs finite values):
-// every entry of Â[:, k] is then non-finite, so only the non-finite terms S[i,p] a_p decide it, and
-// IEEE addition in ANY order gives NaN if a term is NaN or both +Inf and -Inf occur, else the sign
-// of the infinite terms -- exactly what the oracle's sequential sum gives.  The CTA finds the
-// non-finite values of the whole column, ORs each row's term signs into shared flags, and writes
-// its rows.  (Rare path: one Philox block per (non-finite value, tile).)
-__device__ __forceinline__ void f4_nonfinite_column(const ApplyArgs& P, const F4Item& it, int64_t cb, int64_t ce,
-                                                 uint32_t* flags /* >= kF4Tiles * 128 + 1 words of smem */) {
-  const int T = f4_ntiles(it);
-  for (int i = threadIdx.x; i <= T * 128; i += blockDim.x) flags[i] = 0u;
-  __syncthreads();
-  const double* vals = reinterpret_cast<const double*>(P.vals);
-  for (int64_t p = cb + threadIdx.x; p < ce; p += blockDim.x) {
-    const double v = vals[p];
-    if (isfinite(v)) continue;
-    if (isnan(v)) { atomicOr(&flags[T * 128], 1u); continue; }
-    const uint32_t vneg = signbit(v) ? 1u : 0u;
-    const uint64_t j = (uint64_t)P.row_offset + (uint32_t)P.rowidx[p];
-    for (int tt = 0; tt < T; ++tt) {
-      const uint4 x = s_block((uint32_t)(it.tile0 + tt), j, P.keys);
-#pragma unroll 1
-      for (int r = 0; r < 128; ++r) {
-        const uint32_t w = r < 64 ? (r < 32 ? x.x : x.y) : (r < 96 ? x.z : x.w);
-        const uint32_t neg = ((w >> (r & 31)) & 1u) ^ vneg;   // sign of S[i,p] a_p
-        atomicOr(&flags[tt * 128 + r], neg ? 2u : 1u);
-      }
-    }
-  }
-  __syncthreads();
-  double* outc = reinterpret_cast<double*>(P.out) + (int64_t)it.col * P.ld;
-  const bool anynan = flags[T * 128] != 0u;
-  for (int r = threadIdx.x; r < T * 128; r += blockDim.x) {
-    const int64_t row = (int64_t)it.tile0 * 128 + r;
-    if (row >= P.d) break;
-    const uint32_t f = flags[r];
-    outc[row] = (anynan || f == 3u) ? __longlong_as_double(0x7FF8000000000000ll)
-                                    : (f == 2u ? -INFINITY : INFINITY);
-  }
-}
-
 // dbg (SKETCH_F4_DEBUG; tuning only, results invalid when nonzero), bit flags: 1 = no S stores,
 // 2 = no MMAs, 4 = no proxy fences, 8 = no digit stores, 16 = no column scan, 32 = S warps skip
 // Philox and the transposes, 64 = MMAs with N = 8.
@@ -226,36 +185,22 @@ __device__ __forceinline__ void f4_nonfinite_column(const ApplyArgs& P, const F4
 #ifndef SK_F4_DEBUG
 #define SK_F4_DEBUG 0
 #endif
-// Two instantiations, launched back to back on the caller's stream:
-//  SPLIT = false: the whole-column items (the bulk).  Epilogue: one fp64 rounding per entry, written
-//    to Â.  A column holding a NaN / Inf is only recorded (item index into nf_list) and skipped.
-//  SPLIT = true: the K-split items (columns longer than kTcMaxColumn, and the last wave halved along K)
-//    -- their parts add exact int64 digit sums into the workspace and the last part to finish converts
-//    -- plus `n_fix` CTAs that write the IEEE result of the non-finite columns recorded by the first
-//    launch.  Keeping the split and non-finite code out of the bulk kernel keeps its schedule (c5:
-//    7.22 ms, against 7.30 ms with all three paths in one kernel; same box, scripts/gpu_ab2.sh).
-template <bool SPLIT>
-__global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArgs P, const F4Item* items, int64_t item0,
-                                                                   int64_t n_items,
+// Epilogue per item: whole columns round Σ_s 2^s D_s - D_64 once into Â; the K-split parts (a column
+// longer than kTcMaxColumn, or a last-wave item halved along K) add their exact int64 (hi, lo - ones)
+// into a workspace slot with integer atomics (order-independent: deterministic) and
+// sk_f4_finish_kernel converts the sums after the launch.  A column holding a NaN / Inf (its digit
+// encoding needs finite values) is only recorded in nf_list and left to sk_rad_ieee_fixup_kernel.
+// (Keeping both rare paths out of this kernel keeps the schedule of its producer loops: c5 7.22 ms,
+// against 7.30 ms with them inline; A/B on one box, scripts/gpu_ab2.sh.)
+__global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArgs P, const F4Item* items,
                                                                    unsigned long long* __restrict__ ws,
-                                                                   unsigned int* __restrict__ ws_count,
                                                                    int* __restrict__ nf_list, int dbg_arg) {
   const int dbg = SK_F4_DEBUG ? dbg_arg : 0;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* stages = smem_raw + ((1024u - (s_u32(smem_raw) & 1023u)) & 1023u);
   F4Shared& sh = *reinterpret_cast<F4Shared*>(stages + kF4Stages * kF4Stage);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (SPLIT && (int64_t)blockIdx.x >= n_items) {
-    // fix-up CTAs: the non-finite columns the bulk launch recorded (nf_list[0] = count, then item indices)
-    const int nfix = nf_list[0];
-    for (int f = (int)(blockIdx.x - n_items); f < nfix; f += (int)(gridDim.x - n_items)) {
-      const F4Item fi = items[nf_list[1 + f]];
-      f4_nonfinite_column(P, fi, P.colptr[fi.col], P.colptr[fi.col + 1], reinterpret_cast<uint32_t*>(stages));
-      __syncthreads();
-    }
-    return;
-  }
-  const F4Item it = items[item0 + blockIdx.x];
+  const F4Item it = items[blockIdx.x];
   // The column's nonzeros [cb, ce); this item's K range [pb, pe) is part `part` of `nparts` equal
   // shares of its 64-nonzero K-steps (nparts > 1: columns longer than kTcMaxColumn, and the
   // last-wave items split along K).  E is the column-wide exponent so all parts use one scale.
@@ -324,11 +269,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
   __syncthreads();
   const int E = sh.E;
   if (sh.nonfinite) {
-    if constexpr (SPLIT) {
-      f4_nonfinite_column(P, it, cb, ce, reinterpret_cast<uint32_t*>(stages));
-    } else {
-      if (threadIdx.x == 0) nf_list[1 + atomicAdd(nf_list, 1)] = (int)(item0 + blockIdx.x);
-    }
+    if (threadIdx.x == 0 && part == 0 && it.tile0 == 0) nf_list[1 + atomicAdd(nf_list, 1)] = it.col;
     __syncthreads();
     if (warp == kF4MmaWarp) {
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -484,11 +425,8 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
 
   // ===================== epilogue: warps 0..11 read D (lane quarter = warp % 4) =====================
   // Σ_s 2^s D_s - D_64 = hi 2^32 + (lo - ones): both parts exact int64.  Whole columns round once
-  // into fp64; the parts of a split column add their (hi, lo - ones) into an int64 workspace
-  // (integer atomics: exact, so the order of the parts cannot change a bit), and the last part to
-  // finish converts the sums.
+  // into fp64; the parts of a split column add their (hi, lo - ones) into the int64 workspace.
   double* outc = reinterpret_cast<double*>(P.out) + (int64_t)it.col * P.ld;
-  unsigned long long* wsg = SPLIT ? ws + 2 * (size_t)it.group * (kF4Tiles * 128) : nullptr;
   if (warp < kF4Producers) {
     if (nsteps > 0) {
       f4_wait(&sh.done, 0);
@@ -519,15 +457,15 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
       const int r = tt * 128 + 32 * qw + lane;
       const int64_t row = (int64_t)it.tile0 * 128 + r;
       if (row < P.d) {
-        if constexpr (SPLIT) {
-          atomicAdd(wsg + 2 * r, (unsigned long long)hi);
-          atomicAdd(wsg + 2 * r + 1, (unsigned long long)(lo - ones));
+        if (nparts > 1) {
+          unsigned long long* wsg = ws + 2 * ((size_t)it.group * (kF4Tiles * 128) + r);
+          atomicAdd(wsg, (unsigned long long)hi);
+          atomicAdd(wsg + 1, (unsigned long long)(lo - ones));
         } else {
           outc[row] = scalbn((double)hi * 4294967296.0 + (double)(lo - ones), E - 62);
         }
       }
     }
-    if constexpr (SPLIT) __threadfence();
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   }
   __syncthreads();
@@ -535,23 +473,39 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(512));
   }
-  if constexpr (SPLIT) {
-    // last part of the split group: convert the int64 sums (its reads see every part's atomics:
-    // each part fenced before counting itself in)
-    if (threadIdx.x == 0) {
-      const unsigned int prev = atomicAdd(ws_count + it.group, 1u);
-      sh.last = prev == (unsigned)(nparts - 1);
-      __threadfence();
-    }
-    __syncthreads();
-    if (sh.last) {
-      for (int r = threadIdx.x; r < T * 128; r += blockDim.x) {
-        const int64_t row = (int64_t)it.tile0 * 128 + r;
-        if (row >= P.d) break;
-        const long long hi = (long long)__ldcg(wsg + 2 * r), lo = (long long)__ldcg(wsg + 2 * r + 1);
-        outc[row] = scalbn((double)hi * 4294967296.0 + (double)lo, E - 62);
-      }
-    }
+}
+
+// Split groups: Â rows of group g = 2^(E-62) ((Σ hi) 2^32 + Σ (lo - ones)), one rounding; E is recomputed
+// from the column (the same scan as the kernel's).  One CTA per group.
+__global__ void sk_f4_finish_kernel(const ApplyArgs P, const F4Item* items, int64_t n_items,
+                                    const unsigned long long* __restrict__ ws) {
+  __shared__ unsigned long long mx;
+  __shared__ int E;
+  // the group's first part: items are scanned from the end (the split parts sit in the last wave)
+  const int g = blockIdx.x;
+  F4Item it{};
+  for (int64_t i = n_items - 1; i >= 0; --i)
+    if (f4_nparts(items[i]) > 1 && items[i].group == g) { it = items[i]; break; }
+  if (threadIdx.x == 0) mx = 0ull;
+  __syncthreads();
+  const int64_t cb = P.colptr[it.col], ce = P.colptr[it.col + 1];
+  unsigned long long m = col_absmax_bits(reinterpret_cast<const double*>(P.vals), cb, ce, threadIdx.x, blockDim.x);
+  for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(&mx, m);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int e = 0;
+    frexp(__longlong_as_double((long long)mx), &e);   // non-finite columns are rewritten by the IEEE fix-up
+    E = e;
+  }
+  __syncthreads();
+  double* outc = reinterpret_cast<double*>(P.out) + (int64_t)it.col * P.ld;
+  for (int r = threadIdx.x; r < f4_ntiles(it) * 128; r += blockDim.x) {
+    const int64_t row = (int64_t)it.tile0 * 128 + r;
+    if (row >= P.d) break;
+    const long long hi = (long long)ws[2 * ((size_t)g * (kF4Tiles * 128) + r)];
+    const long long lo = (long long)ws[2 * ((size_t)g * (kF4Tiles * 128) + r) + 1];
+    outc[row] = scalbn((double)hi * 4294967296.0 + (double)lo, E - 62);
   }
 }
 
@@ -563,37 +517,29 @@ int f4_tiles_per_cta() {   // SKETCH_F4_TILES (tuning only): fewer row tiles per
   return t;
 }
 
-cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const F4Item* items, int64_t n_main, int64_t n_split,
-                                int64_t n_groups, cudaStream_t stream) {
-  if (n_main + n_split == 0) return cudaSuccess;
+cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const F4Item* items, int64_t n_items, int64_t n_groups,
+                                cudaStream_t stream) {
+  if (n_items == 0) return cudaSuccess;
   const size_t smem = (size_t)kF4Stages * kF4Stage + sizeof(F4Shared) + 1024;
   static const int dbg = [] { const char* v = getenv("SKETCH_F4_DEBUG"); return v ? atoi(v) : 0; }();
-  // scratch (stream-ordered): split groups' int64 (hi, lo) per row + one arrival counter per group,
-  // then the non-finite record list (count + item indices of the bulk launch)
-  const size_t ws_bytes = (size_t)n_groups * kF4Tiles * 128 * 16, cnt_bytes = ((size_t)n_groups * 4 + 15) & ~(size_t)15;
-  const size_t nf_bytes = (size_t)(n_main + 1) * 4;
+  // scratch (stream-ordered): the split groups' int64 (hi, lo) per row, then the non-finite column
+  // list (count + column indices)
+  const size_t ws_bytes = (size_t)n_groups * kF4Tiles * 128 * 16, nf_bytes = (size_t)(n_items + 1) * 4;
   unsigned long long* ws = nullptr;
-  cudaError_t e = cudaMallocAsync((void**)&ws, ws_bytes + cnt_bytes + nf_bytes, stream);
+  cudaError_t e = cudaMallocAsync((void**)&ws, ws_bytes + nf_bytes, stream);
   if (e != cudaSuccess) return e;
-  unsigned int* cnt = reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(ws) + ws_bytes);
-  int* nf = reinterpret_cast<int*>(reinterpret_cast<char*>(ws) + ws_bytes + cnt_bytes);
-  e = cudaMemsetAsync(ws, 0, ws_bytes + cnt_bytes + 4, stream);   // workspace, counters, nf count
-  if (e == cudaSuccess && n_main > 0) {
-    e = cudaFuncSetAttribute(sk_rad_f4_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess) {
-      sk_rad_f4_kernel<false><<<(unsigned)n_main, kF4Threads, smem, stream>>>(a, items, 0, n_main, ws, cnt, nf, dbg);
-      e = cudaGetLastError();
-    }
-  }
+  int* nf = reinterpret_cast<int*>(reinterpret_cast<char*>(ws) + ws_bytes);
+  e = cudaMemsetAsync(ws, 0, ws_bytes + 4, stream);   // workspace + the list's count
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(sk_rad_f4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess) {
-    constexpr int kFixCtas = 8;   // exit at once when the bulk launch recorded no non-finite column
-    e = cudaFuncSetAttribute(sk_rad_f4_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess) {
-      sk_rad_f4_kernel<true><<<(unsigned)(n_split + kFixCtas), kF4Threads, smem, stream>>>(a, items, n_main, n_split, ws,
-                                                                                            cnt, nf, dbg);
-      e = cudaGetLastError();
-    }
+    sk_rad_f4_kernel<<<(unsigned)n_items, kF4Threads, smem, stream>>>(a, items, ws, nf, dbg);
+    e = cudaGetLastError();
   }
+  if (e == cudaSuccess && n_groups > 0) {
+    sk_f4_finish_kernel<<<(unsigned)n_groups, 256, 0, stream>>>(a, items, n_items, ws);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = launch_rad_ieee_fixup(0, a, nf, stream);
   const cudaError_t e2 = cudaFreeAsync(ws, stream);
   return e == cudaSuccess ? e2 : e;
 }

@@ -1,21 +1,28 @@
-// sketch_jki.cu -- Algorithm 4 ("jki"): one regeneration of S[:, j] per nonzero ROW
-// of a column group, reused for every nonzero of that row in the group (uniform / Gaussian), sm_100a.
+// sketch_jki.cu -- Algorithm 4 ("jki") with full row reuse: S[:, j] is regenerated
+// ONCE per nonzero row j of a vertical block of up to b_n columns (b_n = all n when the block's
+// accumulator fits in shared memory) and applied to every nonzero of that row (uniform / Gaussian),
+// sm_100a.
 //
-// Algorithm 3 (kji, sketch_kernels.cu) regenerates the column S[:, j] for every stored nonzero
-// (j, k); Algorithm 4 walks A_sub row by row in CSR order ("A will need to be
+// The paper's Algorithm 4 walks A row by row inside vertical blocks stored in CSR ("A will need to be
 // first partitioned into vertical blocks, and within each block, the entries will be stored in CSR
-// format") and regenerates S[:, j] once per nonzero row j of the block.  On the GPU:
-//  * vertical block = a group of kJCols = 16 consecutive columns of A; the plan (sketch_api.cu)
-//    builds each group's CSR (distinct rows j, and per row its entries (column in group, index of the
-//    value in the caller's CSC vals)) -- the paper's "format conversion", timed with the plan;
-//  * work item = (group, tile of 1024 Â rows); warp w of the CTA owns rows row0 + 64 w .. + 63, lane l
-//    rows 2l, 2l + 1 of those = the entries of ONE Philox block (q = row / 2);
-//  * every warp walks the group's rows: one Philox block + transform per (row j, lane), then for each
-//    entry (k, p) of row j: acc[k][2 rows] += S·vals[p], the warp's 64 x 16 accumulator tile in shared
-//    memory (lane-contiguous, conflict-free), written to Â once at the end.
-// RNG work is (nonzero rows of the group) x (d / 2) blocks instead of nnz x (d / 2): the reuse factor
-// nnz / nnzrows per group (Abnormal_A of PAPER.md:697-707 -- dense rows -- reuses each block across
-// all 16 columns).  For scattered sparsity the factor is ~1 and the plan keeps Algorithm 3.
+// format") and says to "tune b_n to minimize the number of random variables
+// generated": the RNG work is Σ_blocks nonzero rows x d instead of nnz x d.  With
+// b_n = n every needed entry of S is generated exactly once (the strict count of SURVEY.md §8(d)).
+// On the GPU:
+//  * work item = (tile of kJRows = 16 rows of Â, block, range of the block's row batches): the CTA
+//    keeps the 16 x b_n accumulator of its tile in shared memory (fp64: 128 B per column, b_n <= 1024);
+//  * a batch = up to kJBatch = 128 nonzero rows (<= kJBatchEnt entries).  Stage (all 512 threads):
+//    S[tile rows, j] for the batch's rows -- 1024 Philox blocks, two per thread -- into shared memory,
+//    and the batch's entries (column, row slot) with their values gathered from the caller's CSC vals;
+//  * scatter: half-warp h (32 per CTA) owns the block's columns k = h mod 32 and applies the batch's
+//    entries of its columns in row order, lane i updating row i: acc[k][i] += S[slot][i] a.  Entries
+//    of one column are applied by one half-warp in a fixed order, so results are deterministic;
+//  * batches are double-buffered: the stage of batch b+1 and the scatter of batch b run between the
+//    same pair of barriers (one __syncthreads per batch);
+//  * the tile's accumulator is written to Â once (or, when the block's batches are split over several
+//    items for load balance, to a workspace slot that a finishing kernel sums in a fixed order).
+// The plan (sketch_api.cu) builds the blocks' CSR on the host -- the paper's "format conversion",
+// timed with the plan -- and only when the exact per-block distinct-row count makes it pay.
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -25,9 +32,22 @@
 namespace sk {
 namespace {
 
-constexpr int kJWarps = 16;
-constexpr int kJRowsPerWarp = 64;
-constexpr int kJRows = kJWarps * kJRowsPerWarp;   // Â rows per work item
+constexpr int kJThreads = 512;
+constexpr int kJLogRep = 8;          // replicated -2 log table: 8 copies (24.8 KB)
+constexpr int kJLogBytes = kBmLogRows * 3 * kJLogRep * 8;
+
+template <typename T>
+constexpr size_t jki_smem_bytes(int bn) {
+  return (size_t)bn * kJRows * sizeof(T)                 // accumulator
+         + 2 * (size_t)kJBatch * kJRows * sizeof(T)     // S of two batches
+         + 2 * (size_t)kJBatchEnt * (4 + sizeof(T))     // entries (descriptor, value) of two batches
+         + 2 * 64 * 2                                   // owner offsets of two batches (33 used)
+         + kJLogBytes;
+}
+
+__device__ __forceinline__ void jki_fill_logtab(double* t) {
+  for (int i = threadIdx.x; i < kBmLogRows * 3 * kJLogRep; i += blockDim.x) t[i] = (&kBmLogTab[0][0])[i / kJLogRep];
+}
 
 template <int DIST, typename T>
 __device__ __forceinline__ void jki_entries(const uint4 x, const double* __restrict__ logtab, T& v0, T& v1) {
@@ -37,86 +57,133 @@ __device__ __forceinline__ void jki_entries(const uint4 x, const double* __restr
     else { v0 = __double2float_rn(d0); v1 = __double2float_rn(d1); }
   } else {
     double g0, g1;
-    gaussian_pair_fast<kLogRep, 0>(x, logtab, nullptr, g0, g1);
+    gaussian_pair_fast<kJLogRep, 0>(x, logtab, nullptr, g0, g1);
     if constexpr (sizeof(T) == 8) { v0 = g0; v1 = g1; }
     else { v0 = __double2float_rn(g0); v1 = __double2float_rn(g1); }
   }
 }
 
 template <int DIST, typename T>
-__global__ void __launch_bounds__(kJWarps * 32, 1) sk_jki_kernel(const ApplyArgs P, JkiPlanView J) {
+__global__ void __launch_bounds__(kJThreads, 1) sk_jki_kernel(const ApplyArgs P, const JkiPlanView J, T* __restrict__ ws) {
   extern __shared__ __align__(16) unsigned char smem[];
-  T* acc = reinterpret_cast<T*>(smem);                                    // [warp][k][64 rows]
-  double* logtab_base = reinterpret_cast<double*>(smem + kJWarps * kJCols * kJRowsPerWarp * sizeof(T));
-  const double* logtab = logtab_base + (threadIdx.x & (kLogRep - 1));   // replicated -2 log table
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const JItem it = J.items[blockIdx.x];
-  if constexpr (DIST == 2) {
-    bm_fill_logtab(logtab_base);
-  }
-  T* mine = acc + warp * (kJCols * kJRowsPerWarp);
-#pragma unroll
-  for (int k = 0; k < kJCols; ++k) {
-    mine[k * kJRowsPerWarp + 2 * lane] = T(0);
-    mine[k * kJRowsPerWarp + 2 * lane + 1] = T(0);
-  }
-  __syncthreads();
-  const int64_t row0 = (int64_t)it.row0 + (int64_t)warp * kJRowsPerWarp + 2 * lane;   // this lane's 2 rows
-  const uint32_t q = (uint32_t)(row0 >> 1);
-  const bool active = row0 < P.d;
+  const int blk = J.batches[it.bt0].block;
+  const int64_t c0 = (int64_t)blk * J.bn;
+  const int nbc = (int)min((int64_t)J.bn, J.n - c0);              // columns of this block
+  T* acc = reinterpret_cast<T*>(smem);                             // [nbc][kJRows]
+  T* S = acc + (size_t)J.bn * kJRows;                              // [2][kJBatch][kJRows]
+  uint32_t* edesc = reinterpret_cast<uint32_t*>(S + 2 * kJBatch * kJRows);   // [2][kJBatchEnt]
+  T* evals = reinterpret_cast<T*>(edesc + 2 * kJBatchEnt);         // [2][kJBatchEnt]
+  uint16_t* own = reinterpret_cast<uint16_t*>(evals + 2 * kJBatchEnt);       // [2][64]
+  double* logtab = reinterpret_cast<double*>(own + 2 * 64);
+  const double* mylog = logtab + (threadIdx.x & (kJLogRep - 1));
+  const int tid = threadIdx.x;
   const T* vals = reinterpret_cast<const T*>(P.vals);
-  const int64_t r_beg = J.grp_rows[it.group], r_end = J.grp_rows[it.group + 1];
-  if (active) {
-    for (int64_t r = r_beg; r < r_end; ++r) {
-      const uint64_t j = (uint64_t)P.row_offset + (uint64_t)__ldg(J.row_j + r);
-      const uint4 x = s_block(q, j, P.keys);
-      T v0, v1;
-      jki_entries<DIST, T>(x, logtab, v0, v1);
-      const int64_t e_beg = __ldg(J.row_ent + r), e_end = __ldg(J.row_ent + r + 1);
-      for (int64_t e = e_beg; e < e_end; ++e) {
-        const uint32_t pk = __ldg(J.ent + e);                  // value index (bits 4..31) << 4 | column in group
-        const int k = (int)(pk & (kJCols - 1));
-        const T a = __ldg(vals + J.ent_base[it.group] + (pk >> 4));
-        T* slot = mine + k * kJRowsPerWarp + 2 * lane;        // the lane's 2 rows, one vector access
-        if constexpr (sizeof(T) == 8) {
-          double2 c = *reinterpret_cast<double2*>(slot);
-          c.x = fma(v0, a, c.x);
-          c.y = fma(v1, a, c.y);
-          *reinterpret_cast<double2*>(slot) = c;
-        } else {
-          float2 c = *reinterpret_cast<float2*>(slot);
-          c.x = fmaf(v0, a, c.x);
-          c.y = fmaf(v1, a, c.y);
-          *reinterpret_cast<float2*>(slot) = c;
-        }
+  const uint32_t q0 = (uint32_t)it.tile * (kJRows / 2);            // Philox block of the tile's first row
+
+  for (int e = tid; e < nbc * kJRows; e += kJThreads) acc[e] = T(0);
+  if constexpr (DIST == 2) {
+    jki_fill_logtab(logtab);
+    __syncthreads();
+  }
+
+  // Stage batch bt into buffer b: S of its rows (2 Philox blocks per thread) and its entries.
+  auto stage = [&](int64_t bt, int b) {
+    const JBatch B = J.batches[bt];
+    T* Sb = S + b * (kJBatch * kJRows);
+    const int ql = tid & 7;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int slot = (tid >> 3) + 64 * h;
+      if (slot < B.nrows) {
+        const uint64_t j = (uint64_t)P.row_offset + (uint32_t)__ldg(J.row_j + B.row0 + slot);
+        const uint4 x = s_block(q0 + ql, j, P.keys);
+        T v0, v1;
+        jki_entries<DIST, T>(x, mylog, v0, v1);
+        Sb[slot * kJRows + 2 * ql] = v0;
+        Sb[slot * kJRows + 2 * ql + 1] = v1;
       }
     }
+    for (int e = tid; e < B.nent; e += kJThreads) {
+      const uint2 en = __ldg(J.ent + B.ent0 + e);                  // {value index, k | slot << 16}
+      edesc[b * kJBatchEnt + e] = en.y;
+      evals[b * kJBatchEnt + e] = __ldg(vals + en.x);
+    }
+    if (tid < kJOwners + 1) own[b * 64 + tid] = __ldg(J.own + bt * (kJOwners + 1) + tid);
+  };
+
+  stage(it.bt0, 0);
+  __syncthreads();
+  const int hw = tid >> 4, i = tid & 15;                           // half-warp = column owner, lane = row
+  for (int64_t bt = it.bt0; bt < it.bt1; ++bt) {
+    const int b = (int)((bt - it.bt0) & 1);
+    const T* Sb = S + b * (kJBatch * kJRows);
+    const int e1 = own[b * 64 + hw + 1];
+    for (int e = own[b * 64 + hw]; e < e1; ++e) {
+      const uint32_t dsc = edesc[b * kJBatchEnt + e];
+      const T a = evals[b * kJBatchEnt + e];
+      T* slot = acc + (dsc & 0xFFFFu) * kJRows + i;
+      *slot = fma(Sb[(dsc >> 16) * kJRows + i], a, *slot);
+    }
+    if (bt + 1 < it.bt1) stage(bt + 1, b ^ 1);
+    __syncthreads();
   }
-  __syncwarp();
-  // one coalesced store per column of the group
+
+  // the tile's rows [16 tile, +16) of the block's columns: to Â, or to this item's workspace slot
+  const int64_t row0 = (int64_t)it.tile * kJRows;
+  T* dst = it.slot < 0 ? reinterpret_cast<T*>(P.out) + c0 * P.ld
+                       : ws + (size_t)it.slot * (size_t)J.bn * (size_t)P.d;
+  for (int e = tid; e < nbc * kJRows; e += kJThreads) {
+    const int c = e >> 4, r = e & 15;
+    if (row0 + r < P.d) dst[(int64_t)c * P.d + row0 + r] = acc[e];
+  }
+}
+
+// Blocks whose batches were split over several items: Â = Σ_parts in slot order (deterministic).
+template <typename T>
+__global__ void sk_jki_finish_kernel(const ApplyArgs P, const JkiPlanView J, const T* __restrict__ ws) {
   T* out = reinterpret_cast<T*>(P.out);
-  const int64_t col0 = (int64_t)it.group * kJCols;
-  for (int k = 0; k < kJCols; ++k) {
-    const int64_t col = col0 + k;
-    if (col >= J.n) break;
-    T* outc = out + col * P.ld;
-    if (row0 < P.d) outc[row0] = mine[k * kJRowsPerWarp + 2 * lane];
-    if (row0 + 1 < P.d) outc[row0 + 1] = mine[k * kJRowsPerWarp + 2 * lane + 1];
+  for (int b = 0; b < J.n_blocks; ++b) {
+    const int s0 = J.blk_slot[b], s1 = J.blk_slot[b + 1];
+    if (s1 - s0 < 1) continue;
+    const int64_t c0 = (int64_t)b * J.bn;
+    const int64_t nel = min((int64_t)J.bn, J.n - c0) * P.d;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nel; e += (int64_t)gridDim.x * blockDim.x) {
+      T s = ws[(size_t)s0 * J.bn * P.d + e];
+      for (int sl = s0 + 1; sl < s1; ++sl) s += ws[(size_t)sl * J.bn * P.d + e];
+      out[c0 * P.ld + e] = s;
+    }
   }
 }
 
 template <int DIST, typename T>
 cudaError_t launch_jki_t(const ApplyArgs& a, const JkiPlanView& J, cudaStream_t stream) {
-  const size_t smem = (size_t)kJWarps * kJCols * kJRowsPerWarp * sizeof(T) + (DIST == 2 ? kLogTabRepBytes : 0);
+  const size_t smem = jki_smem_bytes<T>(J.bn);
   cudaError_t e = cudaFuncSetAttribute(sk_jki_kernel<DIST, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  sk_jki_kernel<DIST, T><<<(unsigned)J.n_items, kJWarps * 32, smem, stream>>>(a, J);
-  return cudaGetLastError();
+  T* ws = nullptr;
+  if (J.n_slots > 0) {
+    e = cudaMallocAsync((void**)&ws, (size_t)J.n_slots * J.bn * a.d * sizeof(T), stream);
+    if (e != cudaSuccess) return e;
+  }
+  sk_jki_kernel<DIST, T><<<(unsigned)J.n_items, kJThreads, smem, stream>>>(a, J, ws);
+  e = cudaGetLastError();
+  if (e == cudaSuccess && J.n_slots > 0) {
+    sk_jki_finish_kernel<T><<<148 * 4, 256, 0, stream>>>(a, J, ws);
+    e = cudaGetLastError();
+  }
+  if (ws) { const cudaError_t e2 = cudaFreeAsync(ws, stream); if (e == cudaSuccess) e = e2; }
+  return e;
 }
 
 }  // namespace
 
-int jki_rows_per_item() { return kJRows; }
+int jki_block_cols(int dtype) {
+  // the largest b_n whose accumulator + staging fits the 227 KB of shared memory per CTA
+  return dtype == 0 ? 1024 : 2048;
+}
+
+size_t jki_smem(int dtype, int bn) { return dtype == 0 ? jki_smem_bytes<double>(bn) : jki_smem_bytes<float>(bn); }
 
 cudaError_t launch_apply_jki(int dist, int dtype, const ApplyArgs& a, const JkiPlanView& J, cudaStream_t stream) {
   if (J.n_items == 0) return cudaSuccess;

@@ -94,10 +94,6 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 2 : 1) sk_rad_kerne
 #pragma unroll
   for (int b = 0; b < 32; ++b) acc[b] = T(0);
   T total = T(0);   // fp32 "T - 2P" form only
-  // fp32: a non-finite value makes T and P non-finite (Inf - 2 Inf = NaN even where IEEE gives -Inf).
-  // Then every row of this warp's slice is non-finite anyway and decided by the infinite terms alone,
-  // so the epilogue re-reads the slice's values (cheap, L2-resident) and, only when one is non-finite,
-  // rebuilds the rows from the signs of the infinite terms; the hot loop is untouched.
   for (int64_t p = s0; p < s1; p += 32) {
     const int cnt = (int)((s1 - p) < 32 ? (s1 - p) : 32);
     int32_t jl = 0;
@@ -132,42 +128,8 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 2 : 1) sk_rad_kerne
   // Fixed-order reduction of the W_k partial tiles, then one coalesced store per row.
   T* red = reinterpret_cast<T*>(smem + kXchBytes);
   T* mine = red + warp * (32 * kRadPad) + lane * kRadPad;
-  if constexpr (sizeof(T) == 4) {
-    bool nonfinite = false;
-    for (int64_t p = s0 + lane; p < s1; p += 32) nonfinite |= !isfinite(ldg_val<T>(P.vals, p));
-    if (__any_sync(kFull, nonfinite)) {   // rare: the infinite terms' signs per row
-      uint32_t pinf = 0u, ninf = 0u;
-      for (int64_t p = s0; p < s1; p += 32) {
-        const T al = p + lane < s1 ? ldg_val<T>(P.vals, p + lane) : T(0);
-        const int32_t jl = p + lane < s1 ? __ldg(P.rowidx + p + lane) : 0;
-        if (__any_sync(kFull, isnan(al))) { pinf = ~0u; ninf = ~0u; }
-        for (unsigned m = __ballot_sync(kFull, isinf(al)); m; m &= m - 1) {
-          const int s = __ffs(m) - 1;
-          const T ai = __shfl_sync(kFull, al, s);
-          const uint32_t jr = (uint32_t)__shfl_sync(kFull, jl, s);
-          const uint4 x = s_block(q, (uint64_t)P.row_offset + jr, P.keys);
-          const uint32_t ww = t == 0 ? x.x : t == 1 ? x.y : t == 2 ? x.z : x.w;   // this lane's 32 rows
-          pinf |= ai > T(0) ? ~ww : ww;                                             // S = -1 where the bit is set
-          ninf |= ai > T(0) ? ww : ~ww;
-        }
-      }
 #pragma unroll
-      for (int b = 0; b < 32; ++b) {
-        const bool pi = (pinf >> b) & 1u, ni = (ninf >> b) & 1u;
-        T v = finish_sign_sum(acc[b], total);
-        if (pi && ni) v = __int_as_float(0x7FC00000);
-        else if (pi) v = __int_as_float(0x7F800000);
-        else if (ni) v = __int_as_float((int)0xFF800000);
-        mine[b] = v;
-      }
-    } else {
-#pragma unroll
-      for (int b = 0; b < 32; ++b) mine[b] = finish_sign_sum(acc[b], total);
-    }
-  } else {
-#pragma unroll
-    for (int b = 0; b < 32; ++b) mine[b] = finish_sign_sum(acc[b], total);
-  }
+  for (int b = 0; b < 32; ++b) mine[b] = finish_sign_sum(acc[b], total);
   __syncthreads();
   T* outc = reinterpret_cast<T*>(P.out) + (int64_t)it.col * P.ld;
   const int rows = WD * kRowsPerWarpRad;
@@ -218,6 +180,13 @@ __device__ __forceinline__ void block_entries(const uint4 x, T (&v)[pair_E<DIST>
 // Rows per lane: 16 (uniform, uniform24: kRowsPerWarpPair = 512 per warp) or 8 (Gaussian:
 // kRowsPerWarpGauss = 256; fewer live accumulators leave the Box-Muller chains registers:
 // c3 16.1 -> 15.0 ms, while uniform prefers 16: 2.71 vs 2.82 ms on c2).
+#ifndef SK_GAUSS_SCREP
+#define SK_GAUSS_SCREP kScRep
+#endif
+#ifndef SK_GAUSS_PERSIST
+#define SK_GAUSS_PERSIST 1
+#endif
+constexpr int kGaussScRep = SK_GAUSS_SCREP;
 template <int DIST> constexpr int pair_rows() { return (DIST == 2 ? kRowsPerWarpGauss : kRowsPerWarpPair) / 32; }
 
 // One work item of the uniform / Gaussian / uniform24 kernel (the CTA's 16 warps; `red` = the
@@ -261,7 +230,7 @@ __device__ __forceinline__ void pair_item(const ApplyArgs& P, const Item it, T* 
         for (int h = 0; h < kPairRows / 2; ++h) {
           const uint4 x = s_block(q0 + h, J, P.keys);
           T v0, v1;
-          pair_entries<DIST, T>(x, v0, v1, logtab, sctab);
+          pair_entries<DIST, T, kLogRep, kGaussScRep>(x, v0, v1, logtab, sctab);
           acc[2 * h] = fma(v0, a, acc[2 * h]);
           acc[2 * h + 1] = fma(v1, a, acc[2 * h + 1]);
         }
@@ -299,7 +268,7 @@ __device__ __forceinline__ void pair_item(const ApplyArgs& P, const Item it, T* 
 // Shared memory: reduction area, then (Gaussian) the replicated -2 log and sin / cos tables.
 template <int DIST> constexpr int pair_red_bytes() { return kWarps * 32 * (pair_rows<DIST>() + 1) * 8; }
 template <int DIST> constexpr size_t pair_smem_bytes() {
-  return (size_t)pair_red_bytes<DIST>() + (DIST == 2 ? (size_t)kLogTabRepBytes + kScTabRepBytes : 0);
+  return (size_t)pair_red_bytes<DIST>() + (DIST == 2 ? (size_t)kLogTabRepBytes + (kGaussScRep ? kScTabRepBytes : 0) : 0);
 }
 
 // Uniform / uniform24: one CTA per item.  Gaussian: persistent, one CTA per SM walking the
@@ -315,13 +284,58 @@ __global__ void __launch_bounds__(kThreads, 1) sk_pair_kernel(const ApplyArgs P)
     double* lt = reinterpret_cast<double*>(smem + pair_red_bytes<DIST>());
     double* st = reinterpret_cast<double*>(smem + pair_red_bytes<DIST>() + kLogTabRepBytes);
     bm_fill_logtab(lt);
-    bm_fill_sctab(st);
+    if (kGaussScRep) bm_fill_sctab(st);
     __syncthreads();
     logtab = lt + (threadIdx.x & (kLogRep - 1));        // this lane's copies
     sctab = st + 2 * (threadIdx.x & (kScRep - 1));
     for (int64_t i = blockIdx.x; i < P.n_items; i += gridDim.x) pair_item<DIST, T>(P, P.items[i], red, logtab, sctab);
   } else {
     pair_item<DIST, T>(P, P.items[blockIdx.x], red, logtab, sctab);
+  }
+}
+
+// ------------------------------------------------------------------ IEEE fix-up of non-finite columns
+//
+// A column of A holding a NaN or an Inf makes every entry of its column of Â non-finite, and IEEE
+// addition in ANY order then gives NaN if a term is NaN or both +Inf and -Inf terms occur, else the
+// sign of the infinite terms -- the oracle's sequential sum.  Kernels whose arithmetic does not give
+// that by itself (the tensor-core digits need finite values; the fp32 "T - 2P" form turns Inf - 2 Inf
+// into NaN) leave those columns to this pass: one warp per column, lane = row within a 32-row chunk,
+// one Philox block per (non-finite value, chunk).  Rare path.
+template <typename T>
+__global__ void sk_rad_ieee_fixup_kernel(const ApplyArgs P, const int* __restrict__ cols, int64_t n_cols) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t ncol = cols ? (int64_t)cols[0] : n_cols;
+  const T* vals = reinterpret_cast<const T*>(P.vals);
+  for (int64_t ci = warp0; ci < ncol; ci += nwarps) {
+    const int64_t k = cols ? (int64_t)cols[1 + ci] : ci;
+    const int64_t pb = P.colptr[k], pe = P.colptr[k + 1];
+    bool bad = false;
+    for (int64_t p = pb + lane; p < pe; p += 32) bad |= !isfinite(vals[p]);
+    if (!__any_sync(kFull, bad)) continue;
+    T* outc = reinterpret_cast<T*>(P.out) + k * P.ld;
+    for (int64_t r0 = 0; r0 < P.d; r0 += 32) {
+      const int64_t row = r0 + lane;
+      uint32_t f = 0;                                    // 1: a +Inf term, 2: a -Inf term, 4: a NaN
+      for (int64_t p0 = pb; p0 < pe; p0 += 32) {
+        const T v = p0 + lane < pe ? vals[p0 + lane] : T(0);
+        const int32_t j = p0 + lane < pe ? P.rowidx[p0 + lane] : 0;
+        if (__any_sync(kFull, isnan(v))) f |= 4u;
+        for (unsigned m = __ballot_sync(kFull, isinf(v)); m; m &= m - 1) {
+          const int s = __ffs(m) - 1;
+          const T vi = __shfl_sync(kFull, v, s);
+          const uint32_t jr = (uint32_t)__shfl_sync(kFull, j, s);
+          const uint4 x = s_block((uint32_t)(row >> 7), (uint64_t)P.row_offset + jr, P.keys);
+          const int t = (int)((row >> 5) & 3);
+          const uint32_t w = t == 0 ? x.x : t == 1 ? x.y : t == 2 ? x.z : x.w;
+          const uint32_t neg = ((w >> (row & 31)) & 1u) ^ (vi < T(0) ? 1u : 0u);   // S = -1 where the bit is set
+          f |= neg ? 2u : 1u;
+        }
+      }
+      if (row < P.d)
+        outc[row] = (f & 4u) || f == 3u ? T(NAN) : (f == 1u ? T(INFINITY) : T(-INFINITY));
+    }
   }
 }
 
@@ -394,15 +408,22 @@ cudaError_t launch_apply(int dist, int dtype, const ApplyArgs& a, cudaStream_t s
   const size_t rad64 = kXchBytes + (size_t)kWarps * 32 * kRadPad * 8;
   const size_t rad32 = kXchBytes + (size_t)kWarps * 32 * kRadPad * 4;
   if (dist == 0) {
-    if (dtype == 1) return launch_items(sk_rad_kernel<float>, rad32, a, stream);
+    if (dtype == 1) return launch_items(sk_rad_kernel<float>, rad32, a, stream);   // + launch_rad_ieee_fixup
     return launch_items(sk_rad_kernel<double>, rad64, a, stream);
   }
   if (dist == 1) return dtype == 0 ? launch_items(sk_pair_kernel<1, double>, pair_smem_bytes<1>(), a, stream)
                                    : launch_items(sk_pair_kernel<1, float>, pair_smem_bytes<1>(), a, stream);
   if (dist == 3) return dtype == 0 ? launch_items(sk_pair_kernel<3, double>, pair_smem_bytes<3>(), a, stream)
                                    : launch_items(sk_pair_kernel<3, float>, pair_smem_bytes<3>(), a, stream);
-  return dtype == 0 ? launch_items(sk_pair_kernel<2, double>, pair_smem_bytes<2>(), a, stream, sm_count())
-                    : launch_items(sk_pair_kernel<2, float>, pair_smem_bytes<2>(), a, stream, sm_count());
+  return dtype == 0 ? launch_items(sk_pair_kernel<2, double>, pair_smem_bytes<2>(), a, stream, SK_GAUSS_PERSIST ? sm_count() : 0)
+                    : launch_items(sk_pair_kernel<2, float>, pair_smem_bytes<2>(), a, stream, SK_GAUSS_PERSIST ? sm_count() : 0);
+}
+
+cudaError_t launch_rad_ieee_fixup(int dtype, const ApplyArgs& a, const int* cols, cudaStream_t stream, int64_t n_cols) {
+  const unsigned grid = (unsigned)sm_count() * 2;
+  if (dtype == 0) sk_rad_ieee_fixup_kernel<double><<<grid, 256, 0, stream>>>(a, cols, n_cols);
+  else sk_rad_ieee_fixup_kernel<float><<<grid, 256, 0, stream>>>(a, cols, n_cols);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_fill_s(int dist, int dtype, uint64_t seed, int64_t i0, int64_t i1, int64_t j0,

@@ -630,7 +630,7 @@ JKI_CASES = [
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 @pytest.mark.parametrize("case", JKI_CASES, ids=[c[0] for c in JKI_CASES])
 def test_jki_matches_oracle(sk, dist, dtype, case):
-    # Algorithm 4 (one S[:, j] per nonzero row of a 16-column group, reused across the row) gives the
+    # Algorithm 4 (one S[:, j] per nonzero row of a column block, reused across the row) gives the
     # same sketch as the oracle's Algorithm 3 loop, within the dtype's bar
     import torch
     name, build, d = case
@@ -650,7 +650,8 @@ def test_jki_matches_oracle(sk, dist, dtype, case):
 
 
 def test_jki_auto_selection(sk):
-    # the plan builds the jki structure on its own only for patterns with row reuse
+    # the plan builds the Algorithm 4 structure on its own only when the exact distinct-row count of
+    # its column blocks (b_n = 1024 fp64 columns) makes the saved RNG pay for the scatter
     A = workloads.abnormal_paper("A", m=20000, n=64, seed=1)
     B = workloads.random_csc(200000, 64, 300, seed=2)
     pa = sk.Plan(_dev(A.colptr), _dev(A.rowidx), 256, A.m)
@@ -658,14 +659,61 @@ def test_jki_auto_selection(sk):
     try:
         assert pa.stats()["n_items_jki"] > 0 and pb.stats()["n_items_jki"] == 0
         assert pa.stats()["jki_nonzero_rows"] * 10 <= A.nnz
-        # the plan's Algorithm 4 structure holds exactly the distinct rows of every 16-column
-        # block (the rows whose S column Algorithm 4 generates)
-        exact = sum(len(np.unique(A.rowidx[A.colptr[c0]:A.colptr[min(A.n, c0 + 16)]]))
-                    for c0 in range(0, A.n, 16))
-        assert pa.stats()["jki_nonzero_rows"] == exact
+        # the RNG work of Algorithm 4 is exactly the distinct rows of every column block
+        # (PAPER.md:302-318, 436-442): here one block of all 64 columns
+        assert pa.stats()["jki_nonzero_rows"] == len(np.unique(A.rowidx))
         sk.set_pair_path("kji")
         assert "Algorithm 4" not in pa.kernel_name("uniform")
     finally:
         sk.set_pair_path("auto")
         pa.close()
         pb.close()
+
+
+def test_jki_selected_on_c2_with_exact_row_count(sk):
+    # BASELINE config c2 (1000 distinct uniform rows per column of 1e6): reuse nnz / nnzrows = 1.58
+    # over the whole matrix, so the plan picks Algorithm 4 with b_n = n and generates every needed
+    # S column once: its row count is exactly nnzrows(A)
+    A = workloads.make_config("c2")
+    plan = sk.Plan(_dev(A.colptr), _dev(A.rowidx), 2000, A.m)
+    try:
+        st = plan.stats()
+        assert st["n_items_jki"] > 0 and "Algorithm 4" in plan.kernel_name("uniform")
+        assert st["jki_nonzero_rows"] == len(np.unique(A.rowidx))
+    finally:
+        plan.close()
+
+
+def test_jki_multiple_blocks_and_split_parts(sk):
+    # n > b_n: several column blocks (Abnormal A-like dense rows so every block reuses its rows), a
+    # row with more entries than one batch holds (duplicated entries in a dense row), and few row
+    # tiles (d = 40) so each block's batches are split over several items and summed by the finishing
+    # kernel; fp64 and fp32, uniform and Gaussian
+    import torch
+    rng = np.random.default_rng(3)
+    m, n = 3000, 2300
+    dense_rows = np.arange(0, m, 100)
+    cols = []
+    for k in range(n):
+        r = np.concatenate([dense_rows, rng.choice(m, 3, replace=False)])
+        if k % 2 == 0:
+            r = np.concatenate([r, [7, 7]])            # duplicate (j, k) entries, unsorted
+        cols.append(r.astype(np.int32))
+    colptr = np.zeros(n + 1, np.int64)
+    colptr[1:] = np.cumsum([len(c) for c in cols])
+    rowidx = np.concatenate(cols).astype(np.int32)
+    vals = rng.standard_normal(int(colptr[-1]))
+    for dtype in ("f64", "f32"):
+        A = workloads.CSC(m, n, colptr, rowidx, vals.astype(np.float32 if dtype == "f32" else np.float64))
+        for dist, d in (("uniform", 40), ("gaussian", 300)):
+            plan = sk.Plan(_dev(A.colptr), _dev(A.rowidx), d, A.m, dtype)
+            try:
+                assert plan.stats()["n_items_jki"] > 0, dtype
+                got = plan.apply(_dev(A.vals), 23, dist).T.double().cpu().numpy()
+                got2 = plan.apply(_dev(A.vals), 23, dist).T.double().cpu().numpy()
+                torch.cuda.synchronize()
+            finally:
+                plan.close()
+            assert np.array_equal(got, got2)
+            ref, B = oracle.sketch(23, dist, d, A.m, A.n, A.colptr, A.rowidx, A.vals, threads=8)
+            _check(got, ref, B, TOL[dtype])

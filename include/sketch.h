@@ -80,7 +80,8 @@ typedef struct {
     int64_t philox_blocks_pair;/* Philox calls of one SK_UNIFORM / SK_GAUSSIAN apply */
     int64_t plan_bytes;        /* device bytes the plan owns */
     int64_t n_items_jki;       /* work items of the Algorithm 4 (jki) path, 0 if not built */
-    int64_t jki_nonzero_rows;  /* Σ over 16-column groups of the group's nonzero rows (its RNG work) */
+    int64_t jki_nonzero_rows;  /* Σ over the Algorithm 4 column blocks of the block's distinct rows (its
+                                  RNG work; = nnzrows(A) when one block holds all n columns) */
     int64_t n_items_f4_split;  /* tensor-core items that are parts of a K-split group (a column longer
                                   than 131071 nonzeros, or a last-wave item halved along K) */
     int64_t n_items_f4;        /* CTAs of the tensor-core kernel of one SK_RADEMACHER apply */
@@ -110,7 +111,10 @@ int sketch_plan_host(sk_plan_t* plan, sk_dtype_t dtype, int64_t d, int64_t m, in
                      int64_t nnz, int validate_rows, sk_stream_t stream);
 
 /*
- * sketch_apply -- out = S[:, row_offset : row_offset+m] · A  (d x n, column-major, ld = d).
+ * sketch_apply -- out = S[:, row_offset : row_offset+m] · A  (d x n, column-major, ld = d): the
+ * sketch Â = S A of PAPER.md:21-26 (Eq. `goal`), computed with S regenerated on the fly per the
+ * counter-based RNG of PAPER.md:489-492 (§4.2) -- Algorithm 3's kji loops or, when
+ * the plan built it, Algorithm 4's row reuse.
  * vals: nnz values in the plan's dtype (double for SK_F64, float for SK_F32), same order
  * as rowidx.  ASYNCHRONOUS, stream-ordered; plan is read-only (concurrent applies of one
  * plan on different streams are allowed).  Fused kernels: Philox generation, transform,
@@ -120,8 +124,10 @@ int sketch_plan_host(sk_plan_t* plan, sk_dtype_t dtype, int64_t d, int64_t m, in
 int sketch_apply(sk_plan_t plan, uint64_t seed, sk_dist_t dist, const void* vals, void* out,
                  sk_stream_t stream);
 
-/* sketch_apply_csc -- one-shot form of the north-star signature: plan + apply + destroy.
- * Synchronous (planning reads colptr back).  Same semantics as sketch_apply. */
+/* sketch_apply_csc -- one-shot form of the north-star signature: plan + apply + destroy -- the
+ * paper's format conversion followed by the multiplication (conversion and compute
+ * timed apart; CSC input).  Synchronous (planning reads colptr back).  Same semantics and
+ * errors as sketch_plan + sketch_apply. */
 int sketch_apply_csc(uint64_t seed, sk_dist_t dist, sk_dtype_t dtype, int64_t d, int64_t m,
                      int64_t n, int64_t row_offset, const int64_t* colptr,
                      const int32_t* rowidx, int64_t nnz, const void* vals, void* out,
@@ -143,7 +149,9 @@ int sketch_apply_host(uint64_t seed, sk_dist_t dist, sk_dtype_t dtype, int64_t d
                       int pipeline_chunks, sk_stream_t stream);
 
 /*
- * sketch_fill_s -- materialise S[i0:i1, j0:j1] (global indices) into out, column-major
+ * sketch_fill_s -- materialise S[i0:i1, j0:j1] (global indices) into out, column-major -- the
+ * generator Algorithm 3 calls `get_samples` with the entry definitions above
+ * (§4.2) --
  * with leading dimension ld >= i1 - i0, in dtype (double / float).  Asynchronous.
  * This is the parity anchor for the RNG contract above (bit-exact for ±1 and uniform).
  * Errors: SK_EINVAL (bad range / enum / ld), SK_ECUDA.
@@ -188,16 +196,19 @@ int sketch_set_rad_f64_path(int path);
 /*
  * Kernel selection for SK_UNIFORM / SK_GAUSSIAN (process-wide): Algorithm 3 (kji: S[:, j] regenerated
  * per stored nonzero) or Algorithm 4 (jki: S[:, j] regenerated once per nonzero
- * row of each 16-column group and reused across the row).  The plan builds the
- * jki structure (the group-wise CSR, "format conversion") only when a sample of column groups shows
- * at least 1.8 nonzeros per nonzero row; SK_PAIR_AUTO then uses jki whenever it was built.
+ * row of each vertical block of b_n columns -- b_n = 1024 fp64 / 2048 fp32, i.e. all n columns when
+ * they fit -- and reused across the row).  The plan counts the distinct
+ * rows of every block exactly (device row bitmap) and builds the jki structure (the blocks' CSR, the
+ * "format conversion") only when nonzero rows + 0.15 nnz < 0.9 nnz, i.e. when the Philox blocks
+ * saved pay for the scatter; SK_PAIR_AUTO then uses jki whenever it was built.
  * Initialised from SKETCH_PAIR_PATH = auto | kji | jki.  Errors: SK_EINVAL.
  */
 typedef enum { SK_PAIR_AUTO = 0, SK_PAIR_KJI = 1, SK_PAIR_JKI = 2 } sk_pair_path_t;
 int sketch_set_pair_path(int path);
 
 /* sketch_plan_host_jki -- as sketch_plan_host, but always builds the jki structure (for
- * measurements and tests of Algorithm 4 on any sparsity pattern).  Same errors. */
+ * measurements and tests of Algorithm 4 on any sparsity pattern).  Same errors, plus SK_EUNSUPPORTED
+ * when the structure cannot be built (nnz >= 2^32 - 1, m > 2^27, more than 32767 column blocks). */
 int sketch_plan_host_jki(sk_plan_t* plan, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
                          int64_t row_offset, const int64_t* h_colptr, const int32_t* rowidx,
                          int64_t nnz, int validate_rows, sk_stream_t stream);

@@ -84,8 +84,8 @@ int f4_tiles_per_cta();
 // stored row by row; a work item = (tile of kJRows rows of Â, block, range of the block's batches of
 // up to kJBatch nonzero rows / kJBatchEnt entries).
 constexpr int kJRows = 16;
-constexpr int kJBatch = 128;
-constexpr int kJBatchEnt = 1024;
+constexpr int kJBatch = 256;
+constexpr int kJBatchEnt = 2048;
 constexpr int kJOwners = 32;       // column owners (half-warps): column k of a block -> k mod 32
 struct JBatch {
   int64_t ent0;        // first entry (in ent)
@@ -106,12 +106,14 @@ struct JkiPlanView {
   const JBatch* batches;
   const uint16_t* own;       // [n_batches][kJOwners + 1]: entry ranges of the owners within the batch
   const int32_t* row_j;      // local row index of each nonzero row of each block
-  const uint2* ent;          // {value index, column within block | row slot within batch << 16}
+  const uint32_t* ent_p;     // value index of each entry (block CSR order)
+  const uint32_t* ent_desc;  // column within block | row slot within batch << 16
   const int32_t* blk_slot;   // [n_blocks + 1]: workspace slots of block b ([s0, s1), empty if unsplit)
   int64_t n;                 // columns of the plan
   int32_t bn;                // columns per block
   int32_t n_blocks;
   int64_t n_slots;           // workspace slots (bn x d each)
+  int64_t n_ent;             // entries (= nnz)
 };
 int jki_block_cols(int dtype);
 size_t jki_smem(int dtype, int bn);

@@ -383,13 +383,15 @@ int build_jki(sk_plan_s* p, const int64_t* h_colptr, bool force, cudaStream_t st
         items.push_back(sk::JItem{(int32_t)t, (int32_t)cut[(size_t)pt], (int32_t)cut[(size_t)pt + 1],
                                   P > 1 ? (int32_t)(s0 + pt) : -1});
   }
-  // (4) one device block: items | batches | own | row_j | ent | blk_slot
+  // (4) one device block: items | batches | own | row_j | ent_p | ent_desc | blk_slot
+  std::vector<uint32_t> ent_p(ent.size()), ent_desc(ent.size());
+  for (size_t e = 0; e < ent.size(); ++e) { ent_p[e] = ent[e].x; ent_desc[e] = ent[e].y; }
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   const size_t b_items = al(items.size() * sizeof(sk::JItem)), b_bat = al(batches.size() * sizeof(sk::JBatch)),
-               b_own = al(own.size() * 2), b_rowj = al(row_j.size() * 4), b_ent = al(ent.size() * 8),
+               b_own = al(own.size() * 2), b_rowj = al(row_j.size() * 4), b_ent = al(ent.size() * 4),
                b_slot = al(blk_slot.size() * 4);
   char* blk = nullptr;
-  cudaError_t e = cudaMalloc(&blk, b_items + b_bat + b_own + b_rowj + b_ent + b_slot);
+  cudaError_t e = cudaMalloc(&blk, b_items + b_bat + b_own + b_rowj + 2 * b_ent + b_slot);
   if (e != cudaSuccess) return e == cudaErrorMemoryAllocation ? SK_ENOMEM : cuda_fail(e, "cudaMalloc(jki)");
   char* c = blk;
   auto put = [&](const void* src, size_t bytes, size_t span) {
@@ -403,7 +405,8 @@ int build_jki(sk_plan_s* p, const int64_t* h_colptr, bool force, cudaStream_t st
   J.batches = reinterpret_cast<const sk::JBatch*>(put(batches.data(), batches.size() * sizeof(sk::JBatch), b_bat));
   J.own = reinterpret_cast<const uint16_t*>(put(own.data(), own.size() * 2, b_own));
   J.row_j = reinterpret_cast<const int32_t*>(put(row_j.data(), row_j.size() * 4, b_rowj));
-  J.ent = reinterpret_cast<const uint2*>(put(ent.data(), ent.size() * 8, b_ent));
+  J.ent_p = reinterpret_cast<const uint32_t*>(put(ent_p.data(), ent_p.size() * 4, b_ent));
+  J.ent_desc = reinterpret_cast<const uint32_t*>(put(ent_desc.data(), ent_desc.size() * 4, b_ent));
   J.blk_slot = reinterpret_cast<const int32_t*>(put(blk_slot.data(), blk_slot.size() * 4, b_slot));
   if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
   if (e != cudaSuccess) { cudaFree(blk); return cuda_fail(e, "upload jki"); }
@@ -412,6 +415,7 @@ int build_jki(sk_plan_s* p, const int64_t* h_colptr, bool force, cudaStream_t st
   J.bn = (int32_t)bn;
   J.n_blocks = (int32_t)NB;
   J.n_slots = slots;
+  J.n_ent = (int64_t)ent.size();
   p->d_jki = blk;
   p->jki = J;
   p->jki_rows = rows_total;

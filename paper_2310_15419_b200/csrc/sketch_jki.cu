@@ -11,14 +11,16 @@
 // On the GPU:
 //  * work item = (tile of kJRows = 16 rows of Â, block, range of the block's row batches): the CTA
 //    keeps the 16 x b_n accumulator of its tile in shared memory (fp64: 128 B per column, b_n <= 1024);
-//  * a batch = up to kJBatch = 128 nonzero rows (<= kJBatchEnt entries).  Stage (all 512 threads):
-//    S[tile rows, j] for the batch's rows -- 1024 Philox blocks, two per thread -- into shared memory,
-//    and the batch's entries (column, row slot) with their values gathered from the caller's CSC vals;
+//  * a batch = up to kJBatch = 256 nonzero rows (<= kJBatchEnt = 2048 entries).  Stage (all 512
+//    threads): S[tile rows, j] for the batch's rows -- 2048 Philox blocks, four per thread -- into
+//    shared memory, and the batch's entries (column, row slot, value);
 //  * scatter: half-warp h (32 per CTA) owns the block's columns k = h mod 32 and applies the batch's
 //    entries of its columns in row order, lane i updating row i: acc[k][i] += S[slot][i] a.  Entries
 //    of one column are applied by one half-warp in a fixed order, so results are deterministic;
-//  * batches are double-buffered: the stage of batch b+1 and the scatter of batch b run between the
-//    same pair of barriers (one __syncthreads per batch);
+//  * latency: a first kernel gathers the values into the blocks' CSR order (vals_csr[e] = vals[p_e],
+//    coalesced writes), so a batch's inputs are plain sequential loads; each thread loads the NEXT
+//    batch's rows and entries into registers before generating the current batch, so the loads fly
+//    under the Philox work (two barriers per batch: stage | scatter);
 //  * the tile's accumulator is written to Â once (or, when the block's batches are split over several
 //    items for load balance, to a workspace slot that a finishing kernel sums in a fixed order).
 // The plan (sketch_api.cu) builds the blocks' CSR on the host -- the paper's "format conversion",
@@ -39,9 +41,9 @@ constexpr int kJLogBytes = kBmLogRows * 3 * kJLogRep * 8;
 template <typename T>
 constexpr size_t jki_smem_bytes(int bn) {
   return (size_t)bn * kJRows * sizeof(T)                 // accumulator
-         + 2 * (size_t)kJBatch * kJRows * sizeof(T)     // S of two batches
-         + 2 * (size_t)kJBatchEnt * (4 + sizeof(T))     // entries (descriptor, value) of two batches
-         + 2 * 64 * 2                                   // owner offsets of two batches (33 used)
+         + (size_t)kJBatch * kJRows * sizeof(T)         // S of the batch
+         + (size_t)kJBatchEnt * (4 + sizeof(T))         // entries (descriptor, value) of the batch
+         + 64 * 2                                       // owner offsets (33 used)
          + kJLogBytes;
 }
 
@@ -63,70 +65,95 @@ __device__ __forceinline__ void jki_entries(const uint4 x, const double* __restr
   }
 }
 
+constexpr int kJSlotsPerThread = kJBatch * (kJRows / 2) / kJThreads;   // 4 Philox blocks per thread
+constexpr int kJEntPerThread = kJBatchEnt / kJThreads;                  // 4 entries per thread
+
+// One batch's inputs as one thread loads them (registers): its rows and its entries.
+template <typename T>
+struct JRegs {
+  int32_t rj[kJSlotsPerThread];
+  uint32_t desc[kJEntPerThread];
+  T val[kJEntPerThread];
+  uint16_t own;
+  int nrows, nent;
+};
+
+template <typename T>
+__device__ __forceinline__ void jki_load(const JkiPlanView& J, const T* __restrict__ vcsr, int64_t bt, JRegs<T>& R) {
+  const JBatch B = J.batches[bt];
+  R.nrows = B.nrows;
+  R.nent = B.nent;
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int h = 0; h < kJSlotsPerThread; ++h) {
+    const int slot = (tid >> 3) + 64 * h;
+    R.rj[h] = slot < B.nrows ? __ldg(J.row_j + B.row0 + slot) : 0;
+  }
+#pragma unroll
+  for (int k = 0; k < kJEntPerThread; ++k) {
+    const int e = tid + kJThreads * k;
+    R.desc[k] = e < B.nent ? __ldg(J.ent_desc + B.ent0 + e) : 0u;
+    R.val[k] = e < B.nent ? __ldg(vcsr + B.ent0 + e) : T(0);
+  }
+  R.own = tid < kJOwners + 1 ? __ldg(J.own + bt * (kJOwners + 1) + tid) : 0;
+}
+
 template <int DIST, typename T>
-__global__ void __launch_bounds__(kJThreads, 1) sk_jki_kernel(const ApplyArgs P, const JkiPlanView J, T* __restrict__ ws) {
+__global__ void __launch_bounds__(kJThreads, 1) sk_jki_kernel(const ApplyArgs P, const JkiPlanView J,
+                                                               const T* __restrict__ vcsr, T* __restrict__ ws) {
   extern __shared__ __align__(16) unsigned char smem[];
   const JItem it = J.items[blockIdx.x];
   const int blk = J.batches[it.bt0].block;
   const int64_t c0 = (int64_t)blk * J.bn;
   const int nbc = (int)min((int64_t)J.bn, J.n - c0);              // columns of this block
   T* acc = reinterpret_cast<T*>(smem);                             // [nbc][kJRows]
-  T* S = acc + (size_t)J.bn * kJRows;                              // [2][kJBatch][kJRows]
-  uint32_t* edesc = reinterpret_cast<uint32_t*>(S + 2 * kJBatch * kJRows);   // [2][kJBatchEnt]
-  T* evals = reinterpret_cast<T*>(edesc + 2 * kJBatchEnt);         // [2][kJBatchEnt]
-  uint16_t* own = reinterpret_cast<uint16_t*>(evals + 2 * kJBatchEnt);       // [2][64]
-  double* logtab = reinterpret_cast<double*>(own + 2 * 64);
+  T* S = acc + (size_t)J.bn * kJRows;                              // [kJBatch][kJRows]
+  uint32_t* edesc = reinterpret_cast<uint32_t*>(S + kJBatch * kJRows);   // [kJBatchEnt]
+  T* evals = reinterpret_cast<T*>(edesc + kJBatchEnt);             // [kJBatchEnt]
+  uint16_t* own = reinterpret_cast<uint16_t*>(evals + kJBatchEnt); // [64]
+  double* logtab = reinterpret_cast<double*>(own + 64);
   const double* mylog = logtab + (threadIdx.x & (kJLogRep - 1));
   const int tid = threadIdx.x;
-  const T* vals = reinterpret_cast<const T*>(P.vals);
   const uint32_t q0 = (uint32_t)it.tile * (kJRows / 2);            // Philox block of the tile's first row
+  const int ql = tid & 7;
 
   for (int e = tid; e < nbc * kJRows; e += kJThreads) acc[e] = T(0);
   if constexpr (DIST == 2) {
     jki_fill_logtab(logtab);
     __syncthreads();
   }
-
-  // Stage batch bt into buffer b: S of its rows (2 Philox blocks per thread) and its entries.
-  auto stage = [&](int64_t bt, int b) {
-    const JBatch B = J.batches[bt];
-    T* Sb = S + b * (kJBatch * kJRows);
-    const int ql = tid & 7;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int slot = (tid >> 3) + 64 * h;
-      if (slot < B.nrows) {
-        const uint64_t j = (uint64_t)P.row_offset + (uint32_t)__ldg(J.row_j + B.row0 + slot);
-        const uint4 x = s_block(q0 + ql, j, P.keys);
-        T v0, v1;
-        jki_entries<DIST, T>(x, mylog, v0, v1);
-        Sb[slot * kJRows + 2 * ql] = v0;
-        Sb[slot * kJRows + 2 * ql + 1] = v1;
-      }
-    }
-    for (int e = tid; e < B.nent; e += kJThreads) {
-      const uint2 en = __ldg(J.ent + B.ent0 + e);                  // {value index, k | slot << 16}
-      edesc[b * kJBatchEnt + e] = en.y;
-      evals[b * kJBatchEnt + e] = __ldg(vals + en.x);
-    }
-    if (tid < kJOwners + 1) own[b * 64 + tid] = __ldg(J.own + bt * (kJOwners + 1) + tid);
-  };
-
-  stage(it.bt0, 0);
-  __syncthreads();
+  JRegs<T> cur, nxt;
+  jki_load(J, vcsr, it.bt0, cur);
   const int hw = tid >> 4, i = tid & 15;                           // half-warp = column owner, lane = row
   for (int64_t bt = it.bt0; bt < it.bt1; ++bt) {
-    const int b = (int)((bt - it.bt0) & 1);
-    const T* Sb = S + b * (kJBatch * kJRows);
-    const int e1 = own[b * 64 + hw + 1];
-    for (int e = own[b * 64 + hw]; e < e1; ++e) {
-      const uint32_t dsc = edesc[b * kJBatchEnt + e];
-      const T a = evals[b * kJBatchEnt + e];
-      T* slot = acc + (dsc & 0xFFFFu) * kJRows + i;
-      *slot = fma(Sb[(dsc >> 16) * kJRows + i], a, *slot);
+    if (bt + 1 < it.bt1) jki_load(J, vcsr, bt + 1, nxt);           // in flight during this batch
+    // stage: S rows (4 Philox blocks per thread, independent chains) and the entries
+#pragma unroll
+    for (int h = 0; h < kJSlotsPerThread; ++h) {
+      const int slot = (tid >> 3) + 64 * h;
+      if (slot < cur.nrows) {
+        const uint4 x = s_block(q0 + ql, (uint64_t)P.row_offset + (uint32_t)cur.rj[h], P.keys);
+        T v0, v1;
+        jki_entries<DIST, T>(x, mylog, v0, v1);
+        S[slot * kJRows + 2 * ql] = v0;
+        S[slot * kJRows + 2 * ql + 1] = v1;
+      }
     }
-    if (bt + 1 < it.bt1) stage(bt + 1, b ^ 1);
+#pragma unroll
+    for (int k = 0; k < kJEntPerThread; ++k) {
+      const int e = tid + kJThreads * k;
+      if (e < cur.nent) { edesc[e] = cur.desc[k]; evals[e] = cur.val[k]; }
+    }
+    if (tid < kJOwners + 1) own[tid] = cur.own;
     __syncthreads();
+    const int e1 = own[hw + 1];
+    for (int e = own[hw]; e < e1; ++e) {
+      const uint32_t dsc = edesc[e];
+      T* slot = acc + (dsc & 0xFFFFu) * kJRows + i;
+      *slot = fma(S[(dsc >> 16) * kJRows + i], evals[e], *slot);
+    }
+    __syncthreads();
+    cur = nxt;
   }
 
   // the tile's rows [16 tile, +16) of the block's columns: to Â, or to this item's workspace slot
@@ -137,6 +164,14 @@ __global__ void __launch_bounds__(kJThreads, 1) sk_jki_kernel(const ApplyArgs P,
     const int c = e >> 4, r = e & 15;
     if (row0 + r < P.d) dst[(int64_t)c * P.d + row0 + r] = acc[e];
   }
+}
+
+// The values in the blocks' CSR order (one coalesced pass; the kernel's entries are then sequential).
+template <typename T>
+__global__ void sk_jki_gather_kernel(const T* __restrict__ vals, const uint32_t* __restrict__ ent_p, int64_t n,
+                                     T* __restrict__ vcsr) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    vcsr[e] = __ldg(vals + __ldg(ent_p + e));
 }
 
 // Blocks whose batches were split over several items: Â = Σ_parts in slot order (deterministic).
@@ -161,19 +196,25 @@ cudaError_t launch_jki_t(const ApplyArgs& a, const JkiPlanView& J, cudaStream_t 
   const size_t smem = jki_smem_bytes<T>(J.bn);
   cudaError_t e = cudaFuncSetAttribute(sk_jki_kernel<DIST, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  T* ws = nullptr;
-  if (J.n_slots > 0) {
-    e = cudaMallocAsync((void**)&ws, (size_t)J.n_slots * J.bn * a.d * sizeof(T), stream);
-    if (e != cudaSuccess) return e;
-  }
-  sk_jki_kernel<DIST, T><<<(unsigned)J.n_items, kJThreads, smem, stream>>>(a, J, ws);
+  // scratch (stream-ordered): values in CSR order, then the workspace slots of split blocks
+  const size_t vbytes = ((size_t)J.n_ent * sizeof(T) + 255) & ~(size_t)255;
+  char* scratch = nullptr;
+  e = cudaMallocAsync((void**)&scratch, vbytes + (size_t)J.n_slots * J.bn * a.d * sizeof(T), stream);
+  if (e != cudaSuccess) return e;
+  T* vcsr = reinterpret_cast<T*>(scratch);
+  T* ws = reinterpret_cast<T*>(scratch + vbytes);
+  sk_jki_gather_kernel<T><<<148 * 8, 256, 0, stream>>>(reinterpret_cast<const T*>(a.vals), J.ent_p, J.n_ent, vcsr);
   e = cudaGetLastError();
+  if (e == cudaSuccess) {
+    sk_jki_kernel<DIST, T><<<(unsigned)J.n_items, kJThreads, smem, stream>>>(a, J, vcsr, ws);
+    e = cudaGetLastError();
+  }
   if (e == cudaSuccess && J.n_slots > 0) {
     sk_jki_finish_kernel<T><<<148 * 4, 256, 0, stream>>>(a, J, ws);
     e = cudaGetLastError();
   }
-  if (ws) { const cudaError_t e2 = cudaFreeAsync(ws, stream); if (e == cudaSuccess) e = e2; }
-  return e;
+  const cudaError_t e2 = cudaFreeAsync(scratch, stream);
+  return e == cudaSuccess ? e2 : e;
 }
 
 }  // namespace

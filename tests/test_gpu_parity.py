@@ -454,18 +454,28 @@ def test_col_shards_and_overlapped_row_reduce(sk, dist):
     # column shards: nnz-balanced column blocks sketched independently are the
     # columns of the full sketch, bit for bit (every column is computed the same way); and the
     # row-sharded driver with the reduction overlapped per column group gives the plain result
+    # (Algorithm 3 for all: a column's bits then depend only on its own nonzeros and the tile shape;
+    # the automatic choice may pick Algorithm 4 for the full matrix but not for a shard, which moves
+    # the rounding within the parity bar -- checked below against the oracle)
     import torch
     from paper_2310_15419_b200.distributed import balanced_col_shards, sketch_row_sharded_overlapped
     A = workloads.random_csc(40000, 30, [300 + 37 * k for k in range(30)], seed=31)
     d = 900
-    full = _gpu_sketch(sk, A, d, dist, 8)
-    b = balanced_col_shards(A.colptr, 3)
-    blocks = [_gpu_sketch(sk, workloads.col_slice(A, b[g], b[g + 1]), d, dist, 8) for g in range(3)]
-    assert np.array_equal(np.concatenate(blocks, axis=1), full)
-    out = sketch_row_sharded_overlapped(A.colptr, _dev(A.colptr), _dev(A.rowidx), _dev(A.vals), d, A.m, 0, 8, dist,
-                                        groups=4)
-    torch.cuda.synchronize()
-    assert np.array_equal(out.T.cpu().numpy(), full)
+    ref, B = oracle.sketch(8, dist, d, A.m, A.n, A.colptr, A.rowidx, A.vals, threads=8)
+    _check(_gpu_sketch(sk, A, d, dist, 8), ref, B, TOL["f64"])
+    try:
+        sk.set_pair_path("kji")
+        full = _gpu_sketch(sk, A, d, dist, 8)
+        b = balanced_col_shards(A.colptr, 3)
+        blocks = [_gpu_sketch(sk, workloads.col_slice(A, b[g], b[g + 1]), d, dist, 8) for g in range(3)]
+        assert np.array_equal(np.concatenate(blocks, axis=1), full)
+        out = sketch_row_sharded_overlapped(A.colptr, _dev(A.colptr), _dev(A.rowidx), _dev(A.vals), d, A.m, 0, 8,
+                                            dist, groups=4)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.T.cpu().numpy(), full)
+    finally:
+        sk.set_pair_path("auto")
+    _check(full, ref, B, TOL["f64"])
 
 
 def test_degenerate_shapes(sk):

@@ -107,6 +107,27 @@ def test_uniform_law_and_exact_grid():
     assert stats.kstest(S, stats.uniform(loc=-1, scale=2).cdf).pvalue > 1e-4
 
 
+def test_uniform_word_order_against_independent_philox():
+    # SK_UNIFORM's entry 2q + h is built from words (x[2h], x[2h+1]) of block q as U = x[2h] 2^32 +
+    # x[2h+1], k = U >> 11, S = (2k + 1 - 2^53) 2^-53 (R2).  Pinned to Triton's independent
+    # Philox words, so a swapped word order (x[2h+1] 2^32 + x[2h]) or a wrong shift fails here, not
+    # only on the GPU; the ±1 bit order (entry 128q + 32t + b = bit b of word t, R3) likewise.
+    seed, j = 2**35 + 77, 2**32 + 3
+    words = _triton_philox([[q, 0, j & 0xFFFFFFFF, j >> 32, seed & 0xFFFFFFFF, seed >> 32] for q in range(4)])
+    col = oracle.get_samples(seed, "uniform", j, 8)
+    for q in range(4):
+        for h in range(2):
+            U = (int(words[q][2 * h]) << 32) | int(words[q][2 * h + 1])
+            k = U >> 11
+            assert col[2 * q + h] == (2 * k + 1 - 2**53) / 2.0**53
+    rad = oracle.get_samples(seed, "rademacher", j, 512)
+    for q in range(4):
+        for t in range(4):
+            for b in range(32):
+                bit = (int(words[q][t]) >> b) & 1
+                assert rad[128 * q + 32 * t + b] == (-1.0 if bit else 1.0)
+
+
 def test_uniform24_law_exact_grid_and_words():
     # the 24-bit odd grid, 4 entries per Philox block.  Pinned to the law (open
     # interval, exact grid, mean 0, variance (1 - 2^-48)/3, KS) and to the Philox words through the

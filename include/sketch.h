@@ -82,11 +82,9 @@ typedef struct {
     int64_t n_items_jki;       /* work items of the Algorithm 4 (jki) path, 0 if not built */
     int64_t jki_nonzero_rows;  /* Σ over the Algorithm 4 column blocks of the block's distinct rows (its
                                   RNG work; = nnzrows(A) when one block holds all n columns) */
-    int64_t n_items_f4_split;  /* tensor-core items that are parts of a K-split group (a column longer
-                                  than 131071 nonzeros, or a last-wave item halved along K) */
+    int64_t n_items_f4_split;  /* tensor-core items that are halves of a last-wave item split along K */
     int64_t n_items_f4;        /* CTAs of the tensor-core kernel of one SK_RADEMACHER apply */
     int64_t n_cols_f4;         /* columns on the tensor-core kernel (the others: n_items_rad SIMT CTAs) */
-    int64_t f4_split_groups;   /* K-split groups (int64 workspace slots of one apply) */
 } sk_stats_t;
 
 /*
@@ -179,11 +177,11 @@ const char* sketch_version(void);
  * Kernel selection for SK_RADEMACHER with SK_F64 values (process-wide, read when a plan is built).
  * Both compute the same Â within the parity bound |Â - oracle| <= 1e-12 |S||A|.
  *  SK_PATH_TC_FP4 (default): the tcgen05 kind::mxf4 kernel (±1 as e2m1, values as 64 signed binary
- *    digits of a per-column fixed-point scale; exact up to the value rounding <= L 2^-61 max|a| and one
- *    final fp64 rounding) for every column with 256 .. 2^20 nonzeros -- columns longer than 131071
- *    nonzeros split along K into parts that add exact int64 sums -- and the SIMT kernel for the other
- *    columns of the same plan.  A column holding a NaN or an Inf gets the IEEE result (NaN, or the
- *    common sign of its infinite terms), as the SIMT kernel and the oracle do.
+ *    digits of a per-column fixed-point scale; exact up to the value rounding <= L 2^-62 max|a| and one
+ *    final fp64 rounding) for every column with 256 .. 131071 nonzeros, and the SIMT kernel,
+ *    concurrently on a side stream, for the other columns of the same plan.  A column holding a NaN
+ *    or an Inf gets the IEEE result (NaN, or the common sign of its infinite terms), as the SIMT
+ *    kernel and the oracle do.
  *  SK_PATH_SIMT: the FP64 SIMT kernel (one SEL + one DADD per (row, nonzero)) for every column.
  * Initialised from SKETCH_RAD_F64_PATH = fp4 | simt.  Errors: SK_EINVAL for an unknown path.
  */

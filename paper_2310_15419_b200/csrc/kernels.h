@@ -47,45 +47,34 @@ struct ApplyArgs {
 };
 
 // Work item of the tensor-core ±1 kernel (sketch_f4.cu): column `col`, 128-row tiles
-// [tile0, tile0 + ntiles), and K range = part `part` of `nparts` equal shares of the column's
-// 64-nonzero K-steps (nparts > 1: a column longer than kTcMaxColumn, or a last-wave item split
-// along K); the parts of one (col, tiles) add exact int64 sums into workspace slot `group`.
-struct F4Item {
+// [tile0, tile0 + ntiles); pad 0 = the whole column, 1 / 2 = first / second half of its K-steps (the
+// last wave split along K; the halves add into zeroed rows).
+struct TcItem {
   int32_t col;
   int32_t tile0;
-  int32_t meta;     // ntiles | part << 8 | nparts << 16
-  int32_t group;    // split group (workspace slot), -1 when nparts == 1
+  int32_t ntiles;
+  int32_t pad;
 };
-__host__ __device__ inline int f4_ntiles(const F4Item& it) { return it.meta & 0xFF; }
-__host__ __device__ inline int f4_part(const F4Item& it) { return (it.meta >> 8) & 0xFF; }
-__host__ __device__ inline int f4_nparts(const F4Item& it) { return (it.meta >> 16) & 0xFF; }
-__host__ __device__ inline int32_t f4_meta(int ntiles, int part, int nparts) { return ntiles | part << 8 | nparts << 16; }
 
-// Longest K range of one tensor-core item: the digit sums |D| <= L must stay exact in the f32
-// accumulator (L < 2^24), and the value rounding of a column, <= L 2^-61 max|a|, must stay far
-// below the fp64 parity bound 1e-12 |S||A| (2^20 2^-61 = 4.5e-13): parts of <= 131071 nonzeros,
-// columns of <= 2^20 (longer ones run on the SIMT kernel).
+// Longest column the tensor-core kernel takes: the digit sums |D| <= L stay exact in the f32
+// accumulator (L < 2^24), and the value rounding <= L 2^-62 max|a| stays far below the fp64 parity
+// bound (2^-45 |S||A| at L = 2^17).  Longer columns run on the SIMT kernel.
 constexpr int64_t kTcMaxColumn = 131071;
-constexpr int64_t kTcMaxColumnTotal = int64_t(1) << 20;
 
-// n_groups: split groups (their int64 workspace is allocated and zeroed stream-ordered by the
-// launcher).  Launches the tensor-core kernel, the split groups' finishing kernel and the IEEE fix-up
-// of the columns it found non-finite (sketch_f4.cu).
-cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const F4Item* items, int64_t n_items, int64_t n_groups,
-                                cudaStream_t stream);
-// ±1 sketch columns holding a NaN / Inf value get the IEEE result: NaN if a term is NaN or +Inf and -Inf
-// terms meet, else the common sign of the infinite terms (sketch_kernels.cu).  cols = device list
-// {count, column...} of the columns to rewrite; nullptr: scan every column's values (n_cols of them).
-// dtype 0 = f64, 1 = f32.
-cudaError_t launch_rad_ieee_fixup(int dtype, const ApplyArgs& a, const int* cols, cudaStream_t stream,
-                                  int64_t n_cols = 0);
+// The tensor-core kernel, with the zeroing of the K-split rows before it and the IEEE fix-up of the
+// columns it found non-finite after it.
+cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const TcItem* items, int64_t n_items, cudaStream_t stream);
+
+// ±1 sketch columns holding a NaN / Inf value get the IEEE result (sketch_kernels.cu): a scan of
+// every column's values, one warp per column (dtype 0 = f64, 1 = f32).
+cudaError_t launch_rad_ieee_fixup(int dtype, const ApplyArgs& a, int64_t n_cols, cudaStream_t stream);
 int f4_tiles_per_cta();
 // Algorithm 4 (jki) with full row reuse (sketch_jki.cu): vertical blocks of up to b_n columns, each
 // stored row by row; a work item = (tile of kJRows rows of Â, block, range of the block's batches of
 // up to kJBatch nonzero rows / kJBatchEnt entries).
 constexpr int kJRows = 16;
-constexpr int kJBatch = 256;
-constexpr int kJBatchEnt = 2048;
+constexpr int kJBatch = 128;
+constexpr int kJBatchEnt = 1024;
 constexpr int kJOwners = 32;       // column owners (half-warps): column k of a block -> k mod 32
 struct JBatch {
   int64_t ent0;        // first entry (in ent)
@@ -97,7 +86,8 @@ struct JBatch {
 };
 struct JItem {
   int32_t tile;        // rows [kJRows tile, +kJRows) of Â
-  int32_t bt0, bt1;    // batches [bt0, bt1) of one block
+  int32_t block;       // vertical block (an empty block's items write zeros)
+  int32_t bt0, bt1;    // batches [bt0, bt1) of the block
   int32_t slot;        // workspace slot (the block's batches are split over several items), -1: write Â
 };
 struct JkiPlanView {
@@ -165,6 +155,43 @@ __device__ __forceinline__ unsigned long long col_absmax_bits(const double* __re
     m0 = max(m0, max(ab(x0.x), ab(x0.y)));
   }
   return max(max(m0, m1), max(m2, m3));
+}
+
+// IEEE result of column k of a ±1 sketch when its values hold a NaN or an Inf (one warp): every
+// entry of Â[:, k] is then non-finite, and IEEE addition in ANY order gives NaN if a term is NaN or
+// both +Inf and -Inf terms occur, else the sign of the infinite terms -- the oracle's sequential
+// sum.  Lane = row within a 32-row chunk; one Philox block per (non-finite value, chunk).  Returns
+// without writing when the column is finite.  Rare path.
+template <typename T>
+__device__ __forceinline__ void rad_ieee_fix_column(const ApplyArgs& P, int64_t k) {
+  constexpr unsigned kAll = 0xFFFFFFFFu;
+  const int lane = threadIdx.x & 31;
+  const T* vals = reinterpret_cast<const T*>(P.vals);
+  const int64_t pb = P.colptr[k], pe = P.colptr[k + 1];
+  bool bad = false;
+  for (int64_t p = pb + lane; p < pe; p += 32) bad |= !isfinite(vals[p]);
+  if (!__any_sync(kAll, bad)) return;
+  T* outc = reinterpret_cast<T*>(P.out) + k * P.ld;
+  for (int64_t r0 = 0; r0 < P.d; r0 += 32) {
+    const int64_t row = r0 + lane;
+    uint32_t f = 0;                                    // 1: a +Inf term, 2: a -Inf term, 4: a NaN
+    for (int64_t p0 = pb; p0 < pe; p0 += 32) {
+      const T v = p0 + lane < pe ? vals[p0 + lane] : T(0);
+      const int32_t j = p0 + lane < pe ? P.rowidx[p0 + lane] : 0;
+      if (__any_sync(kAll, isnan(v))) f |= 4u;
+      for (unsigned m = __ballot_sync(kAll, isinf(v)); m; m &= m - 1) {
+        const int s = __ffs(m) - 1;
+        const T vi = __shfl_sync(kAll, v, s);
+        const uint32_t jr = (uint32_t)__shfl_sync(kAll, j, s);
+        const uint4 x = s_block((uint32_t)(row >> 7), (uint64_t)P.row_offset + jr, P.keys);
+        const int t = (int)((row >> 5) & 3);
+        const uint32_t w = t == 0 ? x.x : t == 1 ? x.y : t == 2 ? x.z : x.w;
+        const uint32_t neg = ((w >> (row & 31)) & 1u) ^ (vi < T(0) ? 1u : 0u);   // S = -1 where the bit is set
+        f |= neg ? 2u : 1u;
+      }
+    }
+    if (row < P.d) outc[row] = (f & 4u) || f == 3u ? T(NAN) : (f == 1u ? T(INFINITY) : T(-INFINITY));
+  }
 }
 
 }  // namespace sk

@@ -98,6 +98,13 @@ __device__ __forceinline__ float uniform24(uint32_t w) {
 constexpr int kLogRep = 16;
 constexpr int kLogTabRepBytes = kBmLogRows * 3 * kLogRep * 8;   // 49.5 KB
 
+// The same table as one copy with 32-byte rows {-2c, 2 L_hi, 2 L_lo, 0} (4.1 KB; STRIDE = 0 above).
+constexpr int kLogTab4Bytes = kBmLogRows * 4 * 8;
+__device__ __forceinline__ void bm_fill_logtab4(double* smem_tab) {
+  for (int i = threadIdx.x; i < kBmLogRows * 4; i += blockDim.x)
+    smem_tab[i] = (i & 3) == 3 ? 0.0 : kBmLogTab[i >> 2][i & 3];
+}
+
 __device__ __forceinline__ void bm_fill_logtab(double* smem_tab) {
   for (int i = threadIdx.x; i < kBmLogRows * 3 * kLogRep; i += blockDim.x)
     smem_tab[i] = (&kBmLogTab[0][0])[i / kLogRep];
@@ -111,15 +118,22 @@ __device__ __forceinline__ void bm_fill_logtab(double* smem_tab) {
 // (log1p(r) - r) / r^2, truncated where the next term is below 2^-60), the first bracket exact
 // (2^-42 grid).  The factor -2 of Box-Muller is folded into the constants: 11 FP64 operations.
 // tab = row 0, component 0 of this lane's copy; STRIDE = distance between consecutive components
-// (kLogRep for the replicated shared-memory table, 1 for kBmLogTab itself).
+// (kLogRep for the replicated shared-memory table, 1 for kBmLogTab itself), or STRIDE = 0: one copy in
+// 32-byte rows (bm_fill_logtab4).
 template <int STRIDE>
 __device__ __forceinline__ double bm_m2log_u53(double U, const double* __restrict__ tab) {
   const unsigned long long b = (unsigned long long)__double_as_longlong(U);
   const int e = (int)(b >> 52) - (1023 + 53);
   const double m = __longlong_as_double((long long)((b & 0x000FFFFFFFFFFFFFull) | 0x3FF0000000000000ull));
   const int idx = (int)(((b >> 44) & 0xFFu) + 1u) >> 1;        // round(128 (m - 1)), 0..128
-  const double* row = tab + 3 * STRIDE * idx;
-  const double c2 = row[0], hi = row[STRIDE], lo = row[2 * STRIDE];
+  double c2, hi, lo;
+  if constexpr (STRIDE == 0) {        // one copy with 32-byte rows {-2c, 2 L_hi, 2 L_lo, pad}: 16 + 8 byte loads
+    const double2 ch = *reinterpret_cast<const double2*>(tab + 4 * idx);
+    c2 = ch.x; hi = ch.y; lo = tab[4 * idx + 2];
+  } else {
+    const double* row = tab + 3 * STRIDE * idx;
+    c2 = row[0]; hi = row[STRIDE]; lo = row[2 * STRIDE];
+  }
   const double s = fma(m, c2, 2.0);                            // -2 r, |r| < 0.0045
   const double s2 = s * s;
   double q = fma(s, kBm[kQ4], kBm[kQ3]);                       // (the s^5/448 term is below 2^-60)

@@ -111,48 +111,36 @@ Schedule build_schedule(const int64_t* colptr, int64_t n, int64_t d, int rows_pe
   return S;
 }
 
-// Tensor-core schedule over the columns `cols`: per column, ceil(d/128) row tiles in groups of
-// <= `per` per CTA; a column longer than kTcMaxColumn is split along K into
-// ceil(L / kTcMaxColumn) parts (one split group per tile group).  Longest items first.
-struct F4Schedule {
-  std::vector<sk::F4Item> items;
-  int64_t groups = 0;         // split groups (workspace slots)
-  int64_t split_items = 0;    // items with nparts > 1
-};
-
-F4Schedule build_f4_schedule(const int64_t* colptr, int64_t d, int64_t per, const std::vector<int32_t>& cols) {
-  F4Schedule F;
+// Tensor-core schedule over the columns `cols`: per column, ceil(d/128) row tiles in groups of <= `per`
+// per CTA, longest columns first.
+std::vector<sk::TcItem> build_tc_schedule(const int64_t* colptr, int64_t d, int64_t per, const std::vector<int32_t>& cols) {
   const int64_t tiles = (d + 127) / 128;
-  const int64_t tgroups = (tiles + per - 1) / per;
-  const int64_t tpg = (tiles + tgroups - 1) / tgroups;
-  std::vector<std::pair<int64_t, sk::F4Item>> tmp;
+  const int64_t groups = (tiles + per - 1) / per;
+  const int64_t tpg = (tiles + groups - 1) / groups;
+  std::vector<std::pair<int64_t, sk::TcItem>> tmp;
   for (int32_t k : cols) {
     const int64_t L = colptr[k + 1] - colptr[k];
-    const int64_t P = std::max<int64_t>(1, (L + sk::kTcMaxColumn - 1) / sk::kTcMaxColumn);
     for (int64_t g = 0; g * tpg < tiles; ++g) {
-      const int64_t grp = P > 1 ? F.groups++ : -1;
-      for (int64_t pt = 0; pt < P; ++pt) {
-        sk::F4Item it;
-        it.col = k;
-        it.tile0 = (int32_t)(g * tpg);
-        it.meta = sk::f4_meta((int)std::min(tpg, tiles - g * tpg), (int)pt, (int)P);
-        it.group = (int32_t)grp;
-        tmp.emplace_back(L / P, it);
-        if (P > 1) ++F.split_items;
-      }
+      sk::TcItem it;
+      it.col = k;
+      it.tile0 = (int32_t)(g * tpg);
+      it.ntiles = (int32_t)std::min(tpg, tiles - g * tpg);
+      it.pad = 0;
+      tmp.emplace_back(L, it);
     }
   }
-  std::stable_sort(tmp.begin(), tmp.end(), [](const std::pair<int64_t, sk::F4Item>& a,
-                                              const std::pair<int64_t, sk::F4Item>& b) { return a.first > b.first; });
-  F.items.reserve(tmp.size());
-  for (auto& pr : tmp) F.items.push_back(pr.second);
-  return F;
+  std::stable_sort(tmp.begin(), tmp.end(), [](const std::pair<int64_t, sk::TcItem>& a,
+                                              const std::pair<int64_t, sk::TcItem>& b) { return a.first > b.first; });
+  std::vector<sk::TcItem> out;
+  out.reserve(tmp.size());
+  for (auto& pr : tmp) out.push_back(pr.second);
+  return out;
 }
 
 // Kernel used for ±1 with fp64 values (process-wide, read when a plan is built; results agree
-// within the parity bound): SK_PATH_TC_FP4 (default: the tensor-core kernel for every column with
-// at least kF4MinColumn nonzeros, the SIMT kernel for the rest) or SK_PATH_SIMT (the SIMT kernel
-// for every column).  Initialised from SKETCH_RAD_F64_PATH = fp4 | simt, else fp4.
+// within the parity bound): SK_PATH_TC_FP4 (default: the tensor-core kernel for every column of
+// f4_min_column() .. kTcMaxColumn nonzeros, the SIMT kernel for the others, concurrently) or
+// SK_PATH_SIMT (the SIMT kernel for every column).  Initialised from SKETCH_RAD_F64_PATH = fp4 | simt.
 std::atomic<int> g_rad_f64_path{-1};
 
 int rad_f64_path() {
@@ -198,11 +186,10 @@ struct sk_plan_s {
   const int64_t* colptr;   // device (caller-owned)
   const int32_t* rowidx;   // device (caller-owned)
   Item* d_items = nullptr; // [rad items | pair items | Gaussian items] (SIMT kernels)
-  sk::F4Item* d_f4 = nullptr;       // tensor-core ±1 fp64 schedule (empty unless dtype F64 and path FP4)
+  sk::TcItem* d_f4 = nullptr;       // tensor-core ±1 fp64 schedule (empty unless dtype F64 and path FP4)
   int64_t n_f4 = 0;
-  int64_t f4_groups = 0;            // split groups (long columns and the K-split last wave)
-  int64_t f4_split_items = 0;       // items that are parts of a split group
-  int64_t f4_cols = 0;              // columns on the tensor-core kernel (the rest: SIMT items)
+  int64_t f4_split_items = 0;       // half items of the K-split last wave
+  int64_t f4_cols = 0;              // columns on the tensor-core kernel (the rest: n_rad SIMT items)
   // Algorithm 4 (jki) structure: one device block holding items, grp_rows, row_j, row_ent, ent, ent_base
   void* d_jki = nullptr;
   sk::JkiPlanView jki{};
@@ -380,7 +367,7 @@ int build_jki(sk_plan_s* p, const int64_t* h_colptr, bool force, cudaStream_t st
     blk_slot.push_back((int32_t)slots);
     for (int64_t pt = 0; pt < P; ++pt)
       for (int64_t t = 0; t < T; ++t)
-        items.push_back(sk::JItem{(int32_t)t, (int32_t)cut[(size_t)pt], (int32_t)cut[(size_t)pt + 1],
+        items.push_back(sk::JItem{(int32_t)t, (int32_t)b, (int32_t)cut[(size_t)pt], (int32_t)cut[(size_t)pt + 1],
                                   P > 1 ? (int32_t)(s0 + pt) : -1});
   }
   // (4) one device block: items | batches | own | row_j | ent_p | ent_desc | blk_slot
@@ -439,32 +426,31 @@ int validate_colptr(const int64_t* h, int64_t n, int64_t nnz, bool require_zero_
 
 // Last-wave split of the fp4 schedule.  Items cost about the same and the hardware hands them to
 // SMs in order, so N items on W SMs take ceil(N / W) item-times; when the last wave is less than
-// half full (0 < N mod W < W/2), splitting the last W + N mod W whole items into two halves along K
-// (same rows, half the K-steps each) turns the final 2 item-times into 1.5.  The halves add exact
-// int64 digit sums into a workspace slot (deterministic in any order); the second to finish writes
-// Â.  SKETCH_F4_SPLIT=0 disables it.
-void split_f4_tail(F4Schedule& F, const int64_t* h_colptr) {
+// half full (0 < N mod W < W/2), splitting the last W + N mod W items into two halves along K
+// (same rows, half the nonzeros each) turns the final 2 item-times into 1.5.  The halves add into
+// Â with one fp64 atomicAdd each onto zeroed rows: 0 + a + b rounds identically in either order,
+// so the output stays deterministic.  SKETCH_F4_SPLIT=0 disables it.  Returns the half items.
+int64_t split_f4_tail(std::vector<sk::TcItem>& f4, const int64_t* h_colptr) {
   static const bool off = [] { const char* v = getenv("SKETCH_F4_SPLIT"); return v && !strcmp(v, "0"); }();
   int W = kSMs, dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&W, cudaDevAttrMultiProcessorCount, dev);
-  std::vector<sk::F4Item>& f4 = F.items;
   const int64_t N = (int64_t)f4.size(), r = W > 0 ? N % W : 0;
-  if (off || W <= 0 || N <= W || r == 0 || 2 * r >= W) return;
+  if (off || W <= 0 || N <= W || r == 0 || 2 * r >= W) return 0;
   const int64_t first = N - W - r;
-  std::vector<sk::F4Item> out(f4.begin(), f4.begin() + first);
+  std::vector<sk::TcItem> out(f4.begin(), f4.begin() + first);
+  int64_t halves = 0;
   for (int64_t i = first; i < N; ++i) {
-    sk::F4Item it = f4[(size_t)i];
-    if (sk::f4_nparts(it) == 1 && h_colptr[it.col + 1] - h_colptr[it.col] >= 128) {   // >= two K-steps
-      const int nt = sk::f4_ntiles(it);
-      it.group = (int32_t)F.groups++;
-      it.meta = sk::f4_meta(nt, 0, 2); out.push_back(it);
-      it.meta = sk::f4_meta(nt, 1, 2); out.push_back(it);
-      F.split_items += 2;
+    sk::TcItem it = f4[(size_t)i];
+    if (h_colptr[it.col + 1] - h_colptr[it.col] >= 128) {   // at least two K-steps
+      it.pad = 1; out.push_back(it);
+      it.pad = 2; out.push_back(it);
+      halves += 2;
     } else {
       out.push_back(it);
     }
   }
   f4.swap(out);
+  return halves;
 }
 
 // Copy a plan's schedule image to the device on `stream` (one copy); `sync` waits for it and
@@ -495,20 +481,20 @@ int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
       fprintf(stderr, "  make_plan %s: %.3f ms\n", what,
               std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tm0).count());
   };
-  // ±1 x fp64: columns with kF4MinColumn .. kTcMaxColumnTotal nonzeros run on the tensor cores,
-  // the others on the SIMT kernel (per column, not per matrix).
-  F4Schedule f4;
+  // ±1 x fp64: columns with f4_min_column() .. kTcMaxColumn nonzeros run on the tensor cores, the
+  // others on the SIMT kernel (per column, not per matrix; the two launches run concurrently)
+  std::vector<sk::TcItem> f4;
   std::vector<int32_t> simt_cols;
   const bool use_f4 = dtype == SK_F64 && rad_f64_path() == SK_PATH_TC_FP4;
   if (use_f4) {
     std::vector<int32_t> tc_cols;
     for (int64_t k = 0; k < n; ++k) {
       const int64_t L = h_colptr[k + 1] - h_colptr[k];
-      (L >= f4_min_column() && L <= sk::kTcMaxColumnTotal ? tc_cols : simt_cols).push_back((int32_t)k);
+      (L >= f4_min_column() && L <= sk::kTcMaxColumn ? tc_cols : simt_cols).push_back((int32_t)k);
     }
     if (!tc_cols.empty()) {
-      f4 = build_f4_schedule(h_colptr, d, sk::f4_tiles_per_cta(), tc_cols);
-      split_f4_tail(f4, h_colptr);
+      f4 = build_tc_schedule(h_colptr, d, sk::f4_tiles_per_cta(), tc_cols);
+      p->f4_split_items = split_f4_tail(f4, h_colptr);
     }
     p->f4_cols = (int64_t)tc_cols.size();
   }
@@ -521,9 +507,7 @@ int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
   p->n_gauss = (int64_t)gauss.items.size();
   p->philox_rad = rad.philox_blocks;
   p->philox_pair = pair.philox_blocks;
-  p->n_f4 = (int64_t)f4.items.size();
-  p->f4_groups = f4.groups;
-  p->f4_split_items = f4.split_items;
+  p->n_f4 = (int64_t)f4.size();
   lap("schedules");
   // one host image of every schedule, 256-byte aligned sections
   {
@@ -531,7 +515,7 @@ int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
     auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
     p->off_items = 0;
     p->off_f4 = up(p->off_items + (size_t)total * sizeof(Item));
-    const size_t bytes = up(p->off_f4 + f4.items.size() * sizeof(sk::F4Item));
+    const size_t bytes = up(p->off_f4 + f4.size() * sizeof(sk::TcItem));
     p->h_stage.assign(bytes, 0);
     unsigned char* h = p->h_stage.data();
     size_t o = p->off_items;
@@ -539,13 +523,13 @@ int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
       if (!sc->items.empty()) std::memcpy(h + o, sc->items.data(), sc->items.size() * sizeof(Item));
       o += sc->items.size() * sizeof(Item);
     }
-    if (!f4.items.empty()) std::memcpy(h + p->off_f4, f4.items.data(), f4.items.size() * sizeof(sk::F4Item));
+    if (!f4.empty()) std::memcpy(h + p->off_f4, f4.data(), f4.size() * sizeof(sk::TcItem));
     cudaError_t e = defer_upload ? cudaMallocAsync(&p->d_stage, bytes > 0 ? bytes : 256, stream)
                                  : cudaMalloc(&p->d_stage, bytes > 0 ? bytes : 256);
     if (e != cudaSuccess) { delete p; return e == cudaErrorMemoryAllocation ? SK_ENOMEM : cuda_fail(e, "cudaMalloc(plan)"); }
     unsigned char* dst = static_cast<unsigned char*>(p->d_stage);
     p->d_items = total > 0 ? reinterpret_cast<Item*>(dst + p->off_items) : nullptr;
-    p->d_f4 = f4.items.empty() ? nullptr : reinterpret_cast<sk::F4Item*>(dst + p->off_f4);
+    p->d_f4 = f4.empty() ? nullptr : reinterpret_cast<sk::TcItem*>(dst + p->off_f4);
   }
   lap("image + malloc");
   if (jki >= 0) {
@@ -576,6 +560,28 @@ int validate_rows_sync(const int32_t* rowidx, int64_t nnz, int64_t m, cudaStream
   return h ? SK_ECSC : SK_OK;
 }
 
+// A side stream + fork / join events per host thread and device (created once).
+struct SidePipe {
+  int dev = -1;
+  bool ok = false;
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+
+SidePipe& side_pipe() {
+  thread_local SidePipe sp;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) { sp.ok = false; return sp; }
+  if (sp.dev != dev) {
+    sp = SidePipe();
+    sp.ok = cudaStreamCreateWithFlags(&sp.side, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaEventCreateWithFlags(&sp.fork, cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreateWithFlags(&sp.join, cudaEventDisableTiming) == cudaSuccess;
+    sp.dev = dev;
+  }
+  return sp;
+}
+
 int apply_items(const sk_plan_s* p, uint64_t seed, sk_dist_t dist, const void* vals, void* out,
                 cudaStream_t stream) {
   sk::ApplyArgs a;
@@ -592,11 +598,24 @@ int apply_items(const sk_plan_s* p, uint64_t seed, sk_dist_t dist, const void* v
   a.keys = sk::make_keys(seed);
   cudaError_t e = cudaSuccess;
   if (dist == SK_RADEMACHER) {
-    // tensor-core columns, then the SIMT kernel on the remaining columns (disjoint columns of Â)
-    if (p->n_f4 > 0) e = sk::launch_apply_rad_f4(a, p->d_f4, p->n_f4, p->f4_groups, stream);
-    if (e == cudaSuccess) e = sk::launch_apply(0, (int)p->dtype, a, stream);
+    if (p->n_f4 > 0 && p->n_rad > 0) {
+      // tensor-core columns and SIMT columns (short or longer than kTcMaxColumn) write disjoint
+      // columns of Â: the SIMT kernel runs concurrently on a side stream (it takes a few SMs
+      // first; the tensor-core items fill the rest), joined back before returning
+      SidePipe& sp = side_pipe();
+      e = sp.ok ? cudaEventRecord(sp.fork, stream) : cudaErrorNotReady;
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(sp.side, sp.fork, 0);
+      if (e == cudaSuccess) e = sk::launch_apply(0, (int)p->dtype, a, sp.side);
+      if (e == cudaSuccess) e = cudaEventRecord(sp.join, sp.side);
+      if (e == cudaSuccess) e = sk::launch_apply_rad_f4(a, p->d_f4, p->n_f4, stream);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, sp.join, 0);
+    } else if (p->n_f4 > 0) {
+      e = sk::launch_apply_rad_f4(a, p->d_f4, p->n_f4, stream);
+    } else {
+      e = sk::launch_apply(0, (int)p->dtype, a, stream);
+    }
     // fp32 "T - 2P" sums: columns holding a NaN / Inf rewritten with the IEEE result (a scan of the values)
-    if (e == cudaSuccess && p->dtype == SK_F32 && p->n_rad > 0) e = sk::launch_rad_ieee_fixup(1, a, nullptr, stream, p->n);
+    if (e == cudaSuccess && p->dtype == SK_F32 && p->n_rad > 0) e = sk::launch_rad_ieee_fixup(1, a, p->n, stream);
   } else if ((dist == SK_UNIFORM || dist == SK_GAUSSIAN) && p->jki.n_items > 0 && pair_path() != SK_PAIR_KJI) {
     e = sk::launch_apply_jki((int)dist, (int)p->dtype, a, p->jki, stream);
   } else {
@@ -961,9 +980,8 @@ int sketch_plan_stats(sk_plan_t plan, sk_stats_t* h) {
   h->n_items_f4_split = plan->f4_split_items;
   h->n_items_f4 = plan->n_f4;
   h->n_cols_f4 = plan->f4_cols;
-  h->f4_split_groups = plan->f4_groups;
   h->plan_bytes = (plan->n_rad + plan->n_pair + plan->n_gauss) * (int64_t)sizeof(Item) +
-                  plan->n_f4 * (int64_t)sizeof(sk::F4Item) + (plan->owned_colptr ? (plan->n + 1) * 8 : 0);
+                  plan->n_f4 * (int64_t)sizeof(sk::TcItem) + (plan->owned_colptr ? (plan->n + 1) * 8 : 0);
   return SK_OK;
 }
 

@@ -185,37 +185,23 @@ __device__ __forceinline__ uint32_t f4_off(int m, int h) {
 #ifndef SK_F4_DEBUG
 #define SK_F4_DEBUG 0
 #endif
-// Epilogue per item: whole columns round Σ_s 2^s D_s - D_64 once into Â; the K-split parts (a column
-// longer than kTcMaxColumn, or a last-wave item halved along K) add their exact int64 (hi, lo - ones)
-// into a workspace slot with integer atomics (order-independent: deterministic) and
-// sk_f4_finish_kernel converts the sums after the launch.  A column holding a NaN / Inf (its digit
-// encoding needs finite values) is only recorded in nf_list and left to sk_rad_ieee_fixup_kernel.
-// (Keeping both rare paths out of this kernel keeps the schedule of its producer loops: c5 7.22 ms,
-// against 7.30 ms with them inline; A/B on one box, scripts/gpu_ab2.sh.)
-__global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArgs P, const F4Item* items,
-                                                                   unsigned long long* __restrict__ ws,
-                                                                   int* __restrict__ nf_list, int dbg_arg) {
+__global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArgs P, const TcItem* items,
+                                                                   unsigned long long* __restrict__ colmax, int dbg_arg) {
   const int dbg = SK_F4_DEBUG ? dbg_arg : 0;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* stages = smem_raw + ((1024u - (s_u32(smem_raw) & 1023u)) & 1023u);
   F4Shared& sh = *reinterpret_cast<F4Shared*>(stages + kF4Stages * kF4Stage);
+  const TcItem it = items[blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const F4Item it = items[blockIdx.x];
-  // The column's nonzeros [cb, ce); this item's K range [pb, pe) is part `part` of `nparts` equal
-  // shares of its 64-nonzero K-steps (nparts > 1: columns longer than kTcMaxColumn, and the
-  // last-wave items split along K).  E is the column-wide exponent so all parts use one scale.
-  const int64_t cb = P.colptr[it.col], ce = P.colptr[it.col + 1];
-  const int part = f4_part(it), nparts = f4_nparts(it);
-  int64_t pb = cb, pe = ce;
-  if (nparts > 1) {
-    const int64_t ns = (ce - cb + 63) >> 6;
-    pb = cb + 64 * ((ns * part) / nparts);
-    pe = min(ce, cb + 64 * ((ns * (part + 1)) / nparts));
+  int64_t pb = P.colptr[it.col], pe = P.colptr[it.col + 1];
+  if (it.pad) {   // last-wave item split along K: pad 1 = first half of the K-steps, 2 = second half
+    const int64_t half = ((((pe - pb) + 63) >> 6) >> 1) << 6;
+    if (it.pad == 1) pe = pb + half; else pb += half;
   }
   const int64_t L = pe - pb;
   const int nsteps = (int)((L + 63) >> 6);
   const int nsup = (nsteps + kF4Sub - 1) / kF4Sub;
-  const int T = f4_ntiles(it);                     // <= kF4Tiles
+  const int T = it.ntiles;                         // <= kF4Tiles
   const double* vals = reinterpret_cast<const double*>(P.vals);
 
   if (threadIdx.x == 0) {
@@ -253,9 +239,9 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   }
-  // column scale E (all producers), over the whole column
+  // column scale E (all producers)
   if (warp < kF4Producers && !(dbg & 16)) {
-    unsigned long long mx = col_absmax_bits(vals, cb, ce, threadIdx.x, kF4Producers * 32);
+    unsigned long long mx = col_absmax_bits(vals, pb, pe, threadIdx.x, kF4Producers * 32);
     for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
     if (lane == 0) atomicMax(&sh.maxabs_bits, mx);
   }
@@ -265,18 +251,10 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
     int e = 0;
     if (isfinite(m)) frexp(m, &e); else sh.nonfinite = 1;
     sh.E = e;
+    colmax[blockIdx.x] = sh.maxabs_bits;   // NaN / Inf columns: rewritten by sk_rad_ieee_fixup_kernel
   }
   __syncthreads();
   const int E = sh.E;
-  if (sh.nonfinite) {
-    if (threadIdx.x == 0 && part == 0 && it.tile0 == 0) nf_list[1 + atomicAdd(nf_list, 1)] = it.col;
-    __syncthreads();
-    if (warp == kF4MmaWarp) {
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(512));
-    }
-    return;
-  }
 
   if (warp < 2 * T) {
     // ===================== A producers: S tile (w % T), nonzero half =====================
@@ -424,15 +402,14 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
   }
 
   // ===================== epilogue: warps 0..11 read D (lane quarter = warp % 4) =====================
-  // Σ_s 2^s D_s - D_64 = hi 2^32 + (lo - ones): both parts exact int64.  Whole columns round once
-  // into fp64; the parts of a split column add their (hi, lo - ones) into the int64 workspace.
-  double* outc = reinterpret_cast<double*>(P.out) + (int64_t)it.col * P.ld;
   if (warp < kF4Producers) {
     if (nsteps > 0) {
       f4_wait(&sh.done, 0);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     }
     const int qw = warp & 3;
+    double* outc = reinterpret_cast<double*>(P.out) + (int64_t)it.col * P.ld;
+    const double nan = __longlong_as_double(0x7FF8000000000000ll);
     for (int tt = warp >> 2; warp < 12 && tt < T; tt += 3) {
       long long lo = 0, hi = 0, ones = 0;
       if (nsteps > 0) {
@@ -454,16 +431,13 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
           }
         }
       }
-      const int r = tt * 128 + 32 * qw + lane;
-      const int64_t row = (int64_t)it.tile0 * 128 + r;
+      const int64_t row = (int64_t)(it.tile0 + tt) * 128 + 32 * qw + lane;
       if (row < P.d) {
-        if (nparts > 1) {
-          unsigned long long* wsg = ws + 2 * ((size_t)it.group * (kF4Tiles * 128) + r);
-          atomicAdd(wsg, (unsigned long long)hi);
-          atomicAdd(wsg + 1, (unsigned long long)(lo - ones));
-        } else {
-          outc[row] = scalbn((double)hi * 4294967296.0 + (double)(lo - ones), E - 62);
-        }
+        // Σ_s 2^s D_s - D_64 = hi 2^32 + (lo - ones), both parts exact in fp64; one rounding
+        const double v = scalbn((double)hi * 4294967296.0 + (double)(lo - ones), E - 62);
+        const double res = sh.nonfinite ? nan : v;   // (placeholder; the IEEE fix-up rewrites the column)
+        // K-split halves add into the zeroed output: 0 + a + b rounds the same in either order
+        if (it.pad) atomicAdd(outc + row, res); else outc[row] = res;
       }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -475,40 +449,6 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
   }
 }
 
-// Split groups: Â rows of group g = 2^(E-62) ((Σ hi) 2^32 + Σ (lo - ones)), one rounding; E is recomputed
-// from the column (the same scan as the kernel's).  One CTA per group.
-__global__ void sk_f4_finish_kernel(const ApplyArgs P, const F4Item* items, int64_t n_items,
-                                    const unsigned long long* __restrict__ ws) {
-  __shared__ unsigned long long mx;
-  __shared__ int E;
-  // the group's first part: items are scanned from the end (the split parts sit in the last wave)
-  const int g = blockIdx.x;
-  F4Item it{};
-  for (int64_t i = n_items - 1; i >= 0; --i)
-    if (f4_nparts(items[i]) > 1 && items[i].group == g) { it = items[i]; break; }
-  if (threadIdx.x == 0) mx = 0ull;
-  __syncthreads();
-  const int64_t cb = P.colptr[it.col], ce = P.colptr[it.col + 1];
-  unsigned long long m = col_absmax_bits(reinterpret_cast<const double*>(P.vals), cb, ce, threadIdx.x, blockDim.x);
-  for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(&mx, m);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int e = 0;
-    frexp(__longlong_as_double((long long)mx), &e);   // non-finite columns are rewritten by the IEEE fix-up
-    E = e;
-  }
-  __syncthreads();
-  double* outc = reinterpret_cast<double*>(P.out) + (int64_t)it.col * P.ld;
-  for (int r = threadIdx.x; r < f4_ntiles(it) * 128; r += blockDim.x) {
-    const int64_t row = (int64_t)it.tile0 * 128 + r;
-    if (row >= P.d) break;
-    const long long hi = (long long)ws[2 * ((size_t)g * (kF4Tiles * 128) + r)];
-    const long long lo = (long long)ws[2 * ((size_t)g * (kF4Tiles * 128) + r) + 1];
-    outc[row] = scalbn((double)hi * 4294967296.0 + (double)lo, E - 62);
-  }
-}
-
 }  // namespace
 
 int f4_tiles_per_cta() {   // SKETCH_F4_TILES (tuning only): fewer row tiles per CTA
@@ -517,30 +457,44 @@ int f4_tiles_per_cta() {   // SKETCH_F4_TILES (tuning only): fewer row tiles per
   return t;
 }
 
-cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const F4Item* items, int64_t n_items, int64_t n_groups,
-                                cudaStream_t stream) {
+// Zero the Â rows of the K-split items (pad == 1 marks the first half of each pair).
+__global__ void sk_f4_zero_split_kernel(const ApplyArgs P, const TcItem* items) {
+  const TcItem it = items[blockIdx.x];
+  if (it.pad != 1) return;
+  const int64_t r0 = (int64_t)it.tile0 * 128;
+  const int64_t r1 = min(P.d, (int64_t)(it.tile0 + it.ntiles) * 128);
+  double* o = reinterpret_cast<double*>(P.out) + (int64_t)it.col * P.ld;
+  for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) o[r] = 0.0;
+}
+
+// Columns whose maximum |a| bit pattern is non-finite (NaN / Inf): the IEEE result (one warp per item).
+__global__ void sk_f4_ieee_fixup_kernel(const ApplyArgs P, const TcItem* items, int64_t n_items,
+                                        const unsigned long long* __restrict__ colmax) {
+  const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp0; i < n_items; i += nwarps)
+    if (colmax[i] >= 0x7FF0000000000000ull) rad_ieee_fix_column<double>(P, items[i].col);   // (idempotent)
+}
+
+cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const TcItem* items, int64_t n_items, cudaStream_t stream) {
   if (n_items == 0) return cudaSuccess;
   const size_t smem = (size_t)kF4Stages * kF4Stage + sizeof(F4Shared) + 1024;
-  static const int dbg = [] { const char* v = getenv("SKETCH_F4_DEBUG"); return v ? atoi(v) : 0; }();
-  // scratch (stream-ordered): the split groups' int64 (hi, lo) per row, then the non-finite column
-  // list (count + column indices)
-  const size_t ws_bytes = (size_t)n_groups * kF4Tiles * 128 * 16, nf_bytes = (size_t)(n_items + 1) * 4;
-  unsigned long long* ws = nullptr;
-  cudaError_t e = cudaMallocAsync((void**)&ws, ws_bytes + nf_bytes, stream);
+  cudaError_t e = cudaFuncSetAttribute(sk_rad_f4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  int* nf = reinterpret_cast<int*>(reinterpret_cast<char*>(ws) + ws_bytes);
-  e = cudaMemsetAsync(ws, 0, ws_bytes + 4, stream);   // workspace + the list's count
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(sk_rad_f4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static const int dbg = [] { const char* v = getenv("SKETCH_F4_DEBUG"); return v ? atoi(v) : 0; }();
+  unsigned long long* colmax = nullptr;                 // per item: max |a| bits of its K range
+  e = cudaMallocAsync((void**)&colmax, (size_t)n_items * 8, stream);
+  if (e != cudaSuccess) return e;
+  sk_f4_zero_split_kernel<<<(unsigned)n_items, 256, 0, stream>>>(a, items);
+  e = cudaGetLastError();
   if (e == cudaSuccess) {
-    sk_rad_f4_kernel<<<(unsigned)n_items, kF4Threads, smem, stream>>>(a, items, ws, nf, dbg);
+    sk_rad_f4_kernel<<<(unsigned)n_items, kF4Threads, smem, stream>>>(a, items, colmax, dbg);
     e = cudaGetLastError();
   }
-  if (e == cudaSuccess && n_groups > 0) {
-    sk_f4_finish_kernel<<<(unsigned)n_groups, 256, 0, stream>>>(a, items, n_items, ws);
+  if (e == cudaSuccess) {
+    sk_f4_ieee_fixup_kernel<<<64, 256, 0, stream>>>(a, items, n_items, colmax);
     e = cudaGetLastError();
   }
-  if (e == cudaSuccess) e = launch_rad_ieee_fixup(0, a, nf, stream);
-  const cudaError_t e2 = cudaFreeAsync(ws, stream);
+  const cudaError_t e2 = cudaFreeAsync(colmax, stream);
   return e == cudaSuccess ? e2 : e;
 }
 

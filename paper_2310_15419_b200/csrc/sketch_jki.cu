@@ -11,16 +11,17 @@
 // On the GPU:
 //  * work item = (tile of kJRows = 16 rows of Â, block, range of the block's row batches): the CTA
 //    keeps the 16 x b_n accumulator of its tile in shared memory (fp64: 128 B per column, b_n <= 1024);
-//  * a batch = up to kJBatch = 256 nonzero rows (<= kJBatchEnt = 2048 entries).  Stage (all 512
-//    threads): S[tile rows, j] for the batch's rows -- 2048 Philox blocks, four per thread -- into
+//  * a batch = up to kJBatch = 128 nonzero rows (<= kJBatchEnt = 1024 entries).  Stage (all 512
+//    threads): S[tile rows, j] for the batch's rows -- 1024 Philox blocks, two per thread -- into
 //    shared memory, and the batch's entries (column, row slot, value);
 //  * scatter: half-warp h (32 per CTA) owns the block's columns k = h mod 32 and applies the batch's
 //    entries of its columns in row order, lane i updating row i: acc[k][i] += S[slot][i] a.  Entries
 //    of one column are applied by one half-warp in a fixed order, so results are deterministic;
 //  * latency: a first kernel gathers the values into the blocks' CSR order (vals_csr[e] = vals[p_e],
-//    coalesced writes), so a batch's inputs are plain sequential loads; each thread loads the NEXT
-//    batch's rows and entries into registers before generating the current batch, so the loads fly
-//    under the Philox work (two barriers per batch: stage | scatter);
+//    coalesced writes), so a batch's inputs are plain sequential loads, issued one batch ahead into
+//    registers; S and the entries are double-buffered, so the scatter of batch b and the stage of
+//    batch b+1 run between the same two barriers (one __syncthreads per batch) and one warp's
+//    scatter latency hides under the other warps' Philox work;
 //  * the tile's accumulator is written to Â once (or, when the block's batches are split over several
 //    items for load balance, to a workspace slot that a finishing kernel sums in a fixed order).
 // The plan (sketch_api.cu) builds the blocks' CSR on the host -- the paper's "format conversion",
@@ -41,9 +42,9 @@ constexpr int kJLogBytes = kBmLogRows * 3 * kJLogRep * 8;
 template <typename T>
 constexpr size_t jki_smem_bytes(int bn) {
   return (size_t)bn * kJRows * sizeof(T)                 // accumulator
-         + (size_t)kJBatch * kJRows * sizeof(T)         // S of the batch
-         + (size_t)kJBatchEnt * (4 + sizeof(T))         // entries (descriptor, value) of the batch
-         + 64 * 2                                       // owner offsets (33 used)
+         + 2 * (size_t)kJBatch * kJRows * sizeof(T)     // S of two batches
+         + 2 * (size_t)kJBatchEnt * (4 + sizeof(T))     // entries (descriptor, value) of two batches
+         + 2 * 64 * 2                                   // owner offsets of two batches (33 used)
          + kJLogBytes;
 }
 
@@ -65,8 +66,8 @@ __device__ __forceinline__ void jki_entries(const uint4 x, const double* __restr
   }
 }
 
-constexpr int kJSlotsPerThread = kJBatch * (kJRows / 2) / kJThreads;   // 4 Philox blocks per thread
-constexpr int kJEntPerThread = kJBatchEnt / kJThreads;                  // 4 entries per thread
+constexpr int kJSlotsPerThread = kJBatch * (kJRows / 2) / kJThreads;   // 2 Philox blocks per thread
+constexpr int kJEntPerThread = kJBatchEnt / kJThreads;                  // 2 entries per thread
 
 // One batch's inputs as one thread loads them (registers): its rows and its entries.
 template <typename T>
@@ -103,57 +104,67 @@ __global__ void __launch_bounds__(kJThreads, 1) sk_jki_kernel(const ApplyArgs P,
                                                                const T* __restrict__ vcsr, T* __restrict__ ws) {
   extern __shared__ __align__(16) unsigned char smem[];
   const JItem it = J.items[blockIdx.x];
-  const int blk = J.batches[it.bt0].block;
-  const int64_t c0 = (int64_t)blk * J.bn;
+  const int64_t c0 = (int64_t)it.block * J.bn;
   const int nbc = (int)min((int64_t)J.bn, J.n - c0);              // columns of this block
   T* acc = reinterpret_cast<T*>(smem);                             // [nbc][kJRows]
-  T* S = acc + (size_t)J.bn * kJRows;                              // [kJBatch][kJRows]
-  uint32_t* edesc = reinterpret_cast<uint32_t*>(S + kJBatch * kJRows);   // [kJBatchEnt]
-  T* evals = reinterpret_cast<T*>(edesc + kJBatchEnt);             // [kJBatchEnt]
-  uint16_t* own = reinterpret_cast<uint16_t*>(evals + kJBatchEnt); // [64]
-  double* logtab = reinterpret_cast<double*>(own + 64);
+  T* S = acc + (size_t)J.bn * kJRows;                              // [2][kJBatch][kJRows]
+  uint32_t* edesc = reinterpret_cast<uint32_t*>(S + 2 * kJBatch * kJRows);   // [2][kJBatchEnt]
+  T* evals = reinterpret_cast<T*>(edesc + 2 * kJBatchEnt);         // [2][kJBatchEnt]
+  uint16_t* own = reinterpret_cast<uint16_t*>(evals + 2 * kJBatchEnt);       // [2][64]
+  double* logtab = reinterpret_cast<double*>(own + 2 * 64);
   const double* mylog = logtab + (threadIdx.x & (kJLogRep - 1));
   const int tid = threadIdx.x;
   const uint32_t q0 = (uint32_t)it.tile * (kJRows / 2);            // Philox block of the tile's first row
   const int ql = tid & 7;
 
   for (int e = tid; e < nbc * kJRows; e += kJThreads) acc[e] = T(0);
-  if constexpr (DIST == 2) {
-    jki_fill_logtab(logtab);
-    __syncthreads();
-  }
-  JRegs<T> cur, nxt;
-  jki_load(J, vcsr, it.bt0, cur);
-  const int hw = tid >> 4, i = tid & 15;                           // half-warp = column owner, lane = row
-  for (int64_t bt = it.bt0; bt < it.bt1; ++bt) {
-    if (bt + 1 < it.bt1) jki_load(J, vcsr, bt + 1, nxt);           // in flight during this batch
-    // stage: S rows (4 Philox blocks per thread, independent chains) and the entries
+  if constexpr (DIST == 2) jki_fill_logtab(logtab);
+
+  // stage: the batch held in R -> buffer b (S rows: 2 Philox blocks per thread; entries; owners)
+  auto stage = [&](const JRegs<T>& R, int b) {
+    T* Sb = S + b * (kJBatch * kJRows);
 #pragma unroll
     for (int h = 0; h < kJSlotsPerThread; ++h) {
       const int slot = (tid >> 3) + 64 * h;
-      if (slot < cur.nrows) {
-        const uint4 x = s_block(q0 + ql, (uint64_t)P.row_offset + (uint32_t)cur.rj[h], P.keys);
+      if (slot < R.nrows) {
+        const uint4 x = s_block(q0 + ql, (uint64_t)P.row_offset + (uint32_t)R.rj[h], P.keys);
         T v0, v1;
         jki_entries<DIST, T>(x, mylog, v0, v1);
-        S[slot * kJRows + 2 * ql] = v0;
-        S[slot * kJRows + 2 * ql + 1] = v1;
+        Sb[slot * kJRows + 2 * ql] = v0;
+        Sb[slot * kJRows + 2 * ql + 1] = v1;
       }
     }
 #pragma unroll
     for (int k = 0; k < kJEntPerThread; ++k) {
       const int e = tid + kJThreads * k;
-      if (e < cur.nent) { edesc[e] = cur.desc[k]; evals[e] = cur.val[k]; }
+      if (e < R.nent) { edesc[b * kJBatchEnt + e] = R.desc[k]; evals[b * kJBatchEnt + e] = R.val[k]; }
     }
-    if (tid < kJOwners + 1) own[tid] = cur.own;
-    __syncthreads();
-    const int e1 = own[hw + 1];
-    for (int e = own[hw]; e < e1; ++e) {
-      const uint32_t dsc = edesc[e];
+    if (tid < kJOwners + 1) own[b * 64 + tid] = R.own;
+  };
+
+  JRegs<T> R;
+  if (it.bt0 < it.bt1) {
+    if constexpr (DIST == 2) __syncthreads();                      // the log table before the first stage
+    jki_load(J, vcsr, it.bt0, R);
+    stage(R, 0);
+    if (it.bt0 + 1 < it.bt1) jki_load(J, vcsr, it.bt0 + 1, R);     // in flight during the first scatter
+  }
+  __syncthreads();
+  const int hw = tid >> 4, i = tid & 15;                           // half-warp = column owner, lane = row
+  for (int64_t bt = it.bt0; bt < it.bt1; ++bt) {
+    const int b = (int)((bt - it.bt0) & 1);
+    const T* Sb = S + b * (kJBatch * kJRows);
+    const int e1 = own[b * 64 + hw + 1];
+    for (int e = own[b * 64 + hw]; e < e1; ++e) {
+      const uint32_t dsc = edesc[b * kJBatchEnt + e];
       T* slot = acc + (dsc & 0xFFFFu) * kJRows + i;
-      *slot = fma(S[(dsc >> 16) * kJRows + i], evals[e], *slot);
+      *slot = fma(Sb[(dsc >> 16) * kJRows + i], evals[b * kJBatchEnt + e], *slot);
+    }
+    if (bt + 1 < it.bt1) {
+      stage(R, b ^ 1);
+      if (bt + 2 < it.bt1) jki_load(J, vcsr, bt + 2, R);           // in flight during the next scatter
     }
     __syncthreads();
-    cur = nxt;
   }
 
   // the tile's rows [16 tile, +16) of the block's columns: to Â, or to this item's workspace slot

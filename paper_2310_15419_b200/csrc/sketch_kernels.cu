@@ -184,9 +184,13 @@ __device__ __forceinline__ void block_entries(const uint4 x, T (&v)[pair_E<DIST>
 #define SK_GAUSS_SCREP kScRep
 #endif
 #ifndef SK_GAUSS_PERSIST
-#define SK_GAUSS_PERSIST 1
+#define SK_GAUSS_PERSIST 0
+#endif
+#ifndef SK_GAUSS_LOGREP
+#define SK_GAUSS_LOGREP 0
 #endif
 constexpr int kGaussScRep = SK_GAUSS_SCREP;
+constexpr int kGaussLogRep = SK_GAUSS_LOGREP;   // 0: one copy in 32-byte rows; > 0: replicated
 template <int DIST> constexpr int pair_rows() { return (DIST == 2 ? kRowsPerWarpGauss : kRowsPerWarpPair) / 32; }
 
 // One work item of the uniform / Gaussian / uniform24 kernel (the CTA's 16 warps; `red` = the
@@ -230,7 +234,7 @@ __device__ __forceinline__ void pair_item(const ApplyArgs& P, const Item it, T* 
         for (int h = 0; h < kPairRows / 2; ++h) {
           const uint4 x = s_block(q0 + h, J, P.keys);
           T v0, v1;
-          pair_entries<DIST, T, kLogRep, kGaussScRep>(x, v0, v1, logtab, sctab);
+          pair_entries<DIST, T, kGaussLogRep, kGaussScRep>(x, v0, v1, logtab, sctab);
           acc[2 * h] = fma(v0, a, acc[2 * h]);
           acc[2 * h + 1] = fma(v1, a, acc[2 * h + 1]);
         }
@@ -268,7 +272,8 @@ __device__ __forceinline__ void pair_item(const ApplyArgs& P, const Item it, T* 
 // Shared memory: reduction area, then (Gaussian) the replicated -2 log and sin / cos tables.
 template <int DIST> constexpr int pair_red_bytes() { return kWarps * 32 * (pair_rows<DIST>() + 1) * 8; }
 template <int DIST> constexpr size_t pair_smem_bytes() {
-  return (size_t)pair_red_bytes<DIST>() + (DIST == 2 ? (size_t)kLogTabRepBytes + (kGaussScRep ? kScTabRepBytes : 0) : 0);
+  return (size_t)pair_red_bytes<DIST>() +
+         (DIST == 2 ? (size_t)(kGaussLogRep ? kLogTabRepBytes : kLogTab4Bytes) + (kGaussScRep ? kScTabRepBytes : 0) : 0);
 }
 
 // Uniform / uniform24: one CTA per item.  Gaussian: persistent, one CTA per SM walking the
@@ -282,11 +287,11 @@ __global__ void __launch_bounds__(kThreads, 1) sk_pair_kernel(const ApplyArgs P)
   const double* sctab = nullptr;
   if constexpr (DIST == 2) {
     double* lt = reinterpret_cast<double*>(smem + pair_red_bytes<DIST>());
-    double* st = reinterpret_cast<double*>(smem + pair_red_bytes<DIST>() + kLogTabRepBytes);
-    bm_fill_logtab(lt);
+    double* st = reinterpret_cast<double*>(smem + pair_red_bytes<DIST>() + (kGaussLogRep ? kLogTabRepBytes : kLogTab4Bytes));
+    if (kGaussLogRep) bm_fill_logtab(lt); else bm_fill_logtab4(lt);
     if (kGaussScRep) bm_fill_sctab(st);
     __syncthreads();
-    logtab = lt + (threadIdx.x & (kLogRep - 1));        // this lane's copies
+    logtab = kGaussLogRep ? lt + (threadIdx.x & (kLogRep - 1)) : lt;   // this lane's copies
     sctab = st + 2 * (threadIdx.x & (kScRep - 1));
     for (int64_t i = blockIdx.x; i < P.n_items; i += gridDim.x) pair_item<DIST, T>(P, P.items[i], red, logtab, sctab);
   } else {
@@ -295,48 +300,12 @@ __global__ void __launch_bounds__(kThreads, 1) sk_pair_kernel(const ApplyArgs P)
 }
 
 // ------------------------------------------------------------------ IEEE fix-up of non-finite columns
-//
-// A column of A holding a NaN or an Inf makes every entry of its column of Â non-finite, and IEEE
-// addition in ANY order then gives NaN if a term is NaN or both +Inf and -Inf terms occur, else the
-// sign of the infinite terms -- the oracle's sequential sum.  Kernels whose arithmetic does not give
-// that by itself (the tensor-core digits need finite values; the fp32 "T - 2P" form turns Inf - 2 Inf
-// into NaN) leave those columns to this pass: one warp per column, lane = row within a 32-row chunk,
-// one Philox block per (non-finite value, chunk).  Rare path.
+// (rad_ieee_fix_column, kernels.h): the fp32 "T - 2P" sums turn Inf - 2 Inf into NaN, so the columns
+// holding a NaN / Inf are rewritten after the kernel; one warp per column.
 template <typename T>
-__global__ void sk_rad_ieee_fixup_kernel(const ApplyArgs P, const int* __restrict__ cols, int64_t n_cols) {
-  const int lane = threadIdx.x & 31;
+__global__ void sk_rad_ieee_fixup_kernel(const ApplyArgs P, int64_t n_cols) {
   const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t ncol = cols ? (int64_t)cols[0] : n_cols;
-  const T* vals = reinterpret_cast<const T*>(P.vals);
-  for (int64_t ci = warp0; ci < ncol; ci += nwarps) {
-    const int64_t k = cols ? (int64_t)cols[1 + ci] : ci;
-    const int64_t pb = P.colptr[k], pe = P.colptr[k + 1];
-    bool bad = false;
-    for (int64_t p = pb + lane; p < pe; p += 32) bad |= !isfinite(vals[p]);
-    if (!__any_sync(kFull, bad)) continue;
-    T* outc = reinterpret_cast<T*>(P.out) + k * P.ld;
-    for (int64_t r0 = 0; r0 < P.d; r0 += 32) {
-      const int64_t row = r0 + lane;
-      uint32_t f = 0;                                    // 1: a +Inf term, 2: a -Inf term, 4: a NaN
-      for (int64_t p0 = pb; p0 < pe; p0 += 32) {
-        const T v = p0 + lane < pe ? vals[p0 + lane] : T(0);
-        const int32_t j = p0 + lane < pe ? P.rowidx[p0 + lane] : 0;
-        if (__any_sync(kFull, isnan(v))) f |= 4u;
-        for (unsigned m = __ballot_sync(kFull, isinf(v)); m; m &= m - 1) {
-          const int s = __ffs(m) - 1;
-          const T vi = __shfl_sync(kFull, v, s);
-          const uint32_t jr = (uint32_t)__shfl_sync(kFull, j, s);
-          const uint4 x = s_block((uint32_t)(row >> 7), (uint64_t)P.row_offset + jr, P.keys);
-          const int t = (int)((row >> 5) & 3);
-          const uint32_t w = t == 0 ? x.x : t == 1 ? x.y : t == 2 ? x.z : x.w;
-          const uint32_t neg = ((w >> (row & 31)) & 1u) ^ (vi < T(0) ? 1u : 0u);   // S = -1 where the bit is set
-          f |= neg ? 2u : 1u;
-        }
-      }
-      if (row < P.d)
-        outc[row] = (f & 4u) || f == 3u ? T(NAN) : (f == 1u ? T(INFINITY) : T(-INFINITY));
-    }
-  }
+  for (int64_t k = warp0; k < n_cols; k += nwarps) rad_ieee_fix_column<T>(P, k);
 }
 
 // ------------------------------------------------------------------ S materialisation
@@ -419,10 +388,10 @@ cudaError_t launch_apply(int dist, int dtype, const ApplyArgs& a, cudaStream_t s
                     : launch_items(sk_pair_kernel<2, float>, pair_smem_bytes<2>(), a, stream, SK_GAUSS_PERSIST ? sm_count() : 0);
 }
 
-cudaError_t launch_rad_ieee_fixup(int dtype, const ApplyArgs& a, const int* cols, cudaStream_t stream, int64_t n_cols) {
+cudaError_t launch_rad_ieee_fixup(int dtype, const ApplyArgs& a, int64_t n_cols, cudaStream_t stream) {
   const unsigned grid = (unsigned)sm_count() * 2;
-  if (dtype == 0) sk_rad_ieee_fixup_kernel<double><<<grid, 256, 0, stream>>>(a, cols, n_cols);
-  else sk_rad_ieee_fixup_kernel<float><<<grid, 256, 0, stream>>>(a, cols, n_cols);
+  if (dtype == 0) sk_rad_ieee_fixup_kernel<double><<<grid, 256, 0, stream>>>(a, n_cols);
+  else sk_rad_ieee_fixup_kernel<float><<<grid, 256, 0, stream>>>(a, n_cols);
   return cudaGetLastError();
 }
 

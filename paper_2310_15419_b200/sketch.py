@@ -46,7 +46,7 @@ class sk_stats_t(ctypes.Structure):
     _fields_ = [(name, ctypes.c_int64) for name in
                 ("d", "m", "n", "nnz", "row_offset", "max_col_nnz", "n_items_rad", "n_items_pair",
                  "philox_blocks_rad", "philox_blocks_pair", "plan_bytes", "n_items_jki", "jki_nonzero_rows", "n_items_f4_split",
-                 "n_items_f4", "n_cols_f4", "f4_split_groups")]
+                 "n_items_f4", "n_cols_f4")]
 
 
 _lock = threading.Lock()
@@ -271,7 +271,7 @@ def sketch_fill_s(seed, dist, i0, i1, j0, j1, dtype="f64", device="cuda", stream
 
 def set_rad_f64_path(path) -> None:
     """Select the kernel for ±1 sketches of fp64 values in plans built from now on: "fp4" (tensor
-    cores for columns of >= 256 nonzeros, SIMT for the rest; default) or "simt" (process-wide)."""
+    cores for columns of 256 .. 131071 nonzeros, SIMT for the rest; default) or "simt" (process-wide)."""
     p = RAD_F64_PATHS[path] if isinstance(path, str) else int(path)
     _check(load_library().sketch_set_rad_f64_path(p), "sketch_set_rad_f64_path")
 

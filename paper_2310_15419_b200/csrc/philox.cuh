@@ -90,24 +90,13 @@ __device__ __forceinline__ float uniform24(uint32_t w) {
 // against 300-bit mpmath: <= 0.6 ulp each; ~40 FP64 operations per pair).  Results agree with the
 // libm-based oracle far inside the Gaussian parity bound (1e-14 relative).
 
-// The -2 log table in shared memory, replicated: copy c of row i, component t lives at
-// [(3 i + t) kLogRep + c], and lane l reads copy l mod kLogRep.  A half-warp's 16 lanes then read
-// 16 different copies of any row mix -- 16 consecutive doubles, one per bank pair -- so the random
-// row gather of Box-Muller is free of bank conflicts (the unreplicated table put every row on one
-// of 4 bank groups: ~8-way conflicts).
-constexpr int kLogRep = 16;
-constexpr int kLogTabRepBytes = kBmLogRows * 3 * kLogRep * 8;   // 49.5 KB
-
-// The same table as one copy with 32-byte rows {-2c, 2 L_hi, 2 L_lo, 0} (4.1 KB; STRIDE = 0 above).
+// The -2 log table in shared memory: one copy in 32-byte rows {-2c, 2 L_hi, 2 L_lo, 0} (4.1 KB; STRIDE = 0
+// below), or replicated (STRIDE copies, copy c of row i component t at [(3 i + t) STRIDE + c], lane l
+// reading copy l mod STRIDE: a half-warp's loads of any row mix then hit distinct bank pairs).
 constexpr int kLogTab4Bytes = kBmLogRows * 4 * 8;
 __device__ __forceinline__ void bm_fill_logtab4(double* smem_tab) {
   for (int i = threadIdx.x; i < kBmLogRows * 4; i += blockDim.x)
     smem_tab[i] = (i & 3) == 3 ? 0.0 : kBmLogTab[i >> 2][i & 3];
-}
-
-__device__ __forceinline__ void bm_fill_logtab(double* smem_tab) {
-  for (int i = threadIdx.x; i < kBmLogRows * 3 * kLogRep; i += blockDim.x)
-    smem_tab[i] = (&kBmLogTab[0][0])[i / kLogRep];
 }
 
 // -2 log(u1) for u1 = U 2^-53, U = k1 + 1 an integer in [1, 2^53] passed as an exact double (so
@@ -118,8 +107,8 @@ __device__ __forceinline__ void bm_fill_logtab(double* smem_tab) {
 // (log1p(r) - r) / r^2, truncated where the next term is below 2^-60), the first bracket exact
 // (2^-42 grid).  The factor -2 of Box-Muller is folded into the constants: 11 FP64 operations.
 // tab = row 0, component 0 of this lane's copy; STRIDE = distance between consecutive components
-// (kLogRep for the replicated shared-memory table, 1 for kBmLogTab itself), or STRIDE = 0: one copy in
-// 32-byte rows (bm_fill_logtab4).
+// (the replication of a replicated table, 1 for kBmLogTab itself), or STRIDE = 0: one copy in 32-byte
+// rows (bm_fill_logtab4).
 template <int STRIDE>
 __device__ __forceinline__ double bm_m2log_u53(double U, const double* __restrict__ tab) {
   const unsigned long long b = (unsigned long long)__double_as_longlong(U);

@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 2 : 1) sk_rad_kerne
 template <int DIST> constexpr int pair_E() { return DIST == 3 ? 4 : 2; }
 // logtab / STRIDE: the -2 log table (philox.cuh bm_m2log_u53); sctab / SCREP: the sin / cos table
 // (bm_sincos); Gaussian only.
-template <int DIST, typename T, int STRIDE = kLogRep, int SCREP = kScRep>
+template <int DIST, typename T, int STRIDE = 0, int SCREP = kScRep>
 __device__ __forceinline__ void pair_entries(const uint4 x, T& v0, T& v1, const double* __restrict__ logtab,
                                              const double* __restrict__ sctab = nullptr) {
   if constexpr (DIST == 1) {
@@ -167,7 +167,7 @@ __device__ __forceinline__ void pair_entries(const uint4 x, T& v0, T& v1, const 
   }
 }
 
-template <int DIST, typename T, int STRIDE = kLogRep, int SCREP = kScRep>
+template <int DIST, typename T, int STRIDE = 0, int SCREP = kScRep>
 __device__ __forceinline__ void block_entries(const uint4 x, T (&v)[pair_E<DIST>()], const double* __restrict__ logtab,
                                               const double* __restrict__ sctab = nullptr) {
   if constexpr (DIST == 3) {
@@ -180,17 +180,13 @@ __device__ __forceinline__ void block_entries(const uint4 x, T (&v)[pair_E<DIST>
 // Rows per lane: 16 (uniform, uniform24: kRowsPerWarpPair = 512 per warp) or 8 (Gaussian:
 // kRowsPerWarpGauss = 256; fewer live accumulators leave the Box-Muller chains registers:
 // c3 16.1 -> 15.0 ms, while uniform prefers 16: 2.71 vs 2.82 ms on c2).
-#ifndef SK_GAUSS_SCREP
-#define SK_GAUSS_SCREP kScRep
-#endif
-#ifndef SK_GAUSS_PERSIST
-#define SK_GAUSS_PERSIST 0
-#endif
-#ifndef SK_GAUSS_LOGREP
-#define SK_GAUSS_LOGREP 0
-#endif
-constexpr int kGaussScRep = SK_GAUSS_SCREP;
-constexpr int kGaussLogRep = SK_GAUSS_LOGREP;   // 0: one copy in 32-byte rows; > 0: replicated
+// Gaussian tables in shared memory: the -2 log table as one copy in 32-byte rows (a 16 + 8 byte load
+// per pair; the rows' bank groups conflict, but the conflict-free replicated layout -- 3 loads of
+// 8 bytes from a 49.5 KB table -- measured slower, c3 13.53 vs 13.05 ms), and the sin / cos table
+// replicated kScRep = 8 times (conflict-free 16-byte loads, instead of ~8-wavefront L1 gathers of
+// kBmSinCosTab: 13.05 vs 13.27 ms).  One CTA per item (a persistent grid-stride variant with the
+// tables filled once per SM measured 15.2 ms: its static item assignment leaves the SMs unbalanced).
+constexpr int kGaussScRep = kScRep;
 template <int DIST> constexpr int pair_rows() { return (DIST == 2 ? kRowsPerWarpGauss : kRowsPerWarpPair) / 32; }
 
 // One work item of the uniform / Gaussian / uniform24 kernel (the CTA's 16 warps; `red` = the
@@ -234,7 +230,7 @@ __device__ __forceinline__ void pair_item(const ApplyArgs& P, const Item it, T* 
         for (int h = 0; h < kPairRows / 2; ++h) {
           const uint4 x = s_block(q0 + h, J, P.keys);
           T v0, v1;
-          pair_entries<DIST, T, kGaussLogRep, kGaussScRep>(x, v0, v1, logtab, sctab);
+          pair_entries<DIST, T, 0, kGaussScRep>(x, v0, v1, logtab, sctab);
           acc[2 * h] = fma(v0, a, acc[2 * h]);
           acc[2 * h + 1] = fma(v1, a, acc[2 * h + 1]);
         }
@@ -266,19 +262,15 @@ __device__ __forceinline__ void pair_item(const ApplyArgs& P, const Item it, T* 
     for (int kk = 1; kk < WK; ++kk) s += red[(kk * WD + rwd) * (32 * kPairPad) + off];
     outc[row] = s;
   }
-  __syncthreads();   // `red` is reused by the CTA's next item
 }
 
-// Shared memory: reduction area, then (Gaussian) the replicated -2 log and sin / cos tables.
+// Shared memory: reduction area, then (Gaussian) the -2 log table and the replicated sin / cos table.
 template <int DIST> constexpr int pair_red_bytes() { return kWarps * 32 * (pair_rows<DIST>() + 1) * 8; }
 template <int DIST> constexpr size_t pair_smem_bytes() {
-  return (size_t)pair_red_bytes<DIST>() +
-         (DIST == 2 ? (size_t)(kGaussLogRep ? kLogTabRepBytes : kLogTab4Bytes) + (kGaussScRep ? kScTabRepBytes : 0) : 0);
+  return (size_t)pair_red_bytes<DIST>() + (DIST == 2 ? (size_t)kLogTab4Bytes + kScTabRepBytes : 0);
 }
 
-// Uniform / uniform24: one CTA per item.  Gaussian: persistent, one CTA per SM walking the
-// longest-first item list with stride gridDim.x (a static LPT-like assignment), so the 113 KB of
-// replicated Box-Muller tables are filled once per SM instead of once per item.
+// One CTA per work item (longest first).
 template <int DIST, typename T>
 __global__ void __launch_bounds__(kThreads, 1) sk_pair_kernel(const ApplyArgs P) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -287,16 +279,14 @@ __global__ void __launch_bounds__(kThreads, 1) sk_pair_kernel(const ApplyArgs P)
   const double* sctab = nullptr;
   if constexpr (DIST == 2) {
     double* lt = reinterpret_cast<double*>(smem + pair_red_bytes<DIST>());
-    double* st = reinterpret_cast<double*>(smem + pair_red_bytes<DIST>() + (kGaussLogRep ? kLogTabRepBytes : kLogTab4Bytes));
-    if (kGaussLogRep) bm_fill_logtab(lt); else bm_fill_logtab4(lt);
-    if (kGaussScRep) bm_fill_sctab(st);
+    double* st = reinterpret_cast<double*>(smem + pair_red_bytes<DIST>() + kLogTab4Bytes);
+    bm_fill_logtab4(lt);
+    bm_fill_sctab(st);
     __syncthreads();
-    logtab = kGaussLogRep ? lt + (threadIdx.x & (kLogRep - 1)) : lt;   // this lane's copies
-    sctab = st + 2 * (threadIdx.x & (kScRep - 1));
-    for (int64_t i = blockIdx.x; i < P.n_items; i += gridDim.x) pair_item<DIST, T>(P, P.items[i], red, logtab, sctab);
-  } else {
-    pair_item<DIST, T>(P, P.items[blockIdx.x], red, logtab, sctab);
+    logtab = lt;
+    sctab = st + 2 * (threadIdx.x & (kScRep - 1));       // this lane's copy
   }
+  pair_item<DIST, T>(P, P.items[blockIdx.x], red, logtab, sctab);
 }
 
 // ------------------------------------------------------------------ IEEE fix-up of non-finite columns
@@ -351,14 +341,12 @@ __global__ void sk_validate_rows_kernel(const int32_t* __restrict__ rowidx, int6
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
 }
 
-// grid = one CTA per item, or at most `max_grid` persistent CTAs that stride over the items.
 template <typename K>
-cudaError_t launch_items(K kernel, size_t smem, const ApplyArgs& a, cudaStream_t stream, int64_t max_grid = 0) {
+cudaError_t launch_items(K kernel, size_t smem, const ApplyArgs& a, cudaStream_t stream) {
   if (a.n_items == 0) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const int64_t grid = max_grid > 0 && a.n_items > max_grid ? max_grid : a.n_items;
-  kernel<<<(unsigned)grid, kThreads, smem, stream>>>(a);
+  kernel<<<(unsigned)a.n_items, kThreads, smem, stream>>>(a);
   return cudaGetLastError();
 }
 
@@ -384,8 +372,8 @@ cudaError_t launch_apply(int dist, int dtype, const ApplyArgs& a, cudaStream_t s
                                    : launch_items(sk_pair_kernel<1, float>, pair_smem_bytes<1>(), a, stream);
   if (dist == 3) return dtype == 0 ? launch_items(sk_pair_kernel<3, double>, pair_smem_bytes<3>(), a, stream)
                                    : launch_items(sk_pair_kernel<3, float>, pair_smem_bytes<3>(), a, stream);
-  return dtype == 0 ? launch_items(sk_pair_kernel<2, double>, pair_smem_bytes<2>(), a, stream, SK_GAUSS_PERSIST ? sm_count() : 0)
-                    : launch_items(sk_pair_kernel<2, float>, pair_smem_bytes<2>(), a, stream, SK_GAUSS_PERSIST ? sm_count() : 0);
+  return dtype == 0 ? launch_items(sk_pair_kernel<2, double>, pair_smem_bytes<2>(), a, stream)
+                    : launch_items(sk_pair_kernel<2, float>, pair_smem_bytes<2>(), a, stream);
 }
 
 cudaError_t launch_rad_ieee_fixup(int dtype, const ApplyArgs& a, int64_t n_cols, cudaStream_t stream) {

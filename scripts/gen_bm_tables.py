@@ -167,7 +167,7 @@ def write(rows) -> None:
              "    1.0 / 4.0, 1.0 / 12.0, 1.0 / 32.0, 1.0 / 80.0, 1.0 / 192.0,",
              f"    {-2.0 * LN2_HI!r}, {-2.0 * LN2_LO!r}, {6.283185307179586 * 2.0 ** -53!r} /* fl(2 pi) 2^-53 */}};",
              "", "// {-2 c_i, 2 log(c_i)_hi, 2 log(c_i)_lo}, i = 0..128: the table of log u scaled for -2 log u",
-             "// (bm_m2log_u53; the kernels copy it to shared memory, replicated per lane, kLogRep copies)",
+             "// (bm_m2log_u53; the kernels copy it to shared memory)",
              "constexpr int kBmLogRows = 129;",
              "__device__ const double kBmLogTab[kBmLogRows][3] = {"]
     for c, hi, lo in rows:

@@ -208,11 +208,16 @@ namespace {
 // Algorithm 4 structure ("A will need to be first partitioned into vertical
 // blocks, and within each block, the entries will be stored in CSR format"), the paper's "format
 // conversion".  Blocks are b_n = jki_block_cols(dtype) consecutive
-// columns (all n when n <= b_n: every needed S entry is generated once).  Unless `force`, the exact
-// number of distinct rows per block (device row bitmap) decides whether the RNG saved pays for the
-// scatter: Algorithm 3 generates ceil(d/2) Philox blocks per stored nonzero, Algorithm 4 per nonzero
-// row of a block plus a shared-memory scatter per entry (~kJScatter of a row's generation).
-constexpr double kJScatter = 0.15;
+// columns (all n when n <= b_n: every needed S entry is generated once).  The exact number of
+// distinct rows per block (device row bitmap) decides, per distribution, whether the Philox work
+// saved pays for the shared-memory scatter of every entry (measured r2, ncu instruction counts on c2:
+// generating one S column costs ~26 thread instructions per Â row for uniform -- more for Gaussian --
+// and the scatter ~16 per Â row and entry, against one register FMA in Algorithm 3):
+//   uniform / uniform24: Algorithm 4 when nonzero rows <= 0.45 nnz (reuse >= 2.2),
+//   Gaussian:            Algorithm 4 when nonzero rows <= 0.8 nnz (reuse >= 1.25).
+// The structure is built (unless forced) only when the Gaussian condition holds.
+constexpr double kJReuseUniform = 0.45, kJReuseGaussian = 0.8;
+constexpr double kJScatter = 0.6;   // batch cost in nonzero-row units: rows + kJScatter entries
 
 int build_jki(sk_plan_s* p, const int64_t* h_colptr, bool force, cudaStream_t stream) {
   const int64_t n = p->n, nnz = p->nnz, m = p->m, d = p->d;
@@ -253,7 +258,7 @@ int build_jki(sk_plan_s* p, const int64_t* h_colptr, bool force, cudaStream_t st
   }
   int64_t rows_total = 0;
   for (auto r : brows) rows_total += (int64_t)r;
-  if (!force && !((double)rows_total + kJScatter * (double)nnz < 0.9 * (double)nnz)) return SK_OK;
+  if (!force && !((double)rows_total <= kJReuseGaussian * (double)nnz)) return SK_OK;
 
   // (2) host CSR of every block: counting sort by row, stable in storage (= column) order
   std::vector<int32_t> rows((size_t)nnz);
@@ -560,6 +565,17 @@ int validate_rows_sync(const int32_t* rowidx, int64_t nnz, int64_t m, cudaStream
   return h ? SK_ECSC : SK_OK;
 }
 
+// Algorithm 4 for this distribution?  SK_PAIR_JKI: whenever the plan built it; SK_PAIR_AUTO: when the
+// reuse clears the distribution's bar (build_jki); SK_PAIR_KJI: never.
+bool use_jki(const sk_plan_s* p, int dist) {
+  if (p->jki.n_items == 0 || (dist != SK_UNIFORM && dist != SK_GAUSSIAN)) return false;
+  const int path = pair_path();
+  if (path == SK_PAIR_KJI) return false;
+  if (path == SK_PAIR_JKI) return true;
+  const double bar = dist == SK_GAUSSIAN ? kJReuseGaussian : kJReuseUniform;
+  return (double)p->jki_rows <= bar * (double)p->nnz;
+}
+
 // A side stream + fork / join events per host thread and device (created once).
 struct SidePipe {
   int dev = -1;
@@ -616,7 +632,7 @@ int apply_items(const sk_plan_s* p, uint64_t seed, sk_dist_t dist, const void* v
     }
     // fp32 "T - 2P" sums: columns holding a NaN / Inf rewritten with the IEEE result (a scan of the values)
     if (e == cudaSuccess && p->dtype == SK_F32 && p->n_rad > 0) e = sk::launch_rad_ieee_fixup(1, a, p->n, stream);
-  } else if ((dist == SK_UNIFORM || dist == SK_GAUSSIAN) && p->jki.n_items > 0 && pair_path() != SK_PAIR_KJI) {
+  } else if (use_jki(p, dist)) {
     e = sk::launch_apply_jki((int)dist, (int)p->dtype, a, p->jki, stream);
   } else {
     e = sk::launch_apply((int)dist, (int)p->dtype, a, stream);
@@ -649,7 +665,7 @@ const char* kernel_name(const sk_plan_s* p, int dist) {
     return "sk_rad_kernel<double>";
   }
   const bool f64 = p->dtype == SK_F64;
-  if (p->jki.n_items > 0 && pair_path() != SK_PAIR_KJI && (dist == SK_UNIFORM || dist == SK_GAUSSIAN)) {
+  if (use_jki(p, dist)) {
     if (dist == SK_UNIFORM) return f64 ? "sk_jki_kernel<uniform, double> (Algorithm 4)" : "sk_jki_kernel<uniform, float> (Algorithm 4)";
     return f64 ? "sk_jki_kernel<gaussian, double> (Algorithm 4)" : "sk_jki_kernel<gaussian, float> (Algorithm 4)";
   }

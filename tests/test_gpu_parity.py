@@ -680,18 +680,26 @@ def test_jki_auto_selection(sk):
         pb.close()
 
 
-def test_jki_selected_on_c2_with_exact_row_count(sk):
+def test_jki_plan_on_c2_with_exact_row_count(sk):
     # BASELINE config c2 (1000 distinct uniform rows per column of 1e6): reuse nnz / nnzrows = 1.58
-    # over the whole matrix, so the plan picks Algorithm 4 with b_n = n and generates every needed
-    # S column once: its row count is exactly nnzrows(A)
+    # over the whole matrix, so the plan builds Algorithm 4 with b_n = n and its RNG work is exactly
+    # nnzrows(A); uniform S keeps Algorithm 3 (the scatter costs more than the Philox blocks saved at
+    # this reuse), Gaussian S takes Algorithm 4; both match the oracle on sampled columns
+    import torch
     A = workloads.make_config("c2")
     plan = sk.Plan(_dev(A.colptr), _dev(A.rowidx), 2000, A.m)
     try:
         st = plan.stats()
-        assert st["n_items_jki"] > 0 and "Algorithm 4" in plan.kernel_name("uniform")
-        assert st["jki_nonzero_rows"] == len(np.unique(A.rowidx))
+        assert st["n_items_jki"] > 0 and st["jki_nonzero_rows"] == len(np.unique(A.rowidx))
+        assert "Algorithm 4" not in plan.kernel_name("uniform") and "Algorithm 4" in plan.kernel_name("gaussian")
+        got = plan.apply(_dev(A.vals), 1, "gaussian").T.cpu().numpy()
+        torch.cuda.synchronize()
     finally:
         plan.close()
+    cols = [0, 1, 499, 998, 999]
+    As = A.select_columns(cols)
+    ref, B = oracle.sketch(1, "gaussian", 2000, As.m, As.n, As.colptr, As.rowidx, As.vals, threads=8)
+    _check(got[:, cols], ref, B, TOL["f64"])
 
 
 def test_jki_multiple_blocks_and_split_parts(sk):

@@ -101,13 +101,18 @@ class ClockSampler:
 
 
 def launches_per_apply(plan, dist: str, stats: dict) -> int:
-    """Kernels of the library one sketch_apply launches: for ±1, the tensor-core kernel's two launches
-    (whole columns; K-split parts + non-finite fix-ups) when columns of >= 256 nonzeros exist (fp64),
-    and the SIMT kernel for the other columns; otherwise the one fused kernel of the distribution."""
+    """Kernels of the library one sketch_apply launches.  ±1: the tensor-core kernel with its two small
+    companions (zeroing of the K-split rows, IEEE fix-up of non-finite columns) when columns of 256 ..
+    131071 nonzeros exist (fp64), the SIMT kernel for the other columns, and for fp32 the IEEE fix-up
+    scan.  Uniform / Gaussian: the fused kernel, or Algorithm 4's gather + kernel (+ the finishing sum
+    of split column blocks)."""
     if dist == "rademacher":
-        return 2 * int(stats.get("n_items_f4", 0) > 0) + int(stats["n_items_rad"] > 0)
+        n = 3 * int(stats.get("n_items_f4", 0) > 0) + int(stats["n_items_rad"] > 0)
+        if "sk_rad_kernel<float>" in plan.kernel_name(dist) and stats["n_items_rad"] > 0:
+            n += 1
+        return n
     if stats.get("n_items_jki", 0) > 0 and "Algorithm 4" in plan.kernel_name(dist):
-        return 1
+        return 3
     return int(stats["n_items_pair"] > 0)
 
 
@@ -129,9 +134,11 @@ def load_profile_traffic(config: str, kernel: str):
 
 
 def cpu_baseline(cfg, A, max_wall_s: float = 8.0):
-    """The oracle, as it stands, on the host cores: a bounded sample of whole columns."""
+    """The oracle, as it stands, on the host cores: a bounded sample of whole columns.  (Under torchrun
+    OMP_NUM_THREADS is 1; rank 0 runs this after the timed region while the other ranks wait, so it
+    takes every core of the host.)"""
     import oracle
-    cores = oracle.max_threads()
+    cores = max(oracle.max_threads(), os.cpu_count() or 1)
     lens = np.diff(A.colptr)
     # grow the column sample until the run takes ~max_wall_s (bounded number of doublings)
     ncols = max(1, min(cfg.n, cores))

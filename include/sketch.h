@@ -197,11 +197,11 @@ int sketch_set_rad_f64_path(int path);
  * row of each vertical block of b_n columns -- b_n = 1024 fp64 / 2048 fp32, i.e. all n columns when
  * they fit -- and reused across the row).  The plan counts the distinct
  * rows of every block exactly (device row bitmap) and builds the jki structure (the blocks' CSR, the
- * "format conversion") when nonzero rows <= 0.8 nnz.  SK_PAIR_AUTO then uses jki for SK_GAUSSIAN
- * whenever it was built, and for SK_UNIFORM when nonzero rows <= 0.45 nnz: the scatter of every
- * entry into the block's shared-memory accumulator costs about as much per Â row as generating a
- * uniform S column, so only a reuse of >= 2.2 pays (measured); SK_PAIR_JKI uses jki
- * whenever it was built.  Initialised from SKETCH_PAIR_PATH = auto | kji | jki.  Errors: SK_EINVAL.
+ * "format conversion") when nonzero rows <= 0.26 nnz.  SK_PAIR_AUTO then uses jki for SK_GAUSSIAN;
+ * SK_UNIFORM keeps kji, because the scatter of every entry into the block's shared-memory
+ * accumulator costs more per Â row than generating a uniform S column (measured);
+ * SK_PAIR_JKI uses jki for both whenever it was built (sketch_plan_host_jki always builds it).
+ * Initialised from SKETCH_PAIR_PATH = auto | kji | jki.  Errors: SK_EINVAL.
  */
 typedef enum { SK_PAIR_AUTO = 0, SK_PAIR_KJI = 1, SK_PAIR_JKI = 2 } sk_pair_path_t;
 int sketch_set_pair_path(int path);

@@ -209,15 +209,15 @@ namespace {
 // blocks, and within each block, the entries will be stored in CSR format"), the paper's "format
 // conversion".  Blocks are b_n = jki_block_cols(dtype) consecutive
 // columns (all n when n <= b_n: every needed S entry is generated once).  The exact number of
-// distinct rows per block (device row bitmap) decides, per distribution, whether the Philox work
-// saved pays for the shared-memory scatter of every entry (measured r2, ncu instruction counts on c2:
-// generating one S column costs ~26 thread instructions per Â row for uniform -- more for Gaussian --
-// and the scatter ~16 per Â row and entry, against one register FMA in Algorithm 3):
-//   uniform / uniform24: Algorithm 4 when nonzero rows <= 0.45 nnz (reuse >= 2.2),
-//   Gaussian:            Algorithm 4 when nonzero rows <= 0.8 nnz (reuse >= 1.25).
+// distinct rows per block (device row bitmap) decides whether the Philox work saved pays for the
+// shared-memory scatter of every entry.  Measured (r2, d = 2000): Algorithm 4 costs
+// ~7.3e-6 ms per nonzero row (Gaussian; 4.6e-6 uniform) plus ~3e-6 ms per entry, Algorithm 3 ~5.0e-6
+// ms (Gaussian; 2.8e-6 uniform) per entry, so:
+//   Gaussian: Algorithm 4 when nonzero rows <= 0.26 nnz (reuse >= 3.8; Abnormal A: 3.0 vs 5.2 ms);
+//   uniform:  Algorithm 3 always (even at reuse 1000, Abnormal A: 2.92 vs 2.80 ms) unless forced.
 // The structure is built (unless forced) only when the Gaussian condition holds.
-constexpr double kJReuseUniform = 0.45, kJReuseGaussian = 0.8;
-constexpr double kJScatter = 0.6;   // batch cost in nonzero-row units: rows + kJScatter entries
+constexpr double kJReuseGaussian = 0.26;
+constexpr double kJScatter = 0.4;   // batch cost in nonzero-row units: rows + kJScatter entries
 
 int build_jki(sk_plan_s* p, const int64_t* h_colptr, bool force, cudaStream_t stream) {
   const int64_t n = p->n, nnz = p->nnz, m = p->m, d = p->d;
@@ -572,8 +572,7 @@ bool use_jki(const sk_plan_s* p, int dist) {
   const int path = pair_path();
   if (path == SK_PAIR_KJI) return false;
   if (path == SK_PAIR_JKI) return true;
-  const double bar = dist == SK_GAUSSIAN ? kJReuseGaussian : kJReuseUniform;
-  return (double)p->jki_rows <= bar * (double)p->nnz;
+  return dist == SK_GAUSSIAN && (double)p->jki_rows <= kJReuseGaussian * (double)p->nnz;
 }
 
 // A side stream + fork / join events per host thread and device (created once).

@@ -66,12 +66,16 @@ class _FakePlan:
 
 def test_launch_count_per_kernel_family():
     f4 = _FakePlan("sk_rad_f4_kernel (tcgen05 kind::mxf4) + sk_rad_kernel<double>")
-    assert bench.launches_per_apply(f4, "rademacher", {"n_items_rad": 0, "n_items_pair": 9, "n_items_f4": 3000}) == 2
-    assert bench.launches_per_apply(f4, "rademacher", {"n_items_rad": 5, "n_items_pair": 9, "n_items_f4": 3000}) == 3
+    assert bench.launches_per_apply(f4, "rademacher", {"n_items_rad": 0, "n_items_pair": 9, "n_items_f4": 3000}) == 3
+    assert bench.launches_per_apply(f4, "rademacher", {"n_items_rad": 5, "n_items_pair": 9, "n_items_f4": 3000}) == 4
     assert bench.launches_per_apply(f4, "rademacher", {"n_items_rad": 5, "n_items_pair": 9, "n_items_f4": 0}) == 1
+    f32 = _FakePlan("sk_rad_kernel<float>")
+    assert bench.launches_per_apply(f32, "rademacher", {"n_items_rad": 5, "n_items_pair": 9, "n_items_f4": 0}) == 2
     simt = _FakePlan("sk_pair_kernel<uniform, double>")
     assert bench.launches_per_apply(simt, "uniform", {"n_items_rad": 1, "n_items_pair": 10, "n_items_jki": 0}) == 1
     assert bench.launches_per_apply(simt, "uniform", {"n_items_rad": 0, "n_items_pair": 0, "n_items_jki": 0}) == 0
+    jki = _FakePlan("sk_jki_kernel<gaussian, double> (Algorithm 4)")
+    assert bench.launches_per_apply(jki, "gaussian", {"n_items_rad": 1, "n_items_pair": 10, "n_items_jki": 7}) == 3
 
 
 def test_traffic_lookup_matches_the_committed_capture():

@@ -649,11 +649,13 @@ def test_jki_matches_oracle(sk, dist, dtype, case):
         A.vals = A.vals.astype(np.float32)
     plan = sk.Plan(_dev(A.colptr), _dev(A.rowidx), d, A.m, dtype, jki=True)
     try:
+        sk.set_pair_path("jki")
         st = plan.stats()
         assert st["n_items_jki"] > 0 and "Algorithm 4" in plan.kernel_name(dist)
         got = plan.apply(_dev(A.vals), 19, dist).T.double().cpu().numpy()
         torch.cuda.synchronize()
     finally:
+        sk.set_pair_path("auto")
         plan.close()
     ref, B = oracle.sketch(19, dist, d, A.m, A.n, A.colptr, A.rowidx, A.vals, threads=8)
     _check(got, ref, B, TOL[dtype])
@@ -661,7 +663,8 @@ def test_jki_matches_oracle(sk, dist, dtype, case):
 
 def test_jki_auto_selection(sk):
     # the plan builds the Algorithm 4 structure on its own only when the exact distinct-row count of
-    # its column blocks (b_n = 1024 fp64 columns) makes the saved RNG pay for the scatter
+    # its column blocks (b_n = 1024 fp64 columns) shows enough reuse (rows <= 0.26 nnz), and then uses
+    # it for Gaussian S (measured to win there; uniform S keeps Algorithm 3)
     A = workloads.abnormal_paper("A", m=20000, n=64, seed=1)
     B = workloads.random_csc(200000, 64, 300, seed=2)
     pa = sk.Plan(_dev(A.colptr), _dev(A.rowidx), 256, A.m)
@@ -672,33 +675,39 @@ def test_jki_auto_selection(sk):
         # the RNG work of Algorithm 4 is exactly the distinct rows of every column block
         # (PAPER.md:302-318, 436-442): here one block of all 64 columns
         assert pa.stats()["jki_nonzero_rows"] == len(np.unique(A.rowidx))
+        assert "Algorithm 4" in pa.kernel_name("gaussian") and "Algorithm 4" not in pa.kernel_name("uniform")
+        sk.set_pair_path("jki")
+        assert "Algorithm 4" in pa.kernel_name("uniform")
         sk.set_pair_path("kji")
-        assert "Algorithm 4" not in pa.kernel_name("uniform")
+        assert "Algorithm 4" not in pa.kernel_name("gaussian")
     finally:
         sk.set_pair_path("auto")
         pa.close()
         pb.close()
 
 
-def test_jki_plan_on_c2_with_exact_row_count(sk):
-    # BASELINE config c2 (1000 distinct uniform rows per column of 1e6): reuse nnz / nnzrows = 1.58
-    # over the whole matrix, so the plan builds Algorithm 4 with b_n = n and its RNG work is exactly
-    # nnzrows(A); uniform S keeps Algorithm 3 (the scatter costs more than the Philox blocks saved at
-    # this reuse), Gaussian S takes Algorithm 4; both match the oracle on sampled columns
+def test_jki_on_c2_with_exact_row_count(sk):
+    # BASELINE config c2 (1000 distinct uniform rows per column of 1e6): a forced Algorithm 4 plan
+    # (b_n = n) generates every needed S column exactly once -- its row count is exactly nnzrows(A)
+    # -- and matches the oracle; the automatic plan keeps Algorithm 3 (reuse 1.58 < 3.8)
     import torch
     A = workloads.make_config("c2")
-    plan = sk.Plan(_dev(A.colptr), _dev(A.rowidx), 2000, A.m)
+    auto = sk.Plan(_dev(A.colptr), _dev(A.rowidx), 2000, A.m)
+    assert auto.stats()["n_items_jki"] == 0
+    auto.close()
+    plan = sk.Plan(_dev(A.colptr), _dev(A.rowidx), 2000, A.m, jki=True)
     try:
+        sk.set_pair_path("jki")
         st = plan.stats()
         assert st["n_items_jki"] > 0 and st["jki_nonzero_rows"] == len(np.unique(A.rowidx))
-        assert "Algorithm 4" not in plan.kernel_name("uniform") and "Algorithm 4" in plan.kernel_name("gaussian")
-        got = plan.apply(_dev(A.vals), 1, "gaussian").T.cpu().numpy()
+        got = plan.apply(_dev(A.vals), 1, "uniform").T.cpu().numpy()
         torch.cuda.synchronize()
     finally:
+        sk.set_pair_path("auto")
         plan.close()
     cols = [0, 1, 499, 998, 999]
     As = A.select_columns(cols)
-    ref, B = oracle.sketch(1, "gaussian", 2000, As.m, As.n, As.colptr, As.rowidx, As.vals, threads=8)
+    ref, B = oracle.sketch(1, "uniform", 2000, As.m, As.n, As.colptr, As.rowidx, As.vals, threads=8)
     _check(got[:, cols], ref, B, TOL["f64"])
 
 
@@ -726,11 +735,13 @@ def test_jki_multiple_blocks_and_split_parts(sk):
         for dist, d in (("uniform", 40), ("gaussian", 300)):
             plan = sk.Plan(_dev(A.colptr), _dev(A.rowidx), d, A.m, dtype)
             try:
-                assert plan.stats()["n_items_jki"] > 0, dtype
+                sk.set_pair_path("jki")
+                assert plan.stats()["n_items_jki"] > 0 and "Algorithm 4" in plan.kernel_name(dist), dtype
                 got = plan.apply(_dev(A.vals), 23, dist).T.double().cpu().numpy()
                 got2 = plan.apply(_dev(A.vals), 23, dist).T.double().cpu().numpy()
                 torch.cuda.synchronize()
             finally:
+                sk.set_pair_path("auto")
                 plan.close()
             assert np.array_equal(got, got2)
             ref, B = oracle.sketch(23, dist, d, A.m, A.n, A.colptr, A.rowidx, A.vals, threads=8)

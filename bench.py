@@ -291,6 +291,7 @@ def per_config_lines(torch, sk, dev, names, steps, warmup, peaks, sm_mhz):
                      "bound": rep["bound"], "frac": rep["frac"], "t_roof_ms": rep["t_roof_ms"],
                      "achieved": rep["achieved"], "peak": rep["peak"], "unit": rep["unit"],
                      "kernel": plan.kernel_name(cfg.dist), "dist": cfg.dist, "dtype": cfg.dtype,
+                     "traffic": load_profile_traffic(name, plan.kernel_name(cfg.dist)),
                      "d": cfg.d, "n": cfg.n, "m": cfg.m, "nnz": A.nnz, "nnzrows": nzr,
                      "g_calls_strict": rl["g_calls_strict"], "g_calls_alg3": rl["g_calls_alg3"],
                      "plan_ms": plan_ms, "launches_per_step": launches_per_apply(plan, cfg.dist, st),

@@ -236,8 +236,43 @@ int build_jki(sk_plan_s* p, const int64_t* h_colptr, bool force, cudaStream_t st
     const int64_t c0 = b * bn, c1 = std::min<int64_t>(n, c0 + bn);
     return std::make_pair(h_colptr[c0] - base, h_colptr[c1] - base);
   };
-  // (1) exact distinct rows per block on the device: one row bitmap, one pass per block
+  // (1) exact distinct rows per block on the device: one row bitmap, one pass per block.  Unless
+  // forced, a first pass over at most 2^23 entries (a column prefix of the blocks) skips matrices whose
+  // reuse cannot reach the bar: extrapolating its repeats linearly over the whole block must reach it.
   std::vector<unsigned long long> brows((size_t)NB, 0);
+  if (!force) {
+    int64_t tot_s = 0, tot_all = 0;
+    std::vector<std::pair<int64_t, int64_t>> pre;
+    for (int64_t b = 0; b < NB; ++b) {
+      const auto pr = block_range(b);
+      const int64_t take = std::min<int64_t>(pr.second - pr.first, std::max<int64_t>(1, (int64_t(1) << 23) / NB));
+      pre.emplace_back(pr.first, pr.first + take);
+      tot_s += take;
+      tot_all += pr.second - pr.first;
+    }
+    if (tot_s < tot_all) {
+      const size_t words = (size_t)((m + 31) / 32);
+      uint32_t* bitmap = nullptr;
+      unsigned long long* cnt = nullptr;
+      std::vector<unsigned long long> h((size_t)NB, 0);
+      SK_CUDA(cudaMallocAsync((void**)&bitmap, std::max<size_t>(words, 1) * 4, stream));
+      cudaError_t e = cudaMallocAsync((void**)&cnt, (size_t)NB * 8, stream);
+      if (e == cudaSuccess) e = cudaMemsetAsync(cnt, 0, (size_t)NB * 8, stream);
+      for (int64_t b = 0; b < NB && e == cudaSuccess; ++b) {
+        e = cudaMemsetAsync(bitmap, 0, std::max<size_t>(words, 1) * 4, stream);
+        if (e == cudaSuccess) e = sk::launch_distinct_rows(p->rowidx, pre[(size_t)b].first, pre[(size_t)b].second, bitmap, cnt + b, stream);
+      }
+      if (e == cudaSuccess) e = cudaMemcpyAsync(h.data(), cnt, (size_t)NB * 8, cudaMemcpyDeviceToHost, stream);
+      cudaFreeAsync(bitmap, stream);
+      if (cnt) cudaFreeAsync(cnt, stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+      if (e != cudaSuccess) return cuda_fail(e, "jki sample");
+      int64_t rows_s = 0;
+      for (auto r : h) rows_s += (int64_t)r;
+      const double repeats = (double)(tot_s - rows_s) * (double)tot_all / (double)std::max<int64_t>(tot_s, 1);
+      if ((double)tot_all - repeats > kJReuseGaussian * (double)tot_all) return SK_OK;
+    }
+  }
   {
     const size_t words = (size_t)((m + 31) / 32);
     uint32_t* bitmap = nullptr;

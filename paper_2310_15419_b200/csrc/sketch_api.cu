@@ -154,9 +154,11 @@ int rad_f64_path() {
 }
 
 // Shortest column the tensor-core kernel takes (shorter ones go to the SIMT kernel, whose CTA has
-// no TMEM / barrier / pipeline fill and drain to amortise).  SKETCH_F4_MIN_COL (tuning only).
+// no TMEM / barrier / pipeline fill and drain to amortise): the measured crossover at d = 2000
+// (scripts/f4_threshold_sweep.py, profiles/r02_f4_threshold_sweep.txt: fp4 / SIMT time 1.16 at
+// L = 1024, 0.94 at 1536).  SKETCH_F4_MIN_COL (tuning only) overrides it.
 int64_t f4_min_column() {
-  static const int64_t v = [] { const char* e = getenv("SKETCH_F4_MIN_COL"); return e ? std::max<int64_t>(1, atoll(e)) : 256; }();
+  static const int64_t v = [] { const char* e = getenv("SKETCH_F4_MIN_COL"); return e ? std::max<int64_t>(1, atoll(e)) : 1280; }();
   return v;
 }
 

@@ -61,9 +61,6 @@ constexpr int kF4Stage = kF4Tiles * kF4ATileS + kF4Sub * kF4BSub;
 constexpr uint32_t kF4SfCol = 448;                // scale factors: TMEM columns [448, 512)
 // try_wait suspend-time hint (ns): a waiting warp sleeps until the phase completes instead of
 // spinning through SYNCS / BRA / YIELD loops that take issue slots from the producers.
-#ifndef SK_F4_WAIT1
-#define SK_F4_WAIT1 0
-#endif
 #ifndef SK_SUSPEND_NS
 #define SK_SUSPEND_NS 1000000
 #endif
@@ -91,9 +88,6 @@ __device__ __forceinline__ void f4_mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void f4_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(s_u32(bar)) : "memory");
 }
-// Warp-wide wait with one observer: lane 0 polls the barrier, the warp then reconverges (bar.warp.sync
-// orders memory among its lanes), so 31 lanes do not each poll the same shared-memory word.
-__device__ __forceinline__ void f4_wait1(uint64_t* bar, uint32_t parity, int lane);
 __device__ __forceinline__ void f4_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
@@ -101,16 +95,6 @@ __device__ __forceinline__ void f4_wait(uint64_t* bar, uint32_t parity) {
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
       "@!P1 bra WAIT_%=;\n\t}"
       :: "r"(s_u32(bar)), "r"(parity), "r"(kSuspendNs) : "memory");
-}
-
-__device__ __forceinline__ void f4_wait1(uint64_t* bar, uint32_t parity, int lane) {
-#if SK_F4_WAIT1
-  if (lane == 0) f4_wait(bar, parity);
-  __syncwarp();
-#else
-  (void)lane;
-  f4_wait(bar, parity);
-#endif
 }
 
 // K-major, no-swizzle smem descriptor: core matrix = 8 rows x 16 B; LBO = stride between the two
@@ -285,7 +269,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
     for (int ss = 0; ss < nsup; ++ss) {
       const int stage = ss % kF4Stages, use = ss / kF4Stages;
       const int jslot = ss % kF4JSlots;
-      f4_wait1(&sh.jfull[jslot], (ss / kF4JSlots) & 1, lane);
+      f4_wait(&sh.jfull[jslot], (ss / kF4JSlots) & 1);
       uint32_t jv[kMine];
 #pragma unroll
       for (int i = 0; i < kMine; ++i) jv[i] = sh.js[jslot][64 * (kc + i) + jl];
@@ -300,7 +284,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
         x[4 * i + 0] = xb.x; x[4 * i + 1] = xb.y; x[4 * i + 2] = xb.z; x[4 * i + 3] = xb.w;
       }
       if (!(dbg & 32)) f4_transpose<4 * kMine>(x, lane);   // lane r: row 32qq + r over 32 nonzeros
-      if (use > 0) f4_wait1(&sh.empty[stage], (use - 1) & 1, lane);
+      if (use > 0) f4_wait(&sh.empty[stage], (use - 1) & 1);
       if (!(dbg & 1)) {
         const uint32_t tile = s_u32(stages + stage * kF4Stage) + (uint32_t)(t * kF4ATileS) + f4_off(lane, h);
 #pragma unroll
@@ -324,7 +308,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
       uint32_t x[2 * kF4Sub];
       int nval[kF4Sub];
       const int jslot = ss % kF4JSlots;
-      f4_wait1(&sh.jfull[jslot], (ss / kF4JSlots) & 1, lane);
+      f4_wait(&sh.jfull[jslot], (ss / kF4JSlots) & 1);
       double vv[kF4Sub];
 #pragma unroll
       for (int sub = 0; sub < kF4Sub; ++sub) vv[sub] = sh.vs[jslot][64 * sub + 32 * h + lane];
@@ -347,7 +331,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
         x[2 * sub + 1] = ~(uint32_t)(U >> 32);
       }
       f4_transpose<2 * kF4Sub>(x, lane);           // lane r: bit r (and 32 + r) of U per K-step
-      if (use > 0) f4_wait1(&sh.empty[stage], (use - 1) & 1, lane);
+      if (use > 0) f4_wait(&sh.empty[stage], (use - 1) & 1);
       if (!(dbg & 8)) {
 #pragma unroll
         for (int sub = 0; sub < kF4Sub; ++sub) {
@@ -370,7 +354,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
     // cp.async.mbarrier.arrive.noinc that fires when they land; it only blocks on ring space.
     for (int ss = 0; ss < nsup; ++ss) {
       const int slot = ss % kF4JSlots, use = ss / kF4JSlots;
-      if (use > 0) f4_wait1(&sh.jempty[slot], (use - 1) & 1, lane);
+      if (use > 0) f4_wait(&sh.jempty[slot], (use - 1) & 1);
 #pragma unroll
       for (int e = 0; e < 2 * kF4Sub; ++e) {
         const int64_t p = pb + (int64_t)ss * (64 * kF4Sub) + 32 * e + lane;
@@ -421,7 +405,7 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
   // ===================== epilogue: warps 0..11 read D (lane quarter = warp % 4) =====================
   if (warp < kF4Producers) {
     if (nsteps > 0) {
-      f4_wait1(&sh.done, 0, lane);
+      f4_wait(&sh.done, 0);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     }
     const int qw = warp & 3;

@@ -170,12 +170,12 @@ def test_rad_f64_kernel_paths(sk, path):
     # relative to the rest, unsorted rows with duplicates, explicit zeros and huge / tiny values
     try:
         sk.set_rad_f64_path(path)
-        # (columns of >= 256 nonzeros run on the tensor cores, the others on the SIMT kernel)
-        cases = [workloads.random_csc(50000, 40, 300, seed=2),
-                 workloads.random_csc(30000, 12, [0, 500, 0, 0, 640, 1, 0, 3300, 0, 2, 0, 100], seed=5),
+        # (columns of 1280 .. 131071 nonzeros run on the tensor cores, the others on the SIMT kernel)
+        cases = [workloads.random_csc(50000, 40, 1300, seed=2),
+                 workloads.random_csc(30000, 12, [0, 500, 0, 0, 1640, 1, 0, 3300, 0, 2, 0, 1279], seed=5),
                  workloads.random_csc(200000, 24, [20000] + [10] * 23, seed=6),
-                 workloads.random_csc(5000, 10, 400, seed=7, sorted_rows=False, duplicates=True)]
-        wide = workloads.random_csc(40000, 6, 700, seed=17)
+                 workloads.random_csc(5000, 10, 1400, seed=7, sorted_rows=False, duplicates=True)]
+        wide = workloads.random_csc(40000, 6, 1700, seed=17)
         wide.vals = wide.vals * np.logspace(-200, 200, wide.nnz)       # dynamic range per column
         wide.vals[::7] = 0.0
         cases.append(wide)
@@ -192,7 +192,7 @@ def test_nan_poisons_only_its_column(sk, path):
     # a NaN value makes its whole column NaN (NaN * ±1 = NaN in every row, as in the oracle); the
     # other columns are unaffected.  (fmax-based column scans would drop the NaN: the tensor-core
     # kernels take max |a| on the IEEE bit patterns, NaN > Inf > finite.)
-    A = workloads.random_csc(50000, 6, 400, seed=41)
+    A = workloads.random_csc(50000, 6, 1500, seed=41)
     A.vals[A.colptr[2] + 5] = np.nan
     try:
         sk.set_rad_f64_path(path)
@@ -295,12 +295,12 @@ def test_f4_long_columns_next_to_tensor_columns(sk):
     # stream, while every other column stays on sk_rad_f4_kernel; results match the oracle and two
     # runs are bit-identical
     import torch
-    lens = [300000, 131072, 131071, 3000, 700, 90, 255, 256]
+    lens = [300000, 131072, 131071, 3000, 1279, 1280, 700, 90]
     A = workloads.random_csc(400000, len(lens), lens, seed=29)
     plan = sk.Plan(_dev(A.colptr), _dev(A.rowidx), 1300, A.m, "f64")
     try:
         st = plan.stats()
-        assert st["n_cols_f4"] == 4 and st["n_items_rad"] > 0, st
+        assert st["n_cols_f4"] == 3 and st["n_items_rad"] > 0, st
         assert "sk_rad_f4_kernel" in plan.kernel_name("rademacher")
         vals = _dev(A.vals)
         o1 = plan.apply(vals, 6, "rademacher").T.cpu().numpy()
@@ -316,7 +316,7 @@ def test_f4_long_columns_next_to_tensor_columns(sk):
 @pytest.mark.parametrize("case", range(16))
 def test_randomized_shapes_match_oracle(sk, case):
     # seeded random shapes through the default kernel selection: m, n, column lengths (empty,
-    # short, >= 256 so the tensor-core path is eligible, occasionally one very long column), d
+    # short, >= 1280 so the tensor-core path is eligible, occasionally one very long column), d
     # (ragged, tiny, > 2048), dtype, distribution and a nonzero row offset
     rng = np.random.default_rng(1000 + case)
     m = int(rng.integers(1, 60000))
@@ -325,12 +325,12 @@ def test_randomized_shapes_match_oracle(sk, case):
     if kind == 0:
         lens = rng.integers(0, 40, n)
     elif kind == 1:
-        lens = rng.integers(256, 700, n)
+        lens = rng.integers(1280, 2000, n)
     elif kind == 2:
         lens = rng.integers(0, 900, n)
         lens[int(rng.integers(0, n))] = min(m, 5000)
     else:
-        lens = rng.integers(300, 400, n)
+        lens = rng.integers(1200, 1400, n)
     lens = [int(min(L, m)) for L in lens]
     d = int(rng.choice([1, 2, 127, 129, 700, 1025, 2049, int(rng.integers(1, 2200))]))
     dtype = np.float32 if case % 3 == 2 else np.float64
@@ -367,12 +367,12 @@ def test_repeated_runs_are_bit_identical(sk, dist, dtype):
 def test_extreme_value_scales(sk, path):
     # columns whose values are all subnormal, all near the top of the fp64 range, or mix both with
     # exact zeros: the tensor-core paths scale each column by 2^(61-E) in two exact factors
-    A = workloads.random_csc(30000, 5, 400, seed=41)
+    A = workloads.random_csc(30000, 5, 1400, seed=41)
     v = A.vals.copy()
     s = [slice(A.colptr[k], A.colptr[k + 1]) for k in range(5)]
     v[s[0]] *= 1e-310                                  # subnormal
-    v[s[1]] *= 1e300                                   # huge (|Â| stays < 1e308 for 400 terms)
-    v[s[2]] = np.where(np.arange(400) % 2 == 0, v[s[2]] * 1e-300, v[s[2]] * 1e200)
+    v[s[1]] *= 1e300                                   # huge (|Â| stays < 1e308 for 1400 terms)
+    v[s[2]] = np.where(np.arange(1400) % 2 == 0, v[s[2]] * 1e-300, v[s[2]] * 1e200)
     v[s[3]] = 0.0                                      # all explicit zeros
     v[s[4]][::3] = 0.0
     A.vals = v

@@ -34,8 +34,8 @@ def _free_port():
 
 
 def _matrix():
-    # > 256 nonzeros in most columns (tensor-core ±1 path) plus short and empty columns (SIMT path)
-    lens = [400 + 37 * k for k in range(24)] + [0, 3, 90, 255]
+    # >= 1280 nonzeros in most columns (tensor-core ±1 path) plus short and empty columns (SIMT path)
+    lens = [1000 + 60 * k for k in range(24)] + [0, 3, 90, 255]
     return workloads.random_csc(120_000, len(lens), lens, seed=51)
 
 

@@ -34,8 +34,9 @@ def _free_port():
 
 
 def _matrix():
-    # >= 1280 nonzeros in most columns (tensor-core ±1 path) plus short and empty columns (SIMT path)
-    lens = [1000 + 60 * k for k in range(24)] + [0, 3, 90, 255]
+    # columns long enough that each rank's row shard keeps >= 1280 nonzeros (tensor-core ±1 path), plus
+    # mid-length, short and empty columns (SIMT path)
+    lens = [2700 + 100 * k for k in range(12)] + [300 + 50 * k for k in range(12)] + [0, 3, 90, 255]
     return workloads.random_csc(120_000, len(lens), lens, seed=51)
 
 

@@ -140,15 +140,26 @@ def sketch_col_sharded(colptr_local, rowidx_local, vals_local, d: int, m: int, s
     return plan.apply(vals_local, seed, dist_name, out=out), plan
 
 
-def overlap_groups(colptr, groups: int):
-    """Column groups [g_0 = 0, ..., g_G = n] with balanced nnz for the overlapped reduction."""
+def overlap_groups(colptr, groups: int, group=None, device=None):
+    """Column groups [g_0 = 0, ..., g_G = n] with balanced nnz for the overlapped reduction.  Under an
+    initialised process group the per-column counts are summed across ranks first, so every rank
+    cuts the same groups (each group is one collective of identical size on every rank)."""
+    colptr = np.asarray(colptr, dtype=np.int64)
+    import torch.distributed as dist
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        import torch
+        cnt = torch.from_numpy(np.diff(colptr))
+        if dist.get_backend(group) == "nccl":
+            cnt = cnt.to(device if device is not None else torch.device("cuda", torch.cuda.current_device()))
+        dist.all_reduce(cnt, op=dist.ReduceOp.SUM, group=group)
+        colptr = np.concatenate([[0], np.cumsum(cnt.cpu().numpy())])
     return balanced_col_shards(colptr, groups)
 
 
 def sketch_row_sharded_overlapped(colptr_h, colptr, rowidx, vals, d: int, m_local: int, row_offset: int,
                                   seed: int, dist_name: str, groups: int = 4, group=None, out=None):
     """Row-sharded sketch whose cross-GPU sum overlaps the compute: the columns are sketched in
-    `groups` nnz-balanced groups on the current stream, and each group's all_reduce is issued on a
+    `groups` nnz-balanced groups (the same on every rank) on the current stream, and each group's all_reduce is issued on a
     side stream as soon as that group's kernel is done.  colptr_h is the host copy of colptr.
     Returns out (n, d) after all reductions completed on the current stream."""
     import torch
@@ -157,7 +168,7 @@ def sketch_row_sharded_overlapped(colptr_h, colptr, rowidx, vals, d: int, m_loca
     n = len(colptr_h) - 1
     if out is None:
         out = torch.empty((n, d), dtype=vals.dtype, device=vals.device)
-    bounds = overlap_groups(colptr_h, groups)
+    bounds = overlap_groups(colptr_h, groups, group=group, device=vals.device)
     comp = torch.cuda.current_stream()
     comm = torch.cuda.Stream()
     dtype = "f64" if vals.dtype == torch.float64 else "f32"

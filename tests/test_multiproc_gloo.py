@@ -157,3 +157,38 @@ def test_balanced_col_shards_split_nnz():
         parts = [int(colptr[b[g + 1]] - colptr[b[g]]) for g in range(world)]
         assert sum(parts) == int(colptr[-1])
         assert max(parts) - min(parts) <= 2 * int(lens.max())
+
+
+# ---------------------------------------------------------------- overlapped reduce: same groups on every rank
+
+def _groups_worker(rank, world, port, q):
+    from paper_2310_15419_b200.distributed import overlap_groups
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # row shards whose per-column nnz differ by rank: rank 0's mass sits in the first columns,
+        # rank 1's in the last, so locally balanced groups would differ and the collectives mismatch
+        lens = [4000, 10, 10, 10, 10, 10, 10, 4000] if rank == 0 else [10, 10, 10, 10, 10, 10, 3000, 9000]
+        colptr = np.concatenate([[0], np.cumsum(lens)])
+        q.put((rank, overlap_groups(colptr, 4)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_overlap_groups_agree_across_ranks():
+    from paper_2310_15419_b200.distributed import balanced_col_shards
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_groups_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0] == res[1]
+    total = np.array([4010, 20, 20, 20, 20, 20, 3010, 13000])
+    assert res[0] == balanced_col_shards(np.concatenate([[0], np.cumsum(total)]), 4)

@@ -85,6 +85,7 @@ typedef struct {
     int64_t n_items_f4_split;  /* tensor-core items that are halves of a last-wave item split along K */
     int64_t n_items_f4;        /* CTAs of the tensor-core kernel of one SK_RADEMACHER apply */
     int64_t n_cols_f4;         /* columns on the tensor-core kernel (the others: n_items_rad SIMT CTAs) */
+    int64_t jki_block_cols;    /* b_n of the Algorithm 4 column blocks (384 f64, 768 f32), 0 if not built */
 } sk_stats_t;
 
 /*
@@ -194,12 +195,13 @@ int sketch_set_rad_f64_path(int path);
 /*
  * Kernel selection for SK_UNIFORM / SK_GAUSSIAN (process-wide): Algorithm 3 (kji: S[:, j] regenerated
  * per stored nonzero) or Algorithm 4 (jki: S[:, j] regenerated once per nonzero
- * row of each vertical block of b_n columns -- b_n = 1024 fp64 / 2048 fp32, i.e. all n columns when
+ * row of each vertical block of b_n columns -- b_n = 384 fp64 / 768 fp32, i.e. all n columns when
  * they fit -- and reused across the row).  The plan counts the distinct
  * rows of every block exactly (device row bitmap) and builds the jki structure (the blocks' CSR, the
- * "format conversion") when nonzero rows <= 0.26 nnz.  SK_PAIR_AUTO then uses jki for SK_GAUSSIAN;
- * SK_UNIFORM keeps kji, because the scatter of every entry into the block's shared-memory
- * accumulator costs more per Â row than generating a uniform S column (measured);
+ * "format conversion") when nonzero rows <= 0.40 nnz (fp64; 0.55 fp32).  SK_PAIR_AUTO then uses jki
+ * where the measured costs favour it: SK_GAUSSIAN at rows <= 0.40 nnz (fp64) / 0.55
+ * (fp32), SK_UNIFORM at rows <= 0.10 nnz (fp64) / 0.30 (fp32) -- the scatter of every entry into the
+ * block's shared-memory accumulator costs about as much as generating a uniform S entry;
  * SK_PAIR_JKI uses jki for both whenever it was built (sketch_plan_host_jki always builds it).
  * Initialised from SKETCH_PAIR_PATH = auto | kji | jki.  Errors: SK_EINVAL.
  */

@@ -72,10 +72,18 @@ int f4_tiles_per_cta();
 // Algorithm 4 (jki) with full row reuse (sketch_jki.cu): vertical blocks of up to b_n columns, each
 // stored row by row; a work item = (tile of kJRows rows of Â, block, range of the block's batches of
 // up to kJBatch nonzero rows / kJBatchEnt entries).
-constexpr int kJRows = 16;
+constexpr int kJRows = 32;
 constexpr int kJBatch = 128;
-constexpr int kJBatchEnt = 1024;
+constexpr int kJBatchEnt = 512;
 constexpr int kJOwners = 32;       // column owners (half-warps): column k of a block -> k mod 32
+constexpr int kJOwnStride = 34;    // owner offsets per batch (33 used; 4-byte multiple for cp.async)
+// An entry's descriptor as the kernel consumes it: byte offset of its accumulator row pair
+// (column within block x 16 pairs x pair bytes, < 2^17) | byte offset of its S row (row slot within
+// the batch x 16 pairs x pair bytes) << 17.  Pair bytes: 16 (f64), 8 (f32).
+inline uint32_t jki_desc(uint32_t col, uint32_t slot, int dtype) {
+  const uint32_t row_bytes = (kJRows / 2) * (dtype == 0 ? 16u : 8u);
+  return col * row_bytes | (slot * row_bytes) << 17;
+}
 struct JBatch {
   int64_t ent0;        // first entry (in ent)
   int32_t row0;        // first nonzero row (in row_j)
@@ -94,10 +102,10 @@ struct JkiPlanView {
   const JItem* items;
   int64_t n_items;
   const JBatch* batches;
-  const uint16_t* own;       // [n_batches][kJOwners + 1]: entry ranges of the owners within the batch
+  const uint16_t* own;       // [n_batches][kJOwnStride]: entry ranges of the owners within the batch
   const int32_t* row_j;      // local row index of each nonzero row of each block
   const uint32_t* ent_p;     // value index of each entry (block CSR order)
-  const uint32_t* ent_desc;  // column within block | row slot within batch << 16
+  const uint32_t* ent_desc;  // jki_desc(column within block, row slot within batch, dtype)
   const int32_t* blk_slot;   // [n_blocks + 1]: workspace slots of block b ([s0, s1), empty if unsplit)
   int64_t n;                 // columns of the plan
   int32_t bn;                // columns per block
@@ -105,6 +113,9 @@ struct JkiPlanView {
   int64_t n_slots;           // workspace slots (bn x d each)
   int64_t n_ent;             // entries (= nnz)
 };
+// Stream-ordered scratch from the library's own memory pool on the current device (its release
+// threshold keeps freed memory mapped, so per-apply scratch does not re-map pages every call).
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t stream);
 int jki_block_cols(int dtype);
 size_t jki_smem(int dtype, int bn);
 cudaError_t launch_apply_jki(int dist, int dtype, const ApplyArgs& a, const JkiPlanView& J, cudaStream_t stream);

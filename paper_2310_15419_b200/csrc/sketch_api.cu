@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -23,6 +24,39 @@
 #include "philox.cuh"
 
 using sk::Item;
+
+namespace sk {
+// One memory pool per device for the library's stream-ordered scratch (jki values / workspace, the
+// device copies of sketch_apply_host).  Its release threshold is unlimited: freed blocks stay mapped
+// for the next call instead of being returned to the driver at every synchronisation (the default
+// pool's threshold 0 re-maps hundreds of MB per call).  The pool holds the high-water mark of the
+// scratch in flight at once.
+cudaError_t scratch_alloc(void** ptr, size_t bytes, cudaStream_t stream) {
+  static std::mutex mu;
+  static cudaMemPool_t pools[128] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 128) return cudaErrorInvalidDevice;
+  cudaMemPool_t pool;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!pools[dev]) {
+      cudaMemPoolProps props{};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = dev;
+      e = cudaMemPoolCreate(&pools[dev], &props);
+      if (e != cudaSuccess) { pools[dev] = nullptr; return e; }
+      uint64_t keep = UINT64_MAX;
+      e = cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep);
+      if (e != cudaSuccess) return e;
+    }
+    pool = pools[dev];
+  }
+  return cudaMallocFromPoolAsync(ptr, bytes, pool, stream);
+}
+}  // namespace sk
 
 namespace {
 
@@ -212,13 +246,17 @@ namespace {
 // conversion".  Blocks are b_n = jki_block_cols(dtype) consecutive
 // columns (all n when n <= b_n: every needed S entry is generated once).  The exact number of
 // distinct rows per block (device row bitmap) decides whether the Philox work saved pays for the
-// shared-memory scatter of every entry.  Measured (r2, d = 2000): Algorithm 4 costs
-// ~7.3e-6 ms per nonzero row (Gaussian; 4.6e-6 uniform) plus ~3e-6 ms per entry, Algorithm 3 ~5.0e-6
-// ms (Gaussian; 2.8e-6 uniform) per entry, so:
-//   Gaussian: Algorithm 4 when nonzero rows <= 0.26 nnz (reuse >= 3.8; Abnormal A: 3.0 vs 5.2 ms);
-//   uniform:  Algorithm 3 always (even at reuse 1000, Abnormal A: 2.92 vs 2.80 ms) unless forced.
-// The structure is built (unless forced) only when the Gaussian condition holds.
-constexpr double kJReuseGaussian = 0.26;
+// shared-memory scatter of every entry.  Measured (r2 reuse sweep, d = 2000, n = 1000 columns of 1000
+// nonzeros drawn from R rows, profiles/r02_jki_reuse_sweep.jsonl): Algorithm 4 costs
+// ~2.2 ms per 1e6 entries (f32 ~1.4: the scatter is bound by shared-memory bandwidth, 24 B per row x
+// entry in fp64) plus 4.3e-6 ms per nonzero row (uniform; Gaussian 6.6e-6; f32 4.6e-6 / 6.8e-6),
+// Algorithm 3 2.72 ms per 1e6 entries (uniform; Gaussian 4.94; f32 2.77 / 5.61).  Algorithm 4 is
+// chosen when nonzero rows <= kJRowsPerNnz[dtype][dist] x nnz:
+//   f64: uniform 0.10 (reuse >= 10), Gaussian 0.40 (reuse >= 2.5);
+//   f32: uniform 0.30, Gaussian 0.55.
+// The structure is built (unless forced) only when the dtype's Gaussian bar (the loosest) holds.
+constexpr double kJRowsPerNnz[2][2] = {{0.10, 0.40}, {0.30, 0.55}};   // [f64, f32][uniform, Gaussian]
+double jki_bar(int dtype, int dist) { return kJRowsPerNnz[dtype == SK_F64 ? 0 : 1][dist == SK_GAUSSIAN ? 1 : 0]; }
 constexpr double kJScatter = 0.4;   // batch cost in nonzero-row units: rows + kJScatter entries
 
 int build_jki(sk_plan_s* p, const int64_t* h_colptr, bool force, cudaStream_t stream) {
@@ -257,8 +295,8 @@ int build_jki(sk_plan_s* p, const int64_t* h_colptr, bool force, cudaStream_t st
       uint32_t* bitmap = nullptr;
       unsigned long long* cnt = nullptr;
       std::vector<unsigned long long> h((size_t)NB, 0);
-      SK_CUDA(cudaMallocAsync((void**)&bitmap, std::max<size_t>(words, 1) * 4, stream));
-      cudaError_t e = cudaMallocAsync((void**)&cnt, (size_t)NB * 8, stream);
+      SK_CUDA(sk::scratch_alloc((void**)&bitmap, std::max<size_t>(words, 1) * 4, stream));
+      cudaError_t e = sk::scratch_alloc((void**)&cnt, (size_t)NB * 8, stream);
       if (e == cudaSuccess) e = cudaMemsetAsync(cnt, 0, (size_t)NB * 8, stream);
       for (int64_t b = 0; b < NB && e == cudaSuccess; ++b) {
         e = cudaMemsetAsync(bitmap, 0, std::max<size_t>(words, 1) * 4, stream);
@@ -272,15 +310,15 @@ int build_jki(sk_plan_s* p, const int64_t* h_colptr, bool force, cudaStream_t st
       int64_t rows_s = 0;
       for (auto r : h) rows_s += (int64_t)r;
       const double repeats = (double)(tot_s - rows_s) * (double)tot_all / (double)std::max<int64_t>(tot_s, 1);
-      if ((double)tot_all - repeats > kJReuseGaussian * (double)tot_all) return SK_OK;
+      if ((double)tot_all - repeats > jki_bar((int)p->dtype, SK_GAUSSIAN) * (double)tot_all) return SK_OK;
     }
   }
   {
     const size_t words = (size_t)((m + 31) / 32);
     uint32_t* bitmap = nullptr;
     unsigned long long* cnt = nullptr;
-    SK_CUDA(cudaMallocAsync((void**)&bitmap, std::max<size_t>(words, 1) * 4, stream));
-    cudaError_t e = cudaMallocAsync((void**)&cnt, (size_t)NB * 8, stream);
+    SK_CUDA(sk::scratch_alloc((void**)&bitmap, std::max<size_t>(words, 1) * 4, stream));
+    cudaError_t e = sk::scratch_alloc((void**)&cnt, (size_t)NB * 8, stream);
     if (e == cudaSuccess) e = cudaMemsetAsync(cnt, 0, (size_t)NB * 8, stream);
     for (int64_t b = 0; b < NB && e == cudaSuccess; ++b) {
       const auto pr = block_range(b);
@@ -295,7 +333,7 @@ int build_jki(sk_plan_s* p, const int64_t* h_colptr, bool force, cudaStream_t st
   }
   int64_t rows_total = 0;
   for (auto r : brows) rows_total += (int64_t)r;
-  if (!force && !((double)rows_total <= kJReuseGaussian * (double)nnz)) return SK_OK;
+  if (!force && !((double)rows_total <= jki_bar((int)p->dtype, SK_GAUSSIAN) * (double)nnz)) return SK_OK;
 
   // (2) host CSR of every block: counting sort by row, stable in storage (= column) order
   std::vector<int32_t> rows((size_t)nnz);
@@ -339,6 +377,7 @@ int build_jki(sk_plan_s* p, const int64_t* h_colptr, bool force, cudaStream_t st
       for (int32_t e = 0; e < cur.nent; ++e) sorted[pos[(ent[first + e].y & 0xFFFFu) % sk::kJOwners]++] = ent[first + e];
       std::copy(sorted.begin(), sorted.end(), ent.begin() + (int64_t)first);
       own.insert(own.end(), off, off + sk::kJOwners + 1);
+      own.resize(own.size() + (sk::kJOwnStride - sk::kJOwners - 1), 0);
       bcost.push_back((double)cur.nrows + kJScatter * (double)cur.nent);
       batches.push_back(cur);
       cur = sk::JBatch{};
@@ -414,7 +453,10 @@ int build_jki(sk_plan_s* p, const int64_t* h_colptr, bool force, cudaStream_t st
   }
   // (4) one device block: items | batches | own | row_j | ent_p | ent_desc | blk_slot
   std::vector<uint32_t> ent_p(ent.size()), ent_desc(ent.size());
-  for (size_t e = 0; e < ent.size(); ++e) { ent_p[e] = ent[e].x; ent_desc[e] = ent[e].y; }
+  for (size_t e = 0; e < ent.size(); ++e) {
+    ent_p[e] = ent[e].x;
+    ent_desc[e] = sk::jki_desc(ent[e].y & 0xFFFFu, ent[e].y >> 16, (int)p->dtype);
+  }
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   const size_t b_items = al(items.size() * sizeof(sk::JItem)), b_bat = al(batches.size() * sizeof(sk::JBatch)),
                b_own = al(own.size() * 2), b_rowj = al(row_j.size() * 4), b_ent = al(ent.size() * 4),
@@ -566,7 +608,7 @@ int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
       o += sc->items.size() * sizeof(Item);
     }
     if (!f4.empty()) std::memcpy(h + p->off_f4, f4.data(), f4.size() * sizeof(sk::TcItem));
-    cudaError_t e = defer_upload ? cudaMallocAsync(&p->d_stage, bytes > 0 ? bytes : 256, stream)
+    cudaError_t e = defer_upload ? sk::scratch_alloc(&p->d_stage, bytes > 0 ? bytes : 256, stream)
                                  : cudaMalloc(&p->d_stage, bytes > 0 ? bytes : 256);
     if (e != cudaSuccess) { delete p; return e == cudaErrorMemoryAllocation ? SK_ENOMEM : cuda_fail(e, "cudaMalloc(plan)"); }
     unsigned char* dst = static_cast<unsigned char*>(p->d_stage);
@@ -591,7 +633,7 @@ int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
 int validate_rows_sync(const int32_t* rowidx, int64_t nnz, int64_t m, cudaStream_t stream) {
   if (nnz == 0) return SK_OK;
   int* flag = nullptr;
-  SK_CUDA(cudaMallocAsync(&flag, sizeof(int), stream));
+  SK_CUDA(sk::scratch_alloc((void**)&flag, sizeof(int), stream));
   int h = 0;
   cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(int), stream);
   if (e == cudaSuccess) e = sk::launch_validate_rows(rowidx, nnz, m, flag, stream);
@@ -609,7 +651,7 @@ bool use_jki(const sk_plan_s* p, int dist) {
   const int path = pair_path();
   if (path == SK_PAIR_KJI) return false;
   if (path == SK_PAIR_JKI) return true;
-  return dist == SK_GAUSSIAN && (double)p->jki_rows <= kJReuseGaussian * (double)p->nnz;
+  return (double)p->jki_rows <= jki_bar((int)p->dtype, dist) * (double)p->nnz;
 }
 
 // A side stream + fork / join events per host thread and device (created once).
@@ -900,11 +942,11 @@ int sketch_apply_host(uint64_t seed, sk_dist_t dist, sk_dtype_t dtype, int64_t d
   void* d_out = nullptr;
   int* d_flag = nullptr;
   int h_flag = 0;
-  SK_STEP(cudaMallocAsync((void**)&d_colptr, (size_t)(n + 1) * 8, stream));
-  SK_STEP(cudaMallocAsync((void**)&d_rowidx, (size_t)std::max<int64_t>(nnz, 1) * 4, stream));
-  SK_STEP(cudaMallocAsync(&d_vals, (size_t)std::max<int64_t>(nnz, 1) * w, stream));
-  SK_STEP(cudaMallocAsync(&d_out, (size_t)std::max<int64_t>(d * n, 1) * w, stream));
-  SK_STEP(cudaMallocAsync((void**)&d_flag, sizeof(int), stream));
+  SK_STEP(sk::scratch_alloc((void**)&d_colptr, (size_t)(n + 1) * 8, stream));
+  SK_STEP(sk::scratch_alloc((void**)&d_rowidx, (size_t)std::max<int64_t>(nnz, 1) * 4, stream));
+  SK_STEP(sk::scratch_alloc(&d_vals, (size_t)std::max<int64_t>(nnz, 1) * w, stream));
+  SK_STEP(sk::scratch_alloc(&d_out, (size_t)std::max<int64_t>(d * n, 1) * w, stream));
+  SK_STEP(sk::scratch_alloc((void**)&d_flag, sizeof(int), stream));
   SK_STEP(cudaMemsetAsync(d_flag, 0, sizeof(int), stream));
   // Order on the upload stream: colptr, group 0 of A, the group plans' schedule images, groups
   // 1.. of A.  The plans (host schedules, same kernels as sketch_apply) are built while group 0
@@ -1032,6 +1074,7 @@ int sketch_plan_stats(sk_plan_t plan, sk_stats_t* h) {
   h->n_items_f4_split = plan->f4_split_items;
   h->n_items_f4 = plan->n_f4;
   h->n_cols_f4 = plan->f4_cols;
+  h->jki_block_cols = plan->jki.n_items > 0 ? plan->jki.bn : 0;
   h->plan_bytes = (plan->n_rad + plan->n_pair + plan->n_gauss) * (int64_t)sizeof(Item) +
                   plan->n_f4 * (int64_t)sizeof(sk::TcItem) + (plan->owned_colptr ? (plan->n + 1) * 8 : 0);
   return SK_OK;

@@ -46,7 +46,7 @@ class sk_stats_t(ctypes.Structure):
     _fields_ = [(name, ctypes.c_int64) for name in
                 ("d", "m", "n", "nnz", "row_offset", "max_col_nnz", "n_items_rad", "n_items_pair",
                  "philox_blocks_rad", "philox_blocks_pair", "plan_bytes", "n_items_jki", "jki_nonzero_rows", "n_items_f4_split",
-                 "n_items_f4", "n_cols_f4")]
+                 "n_items_f4", "n_cols_f4", "jki_block_cols")]
 
 
 _lock = threading.Lock()

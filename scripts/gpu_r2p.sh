@@ -1,0 +1,10 @@
+mkdir -p gpurun_out/r2p
+O=gpurun_out/r2p
+python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1 || { echo build failed; exit 1; }
+timeout 1500 python -m pytest tests -m gpu -q -p no:faulthandler > $O/tests.log 2>&1; echo "tests rc $?" > $O/summary.txt
+tail -1 $O/tests.log >> $O/summary.txt; grep -E "^FAILED|^ERROR" $O/tests.log | head >> $O/summary.txt
+for dist in uniform gaussian; do timeout 600 python scripts/abnormal_bench.py --dist $dist 2>&1 | grep pattern >> $O/summary.txt; done
+timeout 900 python scripts/jki_configs.py c2 c3 >> $O/summary.txt 2>&1
+cd scripts && timeout 1200 python jki_reuse_sweep.py > ../$O/sweep.jsonl 2>&1; cd ..
+timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench rc $?" >> $O/summary.txt
+cat $O/summary.txt; cat $O/sweep.jsonl; tail -c 1500 $O/bench.json

@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--rows", type=int, default=0, help="c5 only: use rows [0, rows)")
     ap.add_argument("--dist", default=None, help="override the config's distribution")
     ap.add_argument("--f32", action="store_true", help="values rounded to fp32 (fp32 arithmetic)")
+    ap.add_argument("--jki", action="store_true", help="forced Algorithm 4 plan and path")
     a = ap.parse_args()
     cfg = workloads.CONFIGS[a.config]
     A = workloads.make_config(cfg.name, row_range=(0, a.rows)) if a.rows else workloads.make_config(cfg.name)
@@ -33,7 +34,9 @@ def main():
     colptr = torch.from_numpy(A.colptr).to(dev)
     rowidx = torch.from_numpy(A.rowidx).to(dev)
     vals = torch.from_numpy(A.vals).to(dev)
-    plan = sk.Plan(colptr, rowidx, cfg.d, A.m, dtype, row_offset=A.row_offset)
+    plan = sk.Plan(colptr, rowidx, cfg.d, A.m, dtype, row_offset=A.row_offset, jki=a.jki)
+    if a.jki:
+        sk.set_pair_path("jki")
     out = torch.empty((cfg.n, cfg.d), dtype=vals.dtype, device=dev)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * a.reps)]
     for r in range(a.reps):

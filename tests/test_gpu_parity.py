@@ -663,33 +663,41 @@ def test_jki_matches_oracle(sk, dist, dtype, case):
 
 def test_jki_auto_selection(sk):
     # the plan builds the Algorithm 4 structure on its own only when the exact distinct-row count of
-    # its column blocks (b_n = 1024 fp64 columns) shows enough reuse (rows <= 0.26 nnz), and then uses
-    # it for Gaussian S (measured to win there; uniform S keeps Algorithm 3)
+    # its column blocks (b_n = 384 fp64 columns) clears the loosest bar (f64 Gaussian: rows <= 0.40
+    # nnz), and then uses it per distribution from the measured costs (sketch_api.cu):
+    # rows/nnz = 0.016 (Abnormal A-like) -> Algorithm 4 for uniform and Gaussian S; 0.25 -> Gaussian
+    # only (uniform needs <= 0.10); 0.95 -> not built
     A = workloads.abnormal_paper("A", m=20000, n=64, seed=1)
+    M = workloads.random_csc(4900, 64, 300, seed=6)
     B = workloads.random_csc(200000, 64, 300, seed=2)
     pa = sk.Plan(_dev(A.colptr), _dev(A.rowidx), 256, A.m)
+    pm = sk.Plan(_dev(M.colptr), _dev(M.rowidx), 256, M.m)
     pb = sk.Plan(_dev(B.colptr), _dev(B.rowidx), 256, B.m)
     try:
-        assert pa.stats()["n_items_jki"] > 0 and pb.stats()["n_items_jki"] == 0
-        assert pa.stats()["jki_nonzero_rows"] * 10 <= A.nnz
+        assert pa.stats()["n_items_jki"] > 0 and pm.stats()["n_items_jki"] > 0 and pb.stats()["n_items_jki"] == 0
         # the RNG work of Algorithm 4 is exactly the distinct rows of every column block
         # (PAPER.md:302-318, 436-442): here one block of all 64 columns
         assert pa.stats()["jki_nonzero_rows"] == len(np.unique(A.rowidx))
-        assert "Algorithm 4" in pa.kernel_name("gaussian") and "Algorithm 4" not in pa.kernel_name("uniform")
+        assert pm.stats()["jki_nonzero_rows"] == len(np.unique(M.rowidx))
+        assert 0.10 < pm.stats()["jki_nonzero_rows"] / M.nnz <= 0.40
+        assert "Algorithm 4" in pa.kernel_name("gaussian") and "Algorithm 4" in pa.kernel_name("uniform")
+        assert "Algorithm 4" in pm.kernel_name("gaussian") and "Algorithm 4" not in pm.kernel_name("uniform")
         sk.set_pair_path("jki")
-        assert "Algorithm 4" in pa.kernel_name("uniform")
+        assert "Algorithm 4" in pm.kernel_name("uniform")
         sk.set_pair_path("kji")
         assert "Algorithm 4" not in pa.kernel_name("gaussian")
     finally:
         sk.set_pair_path("auto")
         pa.close()
+        pm.close()
         pb.close()
 
 
 def test_jki_on_c2_with_exact_row_count(sk):
     # BASELINE config c2 (1000 distinct uniform rows per column of 1e6): a forced Algorithm 4 plan
-    # (b_n = n) generates every needed S column exactly once -- its row count is exactly nnzrows(A)
-    # -- and matches the oracle; the automatic plan keeps Algorithm 3 (reuse 1.58 < 3.8)
+    # generates every needed S column exactly once per column block -- its row count is exactly the
+    # sum over the b_n-column blocks of their distinct rows -- and matches the oracle; the automatic
+    # plan keeps Algorithm 3 (reuse too low)
     import torch
     A = workloads.make_config("c2")
     auto = sk.Plan(_dev(A.colptr), _dev(A.rowidx), 2000, A.m)
@@ -699,7 +707,10 @@ def test_jki_on_c2_with_exact_row_count(sk):
     try:
         sk.set_pair_path("jki")
         st = plan.stats()
-        assert st["n_items_jki"] > 0 and st["jki_nonzero_rows"] == len(np.unique(A.rowidx))
+        bn = st["jki_block_cols"]
+        assert bn > 0 and st["n_items_jki"] > 0
+        want = sum(len(np.unique(A.rowidx[A.colptr[c]:A.colptr[min(c + bn, A.n)]])) for c in range(0, A.n, bn))
+        assert st["jki_nonzero_rows"] == want
         got = plan.apply(_dev(A.vals), 1, "uniform").T.cpu().numpy()
         torch.cuda.synchronize()
     finally:
@@ -724,7 +735,8 @@ def test_jki_multiple_blocks_and_split_parts(sk):
     for k in range(n):
         r = np.concatenate([dense_rows, rng.choice(m, 3, replace=False)])
         if k % 2 == 0:
-            r = np.concatenate([r, [7, 7]])            # duplicate (j, k) entries, unsorted
+            r = np.concatenate([r, [7, 7, 7]])         # duplicate (j, k) entries, unsorted: row 7 holds
+                                                       # > 512 entries (one batch) in every full block
         cols.append(r.astype(np.int32))
     colptr = np.zeros(n + 1, np.int64)
     colptr[1:] = np.cumsum([len(c) for c in cols])

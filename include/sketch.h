@@ -86,6 +86,8 @@ typedef struct {
     int64_t n_items_f4;        /* CTAs of the tensor-core kernel of one SK_RADEMACHER apply */
     int64_t n_cols_f4;         /* columns on the tensor-core kernel (the others: n_items_rad SIMT CTAs) */
     int64_t jki_block_cols;    /* b_n of the Algorithm 4 column blocks (384 f64, 768 f32), 0 if not built */
+    int64_t f4_persistent;     /* 1: the tensor-core columns run on the persistent kernel (mean column
+                                  < 16384 nonzeros; SKETCH_F4_PERSIST = 0 | 1 forces), 0: one CTA per item */
 } sk_stats_t;
 
 /*
@@ -191,6 +193,16 @@ typedef enum {
     SK_PATH_SIMT = 3
 } sk_rad_f64_path_t;
 int sketch_set_rad_f64_path(int path);
+
+/*
+ * sketch_set_f4_persistent -- how plans built from now on run their tensor-core columns (process-wide):
+ * -1 (default) the persistent kernel (one CTA per SM walking the work items, TMEM / barriers set up
+ * once, the next item's column scale computed ahead) when the mean tensor-core column has fewer than
+ * 16384 nonzeros, else one CTA per item; 0 always one CTA per item; 1 always persistent.  Same
+ * results either way (the same per-item arithmetic).  Initialised from SKETCH_F4_PERSIST = 0 | 1.
+ * Errors: SK_EINVAL for another value.
+ */
+int sketch_set_f4_persistent(int mode);
 
 /*
  * Kernel selection for SK_UNIFORM / SK_GAUSSIAN (process-wide): Algorithm 3 (kji: S[:, j] regenerated

@@ -63,7 +63,8 @@ constexpr int64_t kTcMaxColumn = 131071;
 
 // The tensor-core kernel, with the zeroing of the K-split rows before it and the IEEE fix-up of the
 // columns it found non-finite after it.
-cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const TcItem* items, int64_t n_items, cudaStream_t stream);
+cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const TcItem* items, int64_t n_items, bool persistent,
+                                cudaStream_t stream);
 
 // ±1 sketch columns holding a NaN / Inf value get the IEEE result (sketch_kernels.cu): a scan of
 // every column's values, one warp per column (dtype 0 = f64, 1 = f32).

@@ -196,6 +196,26 @@ int64_t f4_min_column() {
   return v;
 }
 
+// Persistent tensor-core kernel (one CTA per SM walking the items; TMEM / barriers / constant rows set
+// up once, the next item's column scale computed ahead, its first stage produced before the previous
+// item's read-out) when the tensor-core columns are short on average: per-item set-up and pipeline
+// fill then weigh more than the persistent kernel's slightly longer stage loop.  Measured on c5 row
+// shards (scripts/gpu_r2ac.sh, profiles/r02_f4_persistent_sweep.txt): mean column 50000 nonzeros
+// 7.24 -> 7.44 ms, 25000 3.73 -> 3.75, 12500 1.97 -> 1.92, 6250 1.089 -> 1.013, 3125 0.617 -> 0.574.
+// SKETCH_F4_PERSIST = 0 | 1 forces the choice.
+std::atomic<int> g_f4_persist{-2};   // -2: not read yet
+
+bool f4_use_persistent(int64_t mean_col) {
+  int v = g_f4_persist.load(std::memory_order_relaxed);
+  if (v == -2) {
+    const char* e = getenv("SKETCH_F4_PERSIST");
+    v = e ? (atoi(e) != 0 ? 1 : 0) : -1;
+    g_f4_persist.store(v, std::memory_order_relaxed);
+  }
+  if (v >= 0) return v != 0;
+  return mean_col < 16384;
+}
+
 const char* kernel_name(const sk_plan_s* p, int dist);
 
 // Uniform / Gaussian kernel choice (process-wide): SK_PAIR_AUTO (jki when the plan built it),
@@ -226,6 +246,7 @@ struct sk_plan_s {
   int64_t n_f4 = 0;
   int64_t f4_split_items = 0;       // half items of the K-split last wave
   int64_t f4_cols = 0;              // columns on the tensor-core kernel (the rest: n_rad SIMT items)
+  bool f4_persist = false;          // the persistent tensor-core kernel (short mean column, f4_use_persistent)
   // Algorithm 4 (jki) structure: one device block holding items, grp_rows, row_j, row_ent, ent, ent_base
   void* d_jki = nullptr;
   sk::JkiPlanView jki{};
@@ -579,6 +600,9 @@ int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
     if (!tc_cols.empty()) {
       f4 = build_tc_schedule(h_colptr, d, sk::f4_tiles_per_cta(), tc_cols);
       p->f4_split_items = split_f4_tail(f4, h_colptr);
+      int64_t tc_nnz = 0;
+      for (int32_t k : tc_cols) tc_nnz += h_colptr[k + 1] - h_colptr[k];
+      p->f4_persist = f4_use_persistent(tc_nnz / (int64_t)tc_cols.size());
     }
     p->f4_cols = (int64_t)tc_cols.size();
   }
@@ -701,10 +725,10 @@ int apply_items(const sk_plan_s* p, uint64_t seed, sk_dist_t dist, const void* v
       if (e == cudaSuccess) e = cudaStreamWaitEvent(sp.side, sp.fork, 0);
       if (e == cudaSuccess) e = sk::launch_apply(0, (int)p->dtype, a, sp.side);
       if (e == cudaSuccess) e = cudaEventRecord(sp.join, sp.side);
-      if (e == cudaSuccess) e = sk::launch_apply_rad_f4(a, p->d_f4, p->n_f4, stream);
+      if (e == cudaSuccess) e = sk::launch_apply_rad_f4(a, p->d_f4, p->n_f4, p->f4_persist, stream);
       if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, sp.join, 0);
     } else if (p->n_f4 > 0) {
-      e = sk::launch_apply_rad_f4(a, p->d_f4, p->n_f4, stream);
+      e = sk::launch_apply_rad_f4(a, p->d_f4, p->n_f4, p->f4_persist, stream);
     } else {
       e = sk::launch_apply(0, (int)p->dtype, a, stream);
     }
@@ -719,25 +743,12 @@ int apply_items(const sk_plan_s* p, uint64_t seed, sk_dist_t dist, const void* v
   return SK_OK;
 }
 
-struct PoolInit {
-  PoolInit() {
-    int dev = 0;
-    cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-  }
-};
-
-void ensure_pool() {
-  thread_local bool done = false;
-  if (!done) { PoolInit p; (void)p; done = true; }
-}
-
 const char* kernel_name(const sk_plan_s* p, int dist) {
   if (dist == SK_RADEMACHER) {
     if (p->dtype == SK_F32) return "sk_rad_kernel<float>";
+    if (p->n_f4 > 0 && p->f4_persist)
+      return p->n_rad > 0 ? "sk_rad_f4p_kernel (tcgen05 kind::mxf4, persistent) + sk_rad_kernel<double>"
+                          : "sk_rad_f4p_kernel (tcgen05 kind::mxf4, persistent)";
     if (p->n_f4 > 0) return p->n_rad > 0 ? "sk_rad_f4_kernel (tcgen05 kind::mxf4) + sk_rad_kernel<double>"
                                          : "sk_rad_f4_kernel (tcgen05 kind::mxf4)";
     return "sk_rad_kernel<double>";
@@ -878,7 +889,6 @@ int sketch_apply_host(uint64_t seed, sk_dist_t dist, sk_dtype_t dtype, int64_t d
   if (nnz > 0 && (!h_rowidx || !h_vals)) return SK_EINVAL;
   rc = validate_colptr(h_colptr, n, nnz, true);
   if (rc) return rc;
-  ensure_pool();
   cudaStream_t stream = (cudaStream_t)stream_;
   const size_t w = dtype_bytes(dtype);
 
@@ -1074,6 +1084,7 @@ int sketch_plan_stats(sk_plan_t plan, sk_stats_t* h) {
   h->n_items_f4_split = plan->f4_split_items;
   h->n_items_f4 = plan->n_f4;
   h->n_cols_f4 = plan->f4_cols;
+  h->f4_persistent = plan->f4_persist ? 1 : 0;
   h->jki_block_cols = plan->jki.n_items > 0 ? plan->jki.bn : 0;
   h->plan_bytes = (plan->n_rad + plan->n_pair + plan->n_gauss) * (int64_t)sizeof(Item) +
                   plan->n_f4 * (int64_t)sizeof(sk::TcItem) + (plan->owned_colptr ? (plan->n + 1) * 8 : 0);
@@ -1106,6 +1117,12 @@ const char* sketch_error_string(int code) {
 const char* sketch_last_error_detail(void) { return g_detail.c_str(); }
 
 const char* sketch_version(void) { return "libsketch 0.2.0 sm_100a"; }
+
+int sketch_set_f4_persistent(int mode) {
+  if (mode < -1 || mode > 1) return SK_EINVAL;
+  g_f4_persist.store(mode, std::memory_order_relaxed);
+  return SK_OK;
+}
 
 int sketch_set_rad_f64_path(int path) {
   if (path != SK_PATH_TC_FP4 && path != SK_PATH_SIMT) return SK_EINVAL;

@@ -37,7 +37,14 @@ namespace {
 
 constexpr int kF4Tiles = 6;                       // 128-row tiles per CTA (max)
 constexpr int kF4AWarps = 2 * kF4Tiles;          // A producers: (tile, nonzero half)
-constexpr int kF4BWarps = 2;                      // B producers: nonzero half
+#ifndef SK_F4_BW
+#define SK_F4_BW 2
+#endif
+// B producers: (nonzero half h, digit half dh).  With 2 warps each makes all 64 digit rows of its
+// nonzero half; with 4 each makes 32 (the conversion is duplicated, the transposes and stores halved).
+constexpr int kF4BWarps = SK_F4_BW;
+constexpr int kF4BW = 2 * 2 / kF4BWarps;           // transposed words per K-step and B warp (2 or 1)
+static_assert(kF4BWarps == 2 || kF4BWarps == 4, "B producers");
 constexpr int kF4Producers = kF4AWarps + kF4BWarps;
 constexpr int kF4LoaderWarp = kF4Producers;       // streams rowidx / vals into a smem ring
 constexpr int kF4MmaWarp = kF4Producers + 1;
@@ -299,13 +306,14 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
     }
   } else if (warp >= kF4AWarps && warp < kF4Producers) {
     // ===================== B producers: digits of nonzero half h =====================
-    const int h = warp - kF4AWarps;
+    const int bw = warp - kF4AWarps;
+    const int h = kF4BWarps == 2 ? bw : (bw & 1), dh = kF4BWarps == 2 ? 0 : (bw >> 1);
     // 2^(61-E) as two exact power-of-two factors (each within the double range)
     const int e1 = 61 - E > 1000 ? 1000 : (61 - E < -1000 ? -1000 : 61 - E);
     const double sc1 = ldexp(1.0, e1), sc2 = ldexp(1.0, 61 - E - e1);
     for (int ss = 0; ss < nsup; ++ss) {
       const int stage = ss % kF4Stages, use = ss / kF4Stages;
-      uint32_t x[2 * kF4Sub];
+      uint32_t x[kF4BW * kF4Sub];
       int nval[kF4Sub];
       const int jslot = ss % kF4JSlots;
       f4_wait(&sh.jfull[jslot], (ss / kF4JSlots) & 1);
@@ -327,18 +335,26 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
           const long long A = __double2ll_rn((v0 * sc1) * sc2);
           U = (unsigned long long)A ^ 0x8000000000000000ull;
         }
-        x[2 * sub] = ~(uint32_t)U;                 // sign bits of the digit nibbles
-        x[2 * sub + 1] = ~(uint32_t)(U >> 32);
+        if constexpr (kF4BW == 2) {
+          x[2 * sub] = ~(uint32_t)U;               // sign bits of the digit nibbles
+          x[2 * sub + 1] = ~(uint32_t)(U >> 32);
+        } else {
+          x[sub] = dh ? ~(uint32_t)(U >> 32) : ~(uint32_t)U;
+        }
       }
-      f4_transpose<2 * kF4Sub>(x, lane);           // lane r: bit r (and 32 + r) of U per K-step
+      f4_transpose<kF4BW * kF4Sub>(x, lane);       // lane r: bit r (and 32 + r) of U per K-step
       if (use > 0) f4_wait(&sh.empty[stage], (use - 1) & 1);
       if (!(dbg & 8)) {
 #pragma unroll
         for (int sub = 0; sub < kF4Sub; ++sub) {
           const uint32_t bt = s_u32(stages + stage * kF4Stage + kF4Tiles * kF4ATileS + sub * kF4BSub);
-          f4_store_row_masked(bt + f4_off(lane, h), x[2 * sub], nval[sub]);
-          f4_store_row_masked(bt + f4_off(32 + lane, h), x[2 * sub + 1], nval[sub]);
-          if (nval[sub] < 32 && lane == 0) {   // partial (last) K chunk: the ones row too
+          if constexpr (kF4BW == 2) {
+            f4_store_row_masked(bt + f4_off(lane, h), x[2 * sub], nval[sub]);
+            f4_store_row_masked(bt + f4_off(32 + lane, h), x[2 * sub + 1], nval[sub]);
+          } else {
+            f4_store_row_masked(bt + f4_off(32 * dh + lane, h), x[sub], nval[sub]);
+          }
+          if (nval[sub] < 32 && lane == 0 && dh == 0) {   // partial (last) K chunk: the ones row too
             const uint32_t z = 0u;              // (y = 0 -> nibbles 0x2 = +1.0)
             f4_store_row_masked(bt + f4_off(kF4Ones, h), z, nval[sub]);
           }
@@ -452,6 +468,448 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
   }
 }
 
+// ============================================================================================
+// Persistent variant (SKETCH_F4_PERSIST=1): one CTA per SM walks the items blockIdx.x + k gridDim.x.
+// TMEM, the barriers, the constant B rows and the scale factors are set up once; a scan warp
+// computes the next item's column scale E while the current item runs (2-slot ring); the A
+// producers produce the first stage of item k before they read out item k-1's accumulators, so the
+// MMA warp restarts as soon as TMEM is free (tfree) with a stage already waiting.  All roles walk
+// the same global stage sequence g (ring slot g % 2, phase g / 2); A warps without a tile in an
+// item (T < 6) skip it and wait for its accumulators, and the B warps arrive on the stage barriers
+// in their place.
+constexpr int kF4PScanWarp = kF4MmaWarp + 1;
+constexpr int kF4PThreads = (kF4PScanWarp + 1) * 32;
+constexpr int kF4PEpiWarps = kF4AWarps;            // epilogue: the 12 A warps (lane quarter = warp % 4)
+
+struct F4PShared {
+  uint64_t full[kF4Stages];
+  uint64_t empty[kF4Stages];
+  uint64_t jfull[kF4JSlots];
+  uint64_t jempty[kF4JSlots];
+  uint64_t done;                // MMA -> epilogue: one phase per item
+  uint64_t tfree;               // epilogue -> MMA: accumulators read out, one phase per item
+  uint64_t efull[2];            // scan warp -> B producers / epilogue: E of item k in slot k % 2
+  uint64_t eempty[2];
+  uint32_t js[kF4JSlots][64 * kF4Sub];
+  double vs[kF4JSlots][64 * kF4Sub];
+  int64_t item[2];              // item index of the CTA's item k in slot k % 2 (-1: no more items)
+  int32_t E[2];
+  int32_t nonfinite[2];
+  uint32_t tmem_base;
+};
+
+struct F4PItem {
+  int64_t pb, pe;
+  int col, tile0, T, pad, nsteps, nsup;
+};
+
+__device__ __forceinline__ F4PItem f4p_item(const ApplyArgs& P, const TcItem* items, int64_t idx) {
+  const TcItem it = items[idx];
+  F4PItem r;
+  r.pb = P.colptr[it.col];
+  r.pe = P.colptr[it.col + 1];
+  if (it.pad) {
+    const int64_t half = ((((r.pe - r.pb) + 63) >> 6) >> 1) << 6;
+    if (it.pad == 1) r.pe = r.pb + half; else r.pb += half;
+  }
+  r.col = it.col;
+  r.tile0 = it.tile0;
+  r.T = it.ntiles;
+  r.pad = it.pad;
+  r.nsteps = (int)((r.pe - r.pb + 63) >> 6);
+  r.nsup = (r.nsteps + kF4Sub - 1) / kF4Sub;
+  return r;
+}
+
+// max |v[p]| bits over [pb, pe) by one warp, 8 independent 16-byte loads in flight per lane
+__device__ __forceinline__ unsigned long long f4p_scan(const double* __restrict__ v, int64_t pb, int64_t pe, int lane) {
+  constexpr unsigned long long kAbs = 0x7FFFFFFFFFFFFFFFull;
+  auto ab = [](double x) { return (unsigned long long)__double_as_longlong(x) & kAbs; };
+  unsigned long long m[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  // first index >= pb whose address is 16-byte aligned (v is 8-byte aligned)
+  int64_t a = pb + ((reinterpret_cast<uintptr_t>(v + pb) & 15) ? 1 : 0);
+  if (a > pe) a = pe;
+  const int64_t n2 = (pe - a) >> 1;
+  if (lane == 0 && pb < a) m[0] = ab(__ldg(v + pb));
+  if (lane == 31 && a + 2 * n2 < pe) m[1] = ab(__ldg(v + a + 2 * n2));
+  const double2* v2 = reinterpret_cast<const double2*>(v + a);
+  int64_t i = lane;
+  for (; i + 7 * 32 < n2; i += 8 * 32) {
+    double2 x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = __ldg(v2 + i + 32 * u);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) m[u] = max(m[u], max(ab(x[u].x), ab(x[u].y)));
+  }
+  for (; i < n2; i += 32) {
+    const double2 x = __ldg(v2 + i);
+    m[0] = max(m[0], max(ab(x.x), ab(x.y)));
+  }
+  unsigned long long r = 0;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) r = max(r, m[u]);
+  for (int o = 16; o; o >>= 1) r = max(r, __shfl_xor_sync(0xFFFFFFFFu, r, o));
+  return r;
+}
+
+static_assert(kF4Stages == 2 && kF4JSlots == 2, "the persistent kernel indexes its rings with g & 1");
+
+// A wait expected to last long (an item, or the rest of one): poll with explicit sleeps instead of
+// the try_wait loop, whose ~40 ns suspensions cost the producers ~7% of an SMSP per waiting warp.
+__device__ __forceinline__ void f4_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  for (;;) {
+    uint32_t ok;
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(ok) : "r"(s_u32(bar)), "r"(parity) : "memory");
+    if (ok) break;
+    __nanosleep(ns);
+  }
+}
+
+__device__ __forceinline__ void f4_arrive_cnt(uint64_t* bar, uint32_t cnt) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" :: "r"(s_u32(bar)), "r"(cnt) : "memory");
+}
+
+// One smem stage of S tile t (nonzero half h) for global stage g (as sk_rad_f4_kernel's A loop).
+__device__ __forceinline__ void f4p_a_stage(F4PShared& sh, unsigned char* stages, const PhiloxKeys& keys,
+                                            uint64_t row_offset, uint32_t g, uint32_t q, int t, int h, int lane) {
+  constexpr int kMine = kF4Sub;
+  const uint32_t stage = g & 1u, use = g >> 1, jslot = g & 1u;
+  const int jl = 32 * h + lane;
+  f4_wait(&sh.jfull[jslot], use & 1u);
+  uint32_t jv[kMine];
+#pragma unroll
+  for (int i = 0; i < kMine; ++i) jv[i] = sh.js[jslot][64 * i + jl];
+  __syncwarp();
+  if (lane == 0) f4_arrive(&sh.jempty[jslot]);
+  uint32_t x[4 * kMine];
+#pragma unroll
+  for (int i = 0; i < kMine; ++i) {
+    const uint4 xb = s_block(q, row_offset + jv[i], keys);
+    x[4 * i + 0] = xb.x; x[4 * i + 1] = xb.y; x[4 * i + 2] = xb.z; x[4 * i + 3] = xb.w;
+  }
+  f4_transpose<4 * kMine>(x, lane);
+  if (use > 0) f4_wait(&sh.empty[stage], (use - 1) & 1u);
+  const uint32_t tile = s_u32(stages + stage * kF4Stage) + (uint32_t)(t * kF4ATileS) + f4_off(lane, h);
+#pragma unroll
+  for (int i = 0; i < kMine; ++i)
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq)
+      f4_store_row(tile + (uint32_t)(i * kF4ATile + qq * 4 * 256), x[4 * i + qq]);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (lane == 0) f4_arrive(&sh.full[stage]);
+}
+
+// Epilogue of item k (warps 0..11): wait for its accumulators, read TMEM, form Â, free TMEM.
+__device__ __forceinline__ void f4p_epilogue(F4PShared& sh, const ApplyArgs& P, const F4PItem& it, int64_t k,
+                                             uint32_t tmem, int warp, int lane) {
+  f4_wait_sleep(&sh.done, (uint32_t)(k & 1), 200);
+  f4_wait(&sh.efull[k & 1], (uint32_t)((k >> 1) & 1));
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const int E = sh.E[k & 1];
+  const int nonfinite = sh.nonfinite[k & 1];
+  const int qw = warp & 3;
+  double* outc = reinterpret_cast<double*>(P.out) + (int64_t)it.col * P.ld;
+  const double nan = __longlong_as_double(0x7FF8000000000000ll);
+  for (int tt = warp >> 2; tt < it.T; tt += 3) {
+    long long lo = 0, hi = 0, ones = 0;
+    if (it.nsteps > 0) {
+      const uint32_t base = tmem + ((uint32_t)(32 * qw) << 16) + (uint32_t)(tt * kF4N);
+#pragma unroll
+      for (int c = 0; c < kF4N; c += 8) {
+        uint32_t D[8];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                     : "=r"(D[0]), "=r"(D[1]), "=r"(D[2]), "=r"(D[3]), "=r"(D[4]), "=r"(D[5]), "=r"(D[6]), "=r"(D[7])
+                     : "r"(base + (uint32_t)c));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const long long dv = (long long)__float2ll_rn(__uint_as_float(D[u]));
+          const int s = c + u;
+          if (s < 32) lo += dv << s;
+          else if (s < 64) hi += dv << (s - 32);
+          else if (s == 64) ones = dv;
+        }
+      }
+    }
+    const int64_t row = (int64_t)(it.tile0 + tt) * 128 + 32 * qw + lane;
+    if (row < P.d) {
+      const double v = scalbn((double)hi * 4294967296.0 + (double)(lo - ones), E - 62);
+      const double res = nonfinite ? nan : v;
+      if (it.pad) atomicAdd(outc + row, res); else outc[row] = res;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncwarp();
+  if (lane == 0) {
+    f4_arrive(&sh.tfree);
+    f4_arrive(&sh.eempty[k & 1]);
+  }
+}
+
+// Item k of this CTA, published by the scan warp (slot k % 2, with efull): -1 when there is none.
+__device__ __forceinline__ int64_t f4p_next(F4PShared& sh, int64_t k) {
+  f4_wait(&sh.efull[k & 1], (uint32_t)((k >> 1) & 1));
+  return sh.item[k & 1];
+}
+
+__global__ void __launch_bounds__(kF4PThreads, 1) sk_rad_f4p_kernel(const ApplyArgs P, const TcItem* items, int64_t n_items,
+                                                                     unsigned long long* next_item) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* stages = smem_raw + ((1024u - (s_u32(smem_raw) & 1023u)) & 1023u);
+  F4PShared& sh = *reinterpret_cast<F4PShared*>(stages + kF4Stages * kF4Stage);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t G = gridDim.x;
+  const double* vals = reinterpret_cast<const double*>(P.vals);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kF4Stages; ++s) { f4_mbar_init(&sh.full[s], kF4AWarps + kF4BWarps); f4_mbar_init(&sh.empty[s], 1); }
+    for (int s = 0; s < kF4JSlots; ++s) { f4_mbar_init(&sh.jfull[s], 32); f4_mbar_init(&sh.jempty[s], kF4AWarps + kF4BWarps); }
+    f4_mbar_init(&sh.done, 1);
+    f4_mbar_init(&sh.tfree, kF4PEpiWarps);
+    for (int s = 0; s < 2; ++s) { f4_mbar_init(&sh.efull[s], 1); f4_mbar_init(&sh.eempty[s], kF4PEpiWarps + kF4BWarps); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kF4MmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 :: "r"(s_u32(&sh.tmem_base)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  for (int i = threadIdx.x; i < kF4Stages * kF4Sub * 8 * 2; i += blockDim.x) {
+    const int s = i / (16 * kF4Sub), sub = (i / 16) % kF4Sub, row = kF4Ones + (i % 16) / 2, h = i & 1;
+    const uint32_t v = row == kF4Ones ? 0x22222222u : 0u;
+    const uint32_t a = s_u32(stages + s * kF4Stage + kF4Tiles * kF4ATileS + sub * kF4BSub) + f4_off(row, h);
+    asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" :: "r"(a), "r"(v) : "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  const uint32_t tmem = sh.tmem_base;
+  if (warp < 4) {
+    const uint32_t taddr = tmem + ((uint32_t)(32 * warp) << 16) + kF4SfCol;
+    const uint32_t v = 0x7F7F7F7Fu;
+#pragma unroll
+    for (int c = 0; c < 64; c += 8)
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1};"
+                   :: "r"(taddr + c), "r"(v) : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp < kF4AWarps) {
+    // ===================== A producers + epilogue =====================
+    // A warps without a tile in an item (T < 6) skip its stages (the B warps arrive for them) and
+    // wait for the item's accumulators instead: a parity wait is only meaningful within one phase of
+    // the barrier, so no warp may run more than one stage ahead of the ring.
+    uint32_t g = 0;
+    F4PItem prev{};
+    bool pending = false;                          // prev's epilogue not done yet
+    PhiloxKeys keys = P.keys;                      // in registers across the item loop (not reloaded
+#pragma unroll                                     // from the constant bank every stage)
+    for (int r = 0; r < 10; ++r) asm volatile("" : "+r"(keys.k0[r]), "+r"(keys.k1[r]));
+    const uint64_t row_offset = (uint64_t)P.row_offset;
+    for (int64_t k = 0;; ++k) {
+      const int64_t idx = f4p_next(sh, k);
+      if (idx < 0) {
+        if (pending) f4p_epilogue(sh, P, prev, k - 1, tmem, warp, lane);
+        break;
+      }
+      const F4PItem it = f4p_item(P, items, idx);
+      const int T = it.T;
+      if (warp < 2 * T) {
+        const int t = warp % T, h = (warp / T) & 1;
+        const uint32_t q = (uint32_t)(it.tile0 + t);
+        int ss = 0;
+        if (it.nsup > 0) {   // the first stage of item k before item k-1's epilogue
+          f4p_a_stage(sh, stages, keys, row_offset, g, q, t, h, lane);
+          ++ss;
+        }
+        if (pending) f4p_epilogue(sh, P, prev, k - 1, tmem, warp, lane);
+        for (; ss < it.nsup; ++ss) f4p_a_stage(sh, stages, keys, row_offset, g + (uint32_t)ss, q, t, h, lane);
+        pending = true;
+      } else {
+        if (pending) f4p_epilogue(sh, P, prev, k - 1, tmem, warp, lane);
+        f4p_epilogue(sh, P, it, k, tmem, warp, lane);   // waits for item k's accumulators
+        pending = false;
+      }
+      g += (uint32_t)it.nsup;
+      prev = it;
+    }
+  } else if (warp < kF4Producers) {
+    // ===================== B producers: digits of nonzero half h =====================
+    const int bw = warp - kF4AWarps;
+    const int h = kF4BWarps == 2 ? bw : (bw & 1), dh = kF4BWarps == 2 ? 0 : (bw >> 1);
+    uint32_t g = 0;
+    uint32_t dirty = 0;                            // (stage, sub) slots whose ones row is masked
+    for (int64_t k = 0;; ++k) {
+      const int64_t idx = f4p_next(sh, k);
+      if (idx < 0) break;
+      const F4PItem it = f4p_item(P, items, idx);
+      // own arrival + the idle A warps' (12 - 2T, made by the dh = 0 warps)
+      const uint32_t cnt = 1u + (dh == 0 ? (uint32_t)(kF4Tiles - it.T) : 0u);
+      const int E = sh.E[k & 1];
+      __syncwarp();
+      if (lane == 0) f4_arrive(&sh.eempty[k & 1]);
+      const int e1 = 61 - E > 1000 ? 1000 : (61 - E < -1000 ? -1000 : 61 - E);
+      const double sc1 = ldexp(1.0, e1), sc2 = ldexp(1.0, 61 - E - e1);
+      for (int ss = 0; ss < it.nsup; ++ss, ++g) {
+        const uint32_t stage = g & 1u, use = g >> 1, jslot = g & 1u;
+        uint32_t x[kF4BW * kF4Sub];
+        int nval[kF4Sub];
+        f4_wait(&sh.jfull[jslot], use & 1u);
+        double vv[kF4Sub];
+#pragma unroll
+        for (int sub = 0; sub < kF4Sub; ++sub) vv[sub] = sh.vs[jslot][64 * sub + 32 * h + lane];
+        __syncwarp();
+        if (lane == 0) f4_arrive_cnt(&sh.jempty[jslot], cnt);
+#pragma unroll
+        for (int sub = 0; sub < kF4Sub; ++sub) {
+          const int ks = kF4Sub * ss + sub;
+          const int64_t c0 = it.pb + (int64_t)ks * 64 + 32 * h;
+          nval[sub] = (int)(it.pe - c0 < 0 ? 0 : (it.pe - c0 > 32 ? 32 : it.pe - c0));
+          unsigned long long U = 0ull;
+          if (lane < nval[sub]) {
+            const long long A = __double2ll_rn((vv[sub] * sc1) * sc2);
+            U = (unsigned long long)A ^ 0x8000000000000000ull;
+          }
+          if constexpr (kF4BW == 2) {
+            x[2 * sub] = ~(uint32_t)U;
+            x[2 * sub + 1] = ~(uint32_t)(U >> 32);
+          } else {
+            x[sub] = dh ? ~(uint32_t)(U >> 32) : ~(uint32_t)U;
+          }
+        }
+        f4_transpose<kF4BW * kF4Sub>(x, lane);
+        if (use > 0) f4_wait(&sh.empty[stage], (use - 1) & 1u);
+#pragma unroll
+        for (int sub = 0; sub < kF4Sub; ++sub) {
+          const uint32_t bt = s_u32(stages + stage * kF4Stage + kF4Tiles * kF4ATileS + sub * kF4BSub);
+          if constexpr (kF4BW == 2) {
+            f4_store_row_masked(bt + f4_off(lane, h), x[2 * sub], nval[sub]);
+            f4_store_row_masked(bt + f4_off(32 + lane, h), x[2 * sub + 1], nval[sub]);
+          } else {
+            f4_store_row_masked(bt + f4_off(32 * dh + lane, h), x[sub], nval[sub]);
+          }
+          // the ones row: +1.0 for the valid nonzeros of this chunk, 0.0 past the column end; a slot
+          // whose previous chunk was partial (an earlier item's end) gets its full row back
+          const uint32_t bit = 1u << (stage * kF4Sub + sub);
+          if (dh == 0 && (nval[sub] < 32 || (dirty & bit))) {
+            if (lane == 0) f4_store_row_masked(bt + f4_off(kF4Ones, h), 0u, nval[sub]);
+            dirty = nval[sub] < 32 ? (dirty | bit) : (dirty & ~bit);
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) f4_arrive_cnt(&sh.full[stage], cnt);
+      }
+    }
+  } else if (warp == kF4LoaderWarp) {
+    // ===================== loader: rowidx / vals -> smem ring =====================
+    uint32_t g = 0;
+    for (int64_t k = 0;; ++k) {
+      const int64_t idx = f4p_next(sh, k);
+      if (idx < 0) break;
+      const F4PItem it = f4p_item(P, items, idx);
+      for (int ss = 0; ss < it.nsup; ++ss, ++g) {
+        const uint32_t slot = g & 1u, use = g >> 1;
+        if (use > 0) f4_wait(&sh.jempty[slot], (use - 1) & 1u);
+#pragma unroll
+        for (int e = 0; e < 2 * kF4Sub; ++e) {
+          const int64_t p = it.pb + (int64_t)ss * (64 * kF4Sub) + 32 * e + lane;
+          const bool ok = p < it.pe;
+          const int64_t ps = ok ? p : it.pb;
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;"
+                       :: "r"(s_u32(&sh.js[slot][32 * e + lane])), "l"(P.rowidx + ps), "r"(ok ? 4 : 0) : "memory");
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;"
+                       :: "r"(s_u32(&sh.vs[slot][32 * e + lane])), "l"(vals + ps), "r"(ok ? 8 : 0) : "memory");
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" :: "r"(s_u32(&sh.jfull[slot])) : "memory");
+      }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  } else if (warp == kF4MmaWarp) {
+    // ===================== MMA issuer =====================
+    if (lane == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t idesc = f4_idesc();
+      uint32_t g = 0;
+      for (int64_t k = 0;; ++k) {
+        const int64_t idx = f4p_next(sh, k);
+        if (idx < 0) break;
+        const F4PItem it = f4p_item(P, items, idx);
+        if (k > 0) {   // item k-1's accumulators read out
+          f4_wait(&sh.tfree, (uint32_t)((k - 1) & 1));
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        }
+        for (int ss = 0; ss < it.nsup; ++ss, ++g) {
+          const uint32_t stage = g & 1u;
+          f4_wait(&sh.full[stage], (g >> 1) & 1u);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t sb = s_u32(stages + stage * kF4Stage);
+          for (int sub = 0; sub < kF4Sub; ++sub) {
+            const int ks = kF4Sub * ss + sub;
+            if (ks >= it.nsteps) break;
+            const uint64_t bdesc = f4_desc(sb + kF4Tiles * kF4ATileS + sub * kF4BSub);
+            for (int tt = 0; tt < it.T; ++tt) {
+              const uint64_t adesc = f4_desc(sb + tt * kF4ATileS + sub * kF4ATile);
+              asm volatile(
+                  "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                  "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}"
+                  :: "r"(tmem + (uint32_t)(tt * kF4N)), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(ks > 0 ? 1u : 0u),
+                     "r"(tmem + kF4SfCol), "r"(tmem + kF4SfCol + 32u));
+            }
+          }
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                       :: "r"(s_u32(&sh.empty[stage])) : "memory");
+        }
+        if (it.nsteps > 0)
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                       :: "r"(s_u32(&sh.done)) : "memory");
+        else
+          f4_arrive(&sh.done);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ===================== scan warp: the CTA's next item and its column scale E, one item ahead ====
+    // Item 0 is blockIdx.x; later items come from a global counter (dynamic: CTAs that drew shorter
+    // items take more of them, as the hardware scheduler does for one CTA per item).
+    for (int64_t k = 0;; ++k) {
+      if (k >= 2) f4_wait_sleep(&sh.eempty[k & 1], (uint32_t)(((k >> 1) - 1) & 1), 2000);
+      int64_t idx = blockIdx.x;
+      if (k > 0) {
+        unsigned long long v = 0;
+        if (lane == 0) v = atomicAdd(next_item, 1ull);
+        idx = G + (int64_t)__shfl_sync(0xFFFFFFFFu, v, 0);
+      }
+      if (idx >= n_items) idx = -1;
+      unsigned long long mx = 0;
+      if (idx >= 0) {
+        const F4PItem it = f4p_item(P, items, idx);
+        mx = f4p_scan(vals, it.pb, it.pe, lane);
+      }
+      if (lane == 0) {
+        const double m = __longlong_as_double((long long)mx);
+        int e = 0;
+        int nf = 0;
+        if (isfinite(m)) frexp(m, &e); else nf = 1;
+        sh.item[k & 1] = idx;
+        sh.E[k & 1] = e;
+        sh.nonfinite[k & 1] = nf;
+        f4_arrive(&sh.efull[k & 1]);
+      }
+      __syncwarp();
+      if (idx < 0) break;
+    }
+  }
+  __syncthreads();
+  if (warp == kF4MmaWarp) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(512));
+  }
+}
+
 }  // namespace
 
 int f4_tiles_per_cta() {   // SKETCH_F4_TILES (tuning only): fewer row tiles per CTA
@@ -483,7 +941,8 @@ __global__ void sk_f4_ieee_fixup_kernel(const ApplyArgs P, const TcItem* items, 
   }
 }
 
-cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const TcItem* items, int64_t n_items, cudaStream_t stream) {
+cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const TcItem* items, int64_t n_items, bool persist,
+                                cudaStream_t stream) {
   if (n_items == 0) return cudaSuccess;
   const size_t smem = (size_t)kF4Stages * kF4Stage + sizeof(F4Shared) + 1024;
   cudaError_t e = cudaFuncSetAttribute(sk_rad_f4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -491,7 +950,27 @@ cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const TcItem* items, int64_t
   static const int dbg = [] { const char* v = getenv("SKETCH_F4_DEBUG"); return v ? atoi(v) : 0; }();
   sk_f4_zero_split_kernel<<<(unsigned)n_items, 256, 0, stream>>>(a, items);
   e = cudaGetLastError();
-  if (e == cudaSuccess) {
+  if (e == cudaSuccess && persist) {
+    const size_t psmem = (size_t)kF4Stages * kF4Stage + sizeof(F4PShared) + 1024;
+    e = cudaFuncSetAttribute(sk_rad_f4p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+    int dev = 0, sms = 148;
+    if (e == cudaSuccess) e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    static const int grid_cap = [] { const char* v = getenv("SKETCH_F4_PGRID"); return v ? atoi(v) : 0; }();
+    if (grid_cap > 0 && grid_cap < sms) sms = grid_cap;   // (tests: many items per CTA on small inputs)
+    unsigned long long* ctr = nullptr;
+    if (e == cudaSuccess) e = scratch_alloc((void**)&ctr, sizeof(unsigned long long), stream);
+    if (e == cudaSuccess) {
+      e = cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), stream);
+      const int64_t grid = n_items < sms ? n_items : sms;
+      if (e == cudaSuccess) {
+        sk_rad_f4p_kernel<<<(unsigned)grid, kF4PThreads, psmem, stream>>>(a, items, n_items, ctr);
+        e = cudaGetLastError();
+      }
+      const cudaError_t e2 = cudaFreeAsync(ctr, stream);
+      if (e == cudaSuccess) e = e2;
+    }
+  } else if (e == cudaSuccess) {
     sk_rad_f4_kernel<<<(unsigned)n_items, kF4Threads, smem, stream>>>(a, items, dbg);
     e = cudaGetLastError();
   }

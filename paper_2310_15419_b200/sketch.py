@@ -29,7 +29,7 @@ EXPORTS = ["sketch_plan", "sketch_plan_host", "sketch_apply", "sketch_apply_csc"
            "sketch_apply_host", "sketch_fill_s", "sketch_plan_stats", "sketch_plan_destroy",
            "sketch_error_string", "sketch_last_error_detail", "sketch_version",
            "sketch_set_rad_f64_path", "sketch_apply_kernel_name", "sketch_set_pair_path",
-           "sketch_plan_host_jki"]
+           "sketch_plan_host_jki", "sketch_set_f4_persistent"]
 RAD_F64_PATHS = {"fp4": 0, "simt": 3}
 PAIR_PATHS = {"auto": 0, "kji": 1, "jki": 2}
 _STRING_RESULTS = ("sketch_error_string", "sketch_last_error_detail", "sketch_version",
@@ -46,7 +46,7 @@ class sk_stats_t(ctypes.Structure):
     _fields_ = [(name, ctypes.c_int64) for name in
                 ("d", "m", "n", "nnz", "row_offset", "max_col_nnz", "n_items_rad", "n_items_pair",
                  "philox_blocks_rad", "philox_blocks_pair", "plan_bytes", "n_items_jki", "jki_nonzero_rows", "n_items_f4_split",
-                 "n_items_f4", "n_cols_f4", "jki_block_cols")]
+                 "n_items_f4", "n_cols_f4", "jki_block_cols", "f4_persistent")]
 
 
 _lock = threading.Lock()
@@ -84,6 +84,7 @@ def load_library(path: str = LIB_PATH):
         lib.sketch_version.argtypes = []
         lib.sketch_version.restype = ctypes.c_char_p
         lib.sketch_set_rad_f64_path.argtypes = [i32]
+        lib.sketch_set_f4_persistent.argtypes = [i32]
         lib.sketch_set_pair_path.argtypes = [i32]
         lib.sketch_plan_host_jki.argtypes = [ctypes.POINTER(vp), i32, i64, i64, i64, i64, vp, vp, i64, i32, vp]
         lib.sketch_apply_kernel_name.argtypes = [vp, i32]
@@ -274,6 +275,13 @@ def set_rad_f64_path(path) -> None:
     cores for columns of 1280 .. 131071 nonzeros, SIMT for the rest; default) or "simt" (process-wide)."""
     p = RAD_F64_PATHS[path] if isinstance(path, str) else int(path)
     _check(load_library().sketch_set_rad_f64_path(p), "sketch_set_rad_f64_path")
+
+
+def set_f4_persistent(mode) -> None:
+    """Tensor-core columns of plans built from now on: "auto" (persistent kernel when the mean column
+    is short; default), "off" (one CTA per item) or "on" (persistent)."""
+    m = {"auto": -1, "off": 0, "on": 1}[mode] if isinstance(mode, str) else int(mode)
+    _check(load_library().sketch_set_f4_persistent(m), "sketch_set_f4_persistent")
 
 
 def set_pair_path(path) -> None:

@@ -278,7 +278,7 @@ def test_f4_last_wave_split_along_k(sk):
         assert st["n_cols_f4"] == 157 and st["n_items_rad"] > 0
         if torch.cuda.get_device_properties(0).multi_processor_count == 148:
             assert st["n_items_f4_split"] == 2 * 157
-        assert "sk_rad_f4_kernel" in plan.kernel_name("rademacher")
+        assert "sk_rad_f4" in plan.kernel_name("rademacher")
         vals = _dev(A.vals)
         o1 = plan.apply(vals, 3, "rademacher").T.cpu().numpy()
         o2 = plan.apply(vals, 3, "rademacher").T.cpu().numpy()
@@ -301,7 +301,7 @@ def test_f4_long_columns_next_to_tensor_columns(sk):
     try:
         st = plan.stats()
         assert st["n_cols_f4"] == 3 and st["n_items_rad"] > 0, st
-        assert "sk_rad_f4_kernel" in plan.kernel_name("rademacher")
+        assert "sk_rad_f4" in plan.kernel_name("rademacher")
         vals = _dev(A.vals)
         o1 = plan.apply(vals, 6, "rademacher").T.cpu().numpy()
         o2 = plan.apply(vals, 6, "rademacher").T.cpu().numpy()
@@ -311,6 +311,53 @@ def test_f4_long_columns_next_to_tensor_columns(sk):
         plan.close()
     ref, B = oracle.sketch(6, "rademacher", 1300, A.m, A.n, A.colptr, A.rowidx, A.vals, threads=16)
     _check(o1, ref, B, TOL["f64"])
+
+
+@pytest.mark.parametrize("d", [2000, 700, 2500])
+def test_f4_persistent_kernel_matches_per_item_kernel(sk, d):
+    # the persistent tensor-core kernel (one CTA per SM walking ~4 items each here: 600+ items of
+    # 6 / 6 / 4 or 6 or 5 / 5 / 5 / 5 row tiles, K-split last-wave halves, a NaN column, a column
+    # exactly at the threshold) computes every item with the same arithmetic as the one-CTA-per-item
+    # kernel: bit-identical results, and both match the oracle
+    import torch
+    rng = np.random.default_rng(d)
+    lens = [int(x) for x in rng.integers(1280, 9000, size=211)]
+    lens[3] = 1280
+    A = workloads.random_csc(50000, len(lens), lens, seed=d + 1)
+    A.vals[A.colptr[10] + 5] = np.nan
+    outs = {}
+    try:
+        for mode in ("off", "on"):
+            sk.set_f4_persistent(mode)
+            plan = sk.Plan(_dev(A.colptr), _dev(A.rowidx), d, A.m, "f64")
+            try:
+                st = plan.stats()
+                assert st["n_cols_f4"] == len(lens) and st["f4_persistent"] == (mode == "on")
+                assert ("sk_rad_f4p_kernel" in plan.kernel_name("rademacher")) == (mode == "on")
+                outs[mode] = plan.apply(_dev(A.vals), 12, "rademacher").T.cpu().numpy()
+                torch.cuda.synchronize()
+            finally:
+                plan.close()
+    finally:
+        sk.set_f4_persistent("auto")
+    assert np.array_equal(outs["on"], outs["off"], equal_nan=True)
+    ref, B = oracle.sketch(12, "rademacher", d, A.m, A.n, A.colptr, A.rowidx, A.vals, threads=16)
+    assert np.all(np.isnan(outs["on"][:, 10])) and np.all(np.isnan(ref[:, 10]))
+    keep = [k for k in range(A.n) if k != 10]
+    _check(outs["on"][:, keep], ref[:, keep], B[:, keep], TOL["f64"])
+
+
+def test_f4_persistent_selection(sk):
+    # the plan picks the persistent kernel for short tensor-core columns (mean < 16384 nonzeros: row
+    # shards of c5 from 4 GPUs on) and one CTA per item for long ones (c5 itself)
+    short = workloads.random_csc(100000, 300, 6000, seed=3)
+    long_ = workloads.random_csc(200000, 40, 40000, seed=4)
+    for A, want in ((short, 1), (long_, 0)):
+        plan = sk.Plan(_dev(A.colptr), _dev(A.rowidx), 1000, A.m, "f64")
+        try:
+            assert plan.stats()["f4_persistent"] == want
+        finally:
+            plan.close()
 
 
 @pytest.mark.parametrize("case", range(16))

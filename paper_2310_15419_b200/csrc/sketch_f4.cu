@@ -37,14 +37,9 @@ namespace {
 
 constexpr int kF4Tiles = 6;                       // 128-row tiles per CTA (max)
 constexpr int kF4AWarps = 2 * kF4Tiles;          // A producers: (tile, nonzero half)
-#ifndef SK_F4_BW
-#define SK_F4_BW 2
-#endif
-// B producers: (nonzero half h, digit half dh).  With 2 warps each makes all 64 digit rows of its
-// nonzero half; with 4 each makes 32 (the conversion is duplicated, the transposes and stores halved).
-constexpr int kF4BWarps = SK_F4_BW;
-constexpr int kF4BW = 2 * 2 / kF4BWarps;           // transposed words per K-step and B warp (2 or 1)
-static_assert(kF4BWarps == 2 || kF4BWarps == 4, "B producers");
+// B producers: nonzero half h, all 64 digit rows (4 warps with 32 rows each measured slower: c5
+// 7.58 vs 7.24 ms)
+constexpr int kF4BWarps = 2;
 constexpr int kF4Producers = kF4AWarps + kF4BWarps;
 constexpr int kF4LoaderWarp = kF4Producers;       // streams rowidx / vals into a smem ring
 constexpr int kF4MmaWarp = kF4Producers + 1;
@@ -306,14 +301,13 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
     }
   } else if (warp >= kF4AWarps && warp < kF4Producers) {
     // ===================== B producers: digits of nonzero half h =====================
-    const int bw = warp - kF4AWarps;
-    const int h = kF4BWarps == 2 ? bw : (bw & 1), dh = kF4BWarps == 2 ? 0 : (bw >> 1);
+    const int h = warp - kF4AWarps;
     // 2^(61-E) as two exact power-of-two factors (each within the double range)
     const int e1 = 61 - E > 1000 ? 1000 : (61 - E < -1000 ? -1000 : 61 - E);
     const double sc1 = ldexp(1.0, e1), sc2 = ldexp(1.0, 61 - E - e1);
     for (int ss = 0; ss < nsup; ++ss) {
       const int stage = ss % kF4Stages, use = ss / kF4Stages;
-      uint32_t x[kF4BW * kF4Sub];
+      uint32_t x[2 * kF4Sub];
       int nval[kF4Sub];
       const int jslot = ss % kF4JSlots;
       f4_wait(&sh.jfull[jslot], (ss / kF4JSlots) & 1);
@@ -335,26 +329,18 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
           const long long A = __double2ll_rn((v0 * sc1) * sc2);
           U = (unsigned long long)A ^ 0x8000000000000000ull;
         }
-        if constexpr (kF4BW == 2) {
-          x[2 * sub] = ~(uint32_t)U;               // sign bits of the digit nibbles
-          x[2 * sub + 1] = ~(uint32_t)(U >> 32);
-        } else {
-          x[sub] = dh ? ~(uint32_t)(U >> 32) : ~(uint32_t)U;
-        }
+        x[2 * sub] = ~(uint32_t)U;                 // sign bits of the digit nibbles
+        x[2 * sub + 1] = ~(uint32_t)(U >> 32);
       }
-      f4_transpose<kF4BW * kF4Sub>(x, lane);       // lane r: bit r (and 32 + r) of U per K-step
+      f4_transpose<2 * kF4Sub>(x, lane);           // lane r: bit r (and 32 + r) of U per K-step
       if (use > 0) f4_wait(&sh.empty[stage], (use - 1) & 1);
       if (!(dbg & 8)) {
 #pragma unroll
         for (int sub = 0; sub < kF4Sub; ++sub) {
           const uint32_t bt = s_u32(stages + stage * kF4Stage + kF4Tiles * kF4ATileS + sub * kF4BSub);
-          if constexpr (kF4BW == 2) {
-            f4_store_row_masked(bt + f4_off(lane, h), x[2 * sub], nval[sub]);
-            f4_store_row_masked(bt + f4_off(32 + lane, h), x[2 * sub + 1], nval[sub]);
-          } else {
-            f4_store_row_masked(bt + f4_off(32 * dh + lane, h), x[sub], nval[sub]);
-          }
-          if (nval[sub] < 32 && lane == 0 && dh == 0) {   // partial (last) K chunk: the ones row too
+          f4_store_row_masked(bt + f4_off(lane, h), x[2 * sub], nval[sub]);
+          f4_store_row_masked(bt + f4_off(32 + lane, h), x[2 * sub + 1], nval[sub]);
+          if (nval[sub] < 32 && lane == 0) {   // partial (last) K chunk: the ones row too
             const uint32_t z = 0u;              // (y = 0 -> nibbles 0x2 = +1.0)
             f4_store_row_masked(bt + f4_off(kF4Ones, h), z, nval[sub]);
           }
@@ -738,16 +724,14 @@ __global__ void __launch_bounds__(kF4PThreads, 1) sk_rad_f4p_kernel(const ApplyA
     }
   } else if (warp < kF4Producers) {
     // ===================== B producers: digits of nonzero half h =====================
-    const int bw = warp - kF4AWarps;
-    const int h = kF4BWarps == 2 ? bw : (bw & 1), dh = kF4BWarps == 2 ? 0 : (bw >> 1);
+    const int h = warp - kF4AWarps;
     uint32_t g = 0;
     uint32_t dirty = 0;                            // (stage, sub) slots whose ones row is masked
     for (int64_t k = 0;; ++k) {
       const int64_t idx = f4p_next(sh, k);
       if (idx < 0) break;
       const F4PItem it = f4p_item(P, items, idx);
-      // own arrival + the idle A warps' (12 - 2T, made by the dh = 0 warps)
-      const uint32_t cnt = 1u + (dh == 0 ? (uint32_t)(kF4Tiles - it.T) : 0u);
+      const uint32_t cnt = 1u + (uint32_t)(kF4Tiles - it.T);   // own arrival + those of the idle A warps (12 - 2T)
       const int E = sh.E[k & 1];
       __syncwarp();
       if (lane == 0) f4_arrive(&sh.eempty[k & 1]);
@@ -755,7 +739,7 @@ __global__ void __launch_bounds__(kF4PThreads, 1) sk_rad_f4p_kernel(const ApplyA
       const double sc1 = ldexp(1.0, e1), sc2 = ldexp(1.0, 61 - E - e1);
       for (int ss = 0; ss < it.nsup; ++ss, ++g) {
         const uint32_t stage = g & 1u, use = g >> 1, jslot = g & 1u;
-        uint32_t x[kF4BW * kF4Sub];
+        uint32_t x[2 * kF4Sub];
         int nval[kF4Sub];
         f4_wait(&sh.jfull[jslot], use & 1u);
         double vv[kF4Sub];
@@ -773,28 +757,20 @@ __global__ void __launch_bounds__(kF4PThreads, 1) sk_rad_f4p_kernel(const ApplyA
             const long long A = __double2ll_rn((vv[sub] * sc1) * sc2);
             U = (unsigned long long)A ^ 0x8000000000000000ull;
           }
-          if constexpr (kF4BW == 2) {
-            x[2 * sub] = ~(uint32_t)U;
-            x[2 * sub + 1] = ~(uint32_t)(U >> 32);
-          } else {
-            x[sub] = dh ? ~(uint32_t)(U >> 32) : ~(uint32_t)U;
-          }
+          x[2 * sub] = ~(uint32_t)U;
+          x[2 * sub + 1] = ~(uint32_t)(U >> 32);
         }
-        f4_transpose<kF4BW * kF4Sub>(x, lane);
+        f4_transpose<2 * kF4Sub>(x, lane);
         if (use > 0) f4_wait(&sh.empty[stage], (use - 1) & 1u);
 #pragma unroll
         for (int sub = 0; sub < kF4Sub; ++sub) {
           const uint32_t bt = s_u32(stages + stage * kF4Stage + kF4Tiles * kF4ATileS + sub * kF4BSub);
-          if constexpr (kF4BW == 2) {
-            f4_store_row_masked(bt + f4_off(lane, h), x[2 * sub], nval[sub]);
-            f4_store_row_masked(bt + f4_off(32 + lane, h), x[2 * sub + 1], nval[sub]);
-          } else {
-            f4_store_row_masked(bt + f4_off(32 * dh + lane, h), x[sub], nval[sub]);
-          }
+          f4_store_row_masked(bt + f4_off(lane, h), x[2 * sub], nval[sub]);
+          f4_store_row_masked(bt + f4_off(32 + lane, h), x[2 * sub + 1], nval[sub]);
           // the ones row: +1.0 for the valid nonzeros of this chunk, 0.0 past the column end; a slot
           // whose previous chunk was partial (an earlier item's end) gets its full row back
           const uint32_t bit = 1u << (stage * kF4Sub + sub);
-          if (dh == 0 && (nval[sub] < 32 || (dirty & bit))) {
+          if (nval[sub] < 32 || (dirty & bit)) {
             if (lane == 0) f4_store_row_masked(bt + f4_off(kF4Ones, h), 0u, nval[sub]);
             dirty = nval[sub] < 32 ? (dirty | bit) : (dirty & ~bit);
           }

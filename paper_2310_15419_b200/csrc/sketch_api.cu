@@ -200,9 +200,9 @@ int64_t f4_min_column() {
 // up once, the next item's column scale computed ahead, its first stage produced before the previous
 // item's read-out) when the tensor-core columns are short on average: per-item set-up and pipeline
 // fill then weigh more than the persistent kernel's slightly longer stage loop.  Measured on c5 row
-// shards (scripts/gpu_r2ac.sh, profiles/r02_f4_persistent_sweep.txt): mean column 50000 nonzeros
-// 7.24 -> 7.44 ms, 25000 3.73 -> 3.75, 12500 1.97 -> 1.92, 6250 1.089 -> 1.013, 3125 0.617 -> 0.574.
-// SKETCH_F4_PERSIST = 0 | 1 forces the choice.
+// shards (scripts/gpu_r2af.sh, profiles/r02_f4_persistent_sweep.txt): mean column 50000 nonzeros
+// 7.234 -> 7.248 ms, 25000 3.728 -> 3.677, 6250 1.089 -> 0.998.  SKETCH_F4_PERSIST = 0 | 1 forces
+// the choice.
 std::atomic<int> g_f4_persist{-2};   // -2: not read yet
 
 bool f4_use_persistent(int64_t mean_col) {
@@ -213,7 +213,7 @@ bool f4_use_persistent(int64_t mean_col) {
     g_f4_persist.store(v, std::memory_order_relaxed);
   }
   if (v >= 0) return v != 0;
-  return mean_col < 16384;
+  return mean_col < 32768;
 }
 
 const char* kernel_name(const sk_plan_s* p, int dist);

@@ -588,6 +588,9 @@ __device__ __forceinline__ void f4p_a_stage(F4PShared& sh, unsigned char* stages
 }
 
 // Epilogue of item k (warps 0..11): wait for its accumulators, read TMEM, form Â, free TMEM.
+// The ones row of B stays all +1.0 in the persistent kernel, so D[i, 64] also sums S over the padded
+// K positions of the item's last K-step (nsteps 64 - L of them); the loader zero-filled their row
+// index, so each is S[i, row_offset + 0], and D[i, 64] - pad S[i, row_offset] is the plain Σ_p S[i, p].
 __device__ __forceinline__ void f4p_epilogue(F4PShared& sh, const ApplyArgs& P, const F4PItem& it, int64_t k,
                                              uint32_t tmem, int warp, int lane) {
   f4_wait_sleep(&sh.done, (uint32_t)(k & 1), 200);
@@ -620,6 +623,12 @@ __device__ __forceinline__ void f4p_epilogue(F4PShared& sh, const ApplyArgs& P, 
       }
     }
     const int64_t row = (int64_t)(it.tile0 + tt) * 128 + 32 * qw + lane;
+    const int pad = it.nsteps * 64 - (int)(it.pe - it.pb);
+    if (pad > 0) {
+      const uint4 x0 = s_block((uint32_t)(it.tile0 + tt), (uint64_t)P.row_offset, P.keys);
+      const uint32_t w = qw == 0 ? x0.x : qw == 1 ? x0.y : qw == 2 ? x0.z : x0.w;
+      ones -= ((w >> lane) & 1u) ? -(long long)pad : (long long)pad;   // bit 1 -> S = -1
+    }
     if (row < P.d) {
       const double v = scalbn((double)hi * 4294967296.0 + (double)(lo - ones), E - 62);
       const double res = nonfinite ? nan : v;
@@ -691,9 +700,12 @@ __global__ void __launch_bounds__(kF4PThreads, 1) sk_rad_f4p_kernel(const ApplyA
     uint32_t g = 0;
     F4PItem prev{};
     bool pending = false;                          // prev's epilogue not done yet
-    PhiloxKeys keys = P.keys;                      // in registers across the item loop (not reloaded
-#pragma unroll                                     // from the constant bank every stage)
-    for (int r = 0; r < 10; ++r) asm volatile("" : "+r"(keys.k0[r]), "+r"(keys.k1[r]));
+    PhiloxKeys keys;                               // in per-thread registers across the item loop (a
+#pragma unroll                                     // shuffle hides their uniformity, so they are not
+    for (int r = 0; r < 10; ++r) {                 // re-read from the constant bank every stage)
+      keys.k0[r] = __shfl_sync(0xFFFFFFFFu, P.keys.k0[r], lane);
+      keys.k1[r] = __shfl_sync(0xFFFFFFFFu, P.keys.k1[r], lane);
+    }
     const uint64_t row_offset = (uint64_t)P.row_offset;
     for (int64_t k = 0;; ++k) {
       const int64_t idx = f4p_next(sh, k);
@@ -726,7 +738,6 @@ __global__ void __launch_bounds__(kF4PThreads, 1) sk_rad_f4p_kernel(const ApplyA
     // ===================== B producers: digits of nonzero half h =====================
     const int h = warp - kF4AWarps;
     uint32_t g = 0;
-    uint32_t dirty = 0;                            // (stage, sub) slots whose ones row is masked
     for (int64_t k = 0;; ++k) {
       const int64_t idx = f4p_next(sh, k);
       if (idx < 0) break;
@@ -767,13 +778,7 @@ __global__ void __launch_bounds__(kF4PThreads, 1) sk_rad_f4p_kernel(const ApplyA
           const uint32_t bt = s_u32(stages + stage * kF4Stage + kF4Tiles * kF4ATileS + sub * kF4BSub);
           f4_store_row_masked(bt + f4_off(lane, h), x[2 * sub], nval[sub]);
           f4_store_row_masked(bt + f4_off(32 + lane, h), x[2 * sub + 1], nval[sub]);
-          // the ones row: +1.0 for the valid nonzeros of this chunk, 0.0 past the column end; a slot
-          // whose previous chunk was partial (an earlier item's end) gets its full row back
-          const uint32_t bit = 1u << (stage * kF4Sub + sub);
-          if (nval[sub] < 32 || (dirty & bit)) {
-            if (lane == 0) f4_store_row_masked(bt + f4_off(kF4Ones, h), 0u, nval[sub]);
-            dirty = nval[sub] < 32 ? (dirty | bit) : (dirty & ~bit);
-          }
+          // (the ones row stays all +1.0: the padding's share of D[i, 64] is removed in the read-out)
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();

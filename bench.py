@@ -101,13 +101,14 @@ class ClockSampler:
 
 
 def launches_per_apply(plan, dist: str, stats: dict) -> int:
-    """Kernels of the library one sketch_apply launches.  ±1: the tensor-core kernel with its two small
-    companions (zeroing of the K-split rows, IEEE fix-up of non-finite columns) when columns of 1280 ..
+    """Kernels of the library one sketch_apply launches.  ±1: the tensor-core kernel with its IEEE fix-up
+    of non-finite columns (and the zeroing of the K-split rows when the plan split its last wave) when columns of 1280 ..
     131071 nonzeros exist (fp64), the SIMT kernel for the other columns, and for fp32 the IEEE fix-up
     scan.  Uniform / Gaussian: the fused kernel, or Algorithm 4's gather + kernel (+ the finishing sum
     of split column blocks)."""
     if dist == "rademacher":
-        n = 3 * int(stats.get("n_items_f4", 0) > 0) + int(stats["n_items_rad"] > 0)
+        f4 = int(stats.get("n_items_f4", 0) > 0)
+        n = 2 * f4 + int(f4 and stats.get("n_items_f4_split", 0) > 0) + int(stats["n_items_rad"] > 0)
         if "sk_rad_kernel<float>" in plan.kernel_name(dist) and stats["n_items_rad"] > 0:
             n += 1
         return n

@@ -63,8 +63,9 @@ constexpr int64_t kTcMaxColumn = 131071;
 
 // The tensor-core kernel, with the zeroing of the K-split rows before it and the IEEE fix-up of the
 // columns it found non-finite after it.
-cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const TcItem* items, int64_t n_items, bool persistent,
-                                cudaStream_t stream);
+// split_begin: first item of the K-split tail (n_items when there is none: no zeroing launch).
+cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const TcItem* items, int64_t n_items, int64_t split_begin,
+                                bool persistent, cudaStream_t stream);
 
 // ±1 sketch columns holding a NaN / Inf value get the IEEE result (sketch_kernels.cu): a scan of
 // every column's values, one warp per column (dtype 0 = f64, 1 = f32).
@@ -117,6 +118,9 @@ struct JkiPlanView {
 // Stream-ordered scratch from the library's own memory pool on the current device (its release
 // threshold keeps freed memory mapped, so per-apply scratch does not re-map pages every call).
 cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t stream);
+// cudaFuncSetAttribute(kernel, MaxDynamicSharedMemorySize, bytes) once per (kernel, device) and size:
+// the call costs several µs of host time, which a small apply (c1) otherwise pays every launch.
+cudaError_t set_max_dynamic_smem(const void* kernel, size_t bytes);
 int jki_block_cols(int dtype);
 size_t jki_smem(int dtype, int bn);
 cudaError_t launch_apply_jki(int dist, int dtype, const ApplyArgs& a, const JkiPlanView& J, cudaStream_t stream);

@@ -56,6 +56,20 @@ cudaError_t scratch_alloc(void** ptr, size_t bytes, cudaStream_t stream) {
   }
   return cudaMallocFromPoolAsync(ptr, bytes, pool, stream);
 }
+
+cudaError_t set_max_dynamic_smem(const void* kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<const void*, int>, size_t>> done;   // ((kernel, device), bytes)
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& d : done)
+    if (d.first.first == kernel && d.first.second == dev && d.second >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) done.push_back({{kernel, dev}, bytes});
+  return e;
+}
 }  // namespace sk
 
 namespace {
@@ -247,6 +261,7 @@ struct sk_plan_s {
   int64_t f4_split_items = 0;       // half items of the K-split last wave
   int64_t f4_cols = 0;              // columns on the tensor-core kernel (the rest: n_rad SIMT items)
   bool f4_persist = false;          // the persistent tensor-core kernel (short mean column, f4_use_persistent)
+  int64_t f4_split_begin = 0;       // first item of the K-split tail (n_f4: none)
   // Algorithm 4 (jki) structure: one device block holding items, grp_rows, row_j, row_ent, ent, ent_base
   void* d_jki = nullptr;
   sk::JkiPlanView jki{};
@@ -600,6 +615,9 @@ int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
     if (!tc_cols.empty()) {
       f4 = build_tc_schedule(h_colptr, d, sk::f4_tiles_per_cta(), tc_cols);
       p->f4_split_items = split_f4_tail(f4, h_colptr);
+      p->f4_split_begin = (int64_t)f4.size();
+      for (size_t i = 0; i < f4.size(); ++i)
+        if (f4[i].pad) { p->f4_split_begin = (int64_t)i; break; }
       int64_t tc_nnz = 0;
       for (int32_t k : tc_cols) tc_nnz += h_colptr[k + 1] - h_colptr[k];
       p->f4_persist = f4_use_persistent(tc_nnz / (int64_t)tc_cols.size());
@@ -725,10 +743,10 @@ int apply_items(const sk_plan_s* p, uint64_t seed, sk_dist_t dist, const void* v
       if (e == cudaSuccess) e = cudaStreamWaitEvent(sp.side, sp.fork, 0);
       if (e == cudaSuccess) e = sk::launch_apply(0, (int)p->dtype, a, sp.side);
       if (e == cudaSuccess) e = cudaEventRecord(sp.join, sp.side);
-      if (e == cudaSuccess) e = sk::launch_apply_rad_f4(a, p->d_f4, p->n_f4, p->f4_persist, stream);
+      if (e == cudaSuccess) e = sk::launch_apply_rad_f4(a, p->d_f4, p->n_f4, p->f4_split_begin, p->f4_persist, stream);
       if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, sp.join, 0);
     } else if (p->n_f4 > 0) {
-      e = sk::launch_apply_rad_f4(a, p->d_f4, p->n_f4, p->f4_persist, stream);
+      e = sk::launch_apply_rad_f4(a, p->d_f4, p->n_f4, p->f4_split_begin, p->f4_persist, stream);
     } else {
       e = sk::launch_apply(0, (int)p->dtype, a, stream);
     }

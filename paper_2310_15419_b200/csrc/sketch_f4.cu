@@ -922,18 +922,20 @@ __global__ void sk_f4_ieee_fixup_kernel(const ApplyArgs P, const TcItem* items, 
   }
 }
 
-cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const TcItem* items, int64_t n_items, bool persist,
-                                cudaStream_t stream) {
+cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const TcItem* items, int64_t n_items, int64_t split_begin,
+                                bool persist, cudaStream_t stream) {
   if (n_items == 0) return cudaSuccess;
   const size_t smem = (size_t)kF4Stages * kF4Stage + sizeof(F4Shared) + 1024;
-  cudaError_t e = cudaFuncSetAttribute(sk_rad_f4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = set_max_dynamic_smem((const void*)sk_rad_f4_kernel, smem);
   if (e != cudaSuccess) return e;
   static const int dbg = [] { const char* v = getenv("SKETCH_F4_DEBUG"); return v ? atoi(v) : 0; }();
-  sk_f4_zero_split_kernel<<<(unsigned)n_items, 256, 0, stream>>>(a, items);
-  e = cudaGetLastError();
+  if (split_begin < n_items) {
+    sk_f4_zero_split_kernel<<<(unsigned)(n_items - split_begin), 256, 0, stream>>>(a, items + split_begin);
+    e = cudaGetLastError();
+  }
   if (e == cudaSuccess && persist) {
     const size_t psmem = (size_t)kF4Stages * kF4Stage + sizeof(F4PShared) + 1024;
-    e = cudaFuncSetAttribute(sk_rad_f4p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+    e = set_max_dynamic_smem((const void*)sk_rad_f4p_kernel, psmem);
     int dev = 0, sms = 148;
     if (e == cudaSuccess) e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

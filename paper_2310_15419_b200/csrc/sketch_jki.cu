@@ -265,7 +265,7 @@ __global__ void sk_jki_finish_kernel(const ApplyArgs P, const JkiPlanView J, con
 template <int DIST, typename T>
 cudaError_t launch_jki_t(const ApplyArgs& a, const JkiPlanView& J, cudaStream_t stream) {
   const size_t smem = jki_smem_bytes<T>(J.bn);
-  cudaError_t e = cudaFuncSetAttribute(sk_jki_kernel<DIST, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = set_max_dynamic_smem((const void*)sk_jki_kernel<DIST, T>, smem);
   if (e != cudaSuccess) return e;
   // scratch (stream-ordered, library pool): values in CSR order, then the workspace slots of split blocks
   const size_t vbytes = ((size_t)J.n_ent * sizeof(T) + 255) & ~(size_t)255;

@@ -344,7 +344,7 @@ __global__ void sk_validate_rows_kernel(const int32_t* __restrict__ rowidx, int6
 template <typename K>
 cudaError_t launch_items(K kernel, size_t smem, const ApplyArgs& a, cudaStream_t stream) {
   if (a.n_items == 0) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = set_max_dynamic_smem((const void*)kernel, smem);
   if (e != cudaSuccess) return e;
   kernel<<<(unsigned)a.n_items, kThreads, smem, stream>>>(a);
   return cudaGetLastError();

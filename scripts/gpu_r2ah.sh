@@ -1,0 +1,6 @@
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1 || { echo build failed; exit 1; }
+for rep in 1 2; do
+  for lib in paper_2310_15419_b200/libsketch.so variants_tmp/libsk_o2.so variants_tmp/libsk_o3.so; do for rows in 50000000 6250000; do
+    echo "$lib rows=$rows $(SKETCH_LIB=$lib SKETCH_F4_PERSIST=1 timeout 120 python scripts/profile_apply.py --config c5 --rows $rows --reps 7 2>&1 | grep '^ms')"
+  done; done
+done

@@ -66,8 +66,13 @@ class _FakePlan:
 
 def test_launch_count_per_kernel_family():
     f4 = _FakePlan("sk_rad_f4_kernel (tcgen05 kind::mxf4) + sk_rad_kernel<double>")
-    assert bench.launches_per_apply(f4, "rademacher", {"n_items_rad": 0, "n_items_pair": 9, "n_items_f4": 3000}) == 3
-    assert bench.launches_per_apply(f4, "rademacher", {"n_items_rad": 5, "n_items_pair": 9, "n_items_f4": 3000}) == 4
+    # tensor-core kernel + IEEE fix-up, + the zeroing kernel when the last wave was split along K
+    assert bench.launches_per_apply(f4, "rademacher", {"n_items_rad": 0, "n_items_pair": 9, "n_items_f4": 3000,
+                                                       "n_items_f4_split": 80}) == 3
+    assert bench.launches_per_apply(f4, "rademacher", {"n_items_rad": 0, "n_items_pair": 9, "n_items_f4": 2960,
+                                                       "n_items_f4_split": 0}) == 2
+    assert bench.launches_per_apply(f4, "rademacher", {"n_items_rad": 5, "n_items_pair": 9, "n_items_f4": 3000,
+                                                       "n_items_f4_split": 80}) == 4
     assert bench.launches_per_apply(f4, "rademacher", {"n_items_rad": 5, "n_items_pair": 9, "n_items_f4": 0}) == 1
     f32 = _FakePlan("sk_rad_kernel<float>")
     assert bench.launches_per_apply(f32, "rademacher", {"n_items_rad": 5, "n_items_pair": 9, "n_items_f4": 0}) == 2

@@ -86,8 +86,8 @@ typedef struct {
     int64_t n_items_f4;        /* CTAs of the tensor-core kernel of one SK_RADEMACHER apply */
     int64_t n_cols_f4;         /* columns on the tensor-core kernel (the others: n_items_rad SIMT CTAs) */
     int64_t jki_block_cols;    /* b_n of the Algorithm 4 column blocks (384 f64, 768 f32), 0 if not built */
-    int64_t f4_persistent;     /* 1: the tensor-core columns run on the persistent kernel (mean column
-                                  < 32768 nonzeros; SKETCH_F4_PERSIST = 0 | 1 forces), 0: one CTA per item */
+    int64_t f4_persistent;     /* 1: the tensor-core columns run on the persistent kernel (more items than
+                                  SMs; SKETCH_F4_PERSIST = 0 | 1 forces), 0: one CTA per item */
 } sk_stats_t;
 
 /*
@@ -197,8 +197,8 @@ int sketch_set_rad_f64_path(int path);
 /*
  * sketch_set_f4_persistent -- how plans built from now on run their tensor-core columns (process-wide):
  * -1 (default) the persistent kernel (one CTA per SM walking the work items, TMEM / barriers set up
- * once, the next item's column scale computed ahead) when the mean tensor-core column has fewer than
- * 32768 nonzeros, else one CTA per item; 0 always one CTA per item; 1 always persistent.  Same
+ * once, the next item's column scale computed ahead) when there is more than one wave of tensor-core
+ * items (more items than SMs), else one CTA per item; 0 always one CTA per item; 1 always persistent.  Same
  * results either way (the same per-item arithmetic).  Initialised from SKETCH_F4_PERSIST = 0 | 1.
  * Errors: SK_EINVAL for another value.
  */

@@ -212,14 +212,14 @@ int64_t f4_min_column() {
 
 // Persistent tensor-core kernel (one CTA per SM walking the items; TMEM / barriers / constant rows set
 // up once, the next item's column scale computed ahead, its first stage produced before the previous
-// item's read-out) when the tensor-core columns are short on average: per-item set-up and pipeline
-// fill then weigh more than the persistent kernel's slightly longer stage loop.  Measured on c5 row
-// shards (scripts/gpu_r2af.sh, profiles/r02_f4_persistent_sweep.txt): mean column 50000 nonzeros
-// 7.234 -> 7.248 ms, 25000 3.728 -> 3.677, 6250 1.089 -> 0.998.  SKETCH_F4_PERSIST = 0 | 1 forces
-// the choice.
+// item's read-out) whenever there is more than one wave of items: it saves the per-item set-up, scan
+// and pipeline fill.  Measured (scripts/gpu_r2aj.sh, profiles/r02_f4_persistent_sweep.txt), per-item ->
+// persistent: c5 7.234 -> 7.165 ms, its 2-way row shard 3.727 -> 3.635, 8-way 1.088 -> 0.988, 1480
+// items of 8192 nonzeros 0.726 -> 0.672; one item per SM (148 x 131071) 1.019 -> 1.025, so a single
+// wave keeps one CTA per item.  SKETCH_F4_PERSIST = 0 | 1 forces the choice.
 std::atomic<int> g_f4_persist{-2};   // -2: not read yet
 
-bool f4_use_persistent(int64_t mean_col) {
+bool f4_use_persistent(int64_t n_items) {
   int v = g_f4_persist.load(std::memory_order_relaxed);
   if (v == -2) {
     const char* e = getenv("SKETCH_F4_PERSIST");
@@ -227,7 +227,9 @@ bool f4_use_persistent(int64_t mean_col) {
     g_f4_persist.store(v, std::memory_order_relaxed);
   }
   if (v >= 0) return v != 0;
-  return mean_col < 32768;
+  int W = kSMs, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&W, cudaDevAttrMultiProcessorCount, dev);
+  return n_items > W;
 }
 
 const char* kernel_name(const sk_plan_s* p, int dist);
@@ -260,7 +262,7 @@ struct sk_plan_s {
   int64_t n_f4 = 0;
   int64_t f4_split_items = 0;       // half items of the K-split last wave
   int64_t f4_cols = 0;              // columns on the tensor-core kernel (the rest: n_rad SIMT items)
-  bool f4_persist = false;          // the persistent tensor-core kernel (short mean column, f4_use_persistent)
+  bool f4_persist = false;          // the persistent tensor-core kernel (more than one wave of items)
   int64_t f4_split_begin = 0;       // first item of the K-split tail (n_f4: none)
   // Algorithm 4 (jki) structure: one device block holding items, grp_rows, row_j, row_ent, ent, ent_base
   void* d_jki = nullptr;
@@ -618,9 +620,7 @@ int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
       p->f4_split_begin = (int64_t)f4.size();
       for (size_t i = 0; i < f4.size(); ++i)
         if (f4[i].pad) { p->f4_split_begin = (int64_t)i; break; }
-      int64_t tc_nnz = 0;
-      for (int32_t k : tc_cols) tc_nnz += h_colptr[k + 1] - h_colptr[k];
-      p->f4_persist = f4_use_persistent(tc_nnz / (int64_t)tc_cols.size());
+      p->f4_persist = f4_use_persistent((int64_t)f4.size());
     }
     p->f4_cols = (int64_t)tc_cols.size();
   }

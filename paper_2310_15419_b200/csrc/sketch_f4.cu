@@ -479,6 +479,7 @@ struct F4PShared {
   uint32_t js[kF4JSlots][64 * kF4Sub];
   double vs[kF4JSlots][64 * kF4Sub];
   int64_t item[2];              // item index of the CTA's item k in slot k % 2 (-1: no more items)
+  unsigned long long mx0;       // max |a| bits of item 0 (scanned by the whole CTA)
   int32_t E[2];
   int32_t nonfinite[2];
   uint32_t tmem_base;
@@ -664,6 +665,7 @@ __global__ void __launch_bounds__(kF4PThreads, 1) sk_rad_f4p_kernel(const ApplyA
     f4_mbar_init(&sh.done, 1);
     f4_mbar_init(&sh.tfree, kF4PEpiWarps);
     for (int s = 0; s < 2; ++s) { f4_mbar_init(&sh.efull[s], 1); f4_mbar_init(&sh.eempty[s], kF4PEpiWarps + kF4BWarps); }
+    sh.mx0 = 0ull;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kF4MmaWarp) {
@@ -689,6 +691,12 @@ __global__ void __launch_bounds__(kF4PThreads, 1) sk_rad_f4p_kernel(const ApplyA
                    :: "r"(taddr + c), "r"(v) : "memory");
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  }
+  {   // item 0's column scale: the whole CTA scans (later items: the scan warp, one item ahead)
+    const F4PItem it0 = f4p_item(P, items, blockIdx.x);
+    unsigned long long mx = col_absmax_bits(vals, it0.pb, it0.pe, threadIdx.x, kF4PThreads);
+    for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+    if (lane == 0) atomicMax(&sh.mx0, mx);
   }
   __syncthreads();
 
@@ -865,8 +873,8 @@ __global__ void __launch_bounds__(kF4PThreads, 1) sk_rad_f4p_kernel(const ApplyA
         idx = G + (int64_t)__shfl_sync(0xFFFFFFFFu, v, 0);
       }
       if (idx >= n_items) idx = -1;
-      unsigned long long mx = 0;
-      if (idx >= 0) {
+      unsigned long long mx = k == 0 ? sh.mx0 : 0ull;
+      if (idx >= 0 && k > 0) {
         const F4PItem it = f4p_item(P, items, idx);
         mx = f4p_scan(vals, it.pb, it.pe, lane);
       }

@@ -89,9 +89,14 @@ def test_traffic_lookup_matches_the_committed_capture():
         t = json.load(f)
     v = bench.load_profile_traffic("c5", "sk_rad_f4_kernel (tcgen05 kind::mxf4)")
     assert v == t["c5"]["sk_rad_f4_kernel"]
-    # the headline kernel reads A once: DRAM traffic within 2% of the algorithmic bytes
+    vp = bench.load_profile_traffic("c5", "sk_rad_f4p_kernel (tcgen05 kind::mxf4, persistent)")
+    assert vp == t["c5"]["sk_rad_f4p_kernel"]
+    # the per-item kernel reads A once (DRAM traffic within 2% of the algorithmic bytes); the persistent
+    # one re-reads ~12% (its scan warp reads the next item's column while 148 columns are in flight:
+    # ~148 MB of working set against the 126 MB L2)
     alg = algorithmic_bytes(2000, 1000, 50_000_000, 8)
     assert abs(v - alg) / alg < 0.02
+    assert 0 <= (vp - alg) / alg < 0.15
 
 
 def test_metric_and_bytes_arithmetic():

@@ -348,8 +348,8 @@ def test_f4_persistent_kernel_matches_per_item_kernel(sk, d):
 
 
 def test_f4_persistent_selection(sk):
-    # the plan picks the persistent kernel for short tensor-core columns (mean < 32768 nonzeros: row
-    # shards of c5 from 2 GPUs on) and one CTA per item for long ones (c5 itself)
+    # the plan picks the persistent kernel when there is more than one wave of tensor-core items (600
+    # items here, c5's 3188) and one CTA per item for a single wave (80 items)
     short = workloads.random_csc(100000, 300, 6000, seed=3)
     long_ = workloads.random_csc(200000, 40, 40000, seed=4)
     for A, want in ((short, 1), (long_, 0)):

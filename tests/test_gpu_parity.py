@@ -360,6 +360,45 @@ def test_f4_persistent_selection(sk):
             plan.close()
 
 
+def test_apply_captures_into_cuda_graph(sk):
+    # sketch_apply is stream-ordered all the way down (kernels, the library pool's scratch, the
+    # persistent kernel's item counter, the side stream of the SIMT columns joined by events), so a
+    # CUDA graph captures it and replays it with the eager results, bit for bit: ±1 with tensor-core
+    # (persistent) and SIMT columns, uniform Algorithm 3, Gaussian Algorithm 4
+    import torch
+    lens = [3000] * 300 + [50, 700, 0, 200000]
+    A = workloads.random_csc(300000, len(lens), lens, seed=41)
+    R = workloads.abnormal_paper("A", m=20000, n=70, seed=1)
+    cases = [(A, "rademacher", False, 600), (A, "uniform", False, 600), (R, "gaussian", True, 700)]
+    for M, dist, jki, d in cases:
+        plan = sk.Plan(_dev(M.colptr), _dev(M.rowidx), d, M.m, "f64", jki=jki)
+        try:
+            if dist == "rademacher":
+                st = plan.stats()
+                assert st["n_items_f4"] > 0 and st["n_items_rad"] > 0
+            if jki:
+                sk.set_pair_path("jki")
+            vals = _dev(M.vals)
+            eager = plan.apply(vals, 17, dist).clone()
+            out = torch.empty_like(eager)
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                plan.apply(vals, 17, dist, out=out)          # warm-up on the capture stream
+            torch.cuda.current_stream().wait_stream(s)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                plan.apply(vals, 17, dist, out=out)
+            for _ in range(2):
+                out.zero_()
+                g.replay()
+                torch.cuda.synchronize()
+                assert torch.equal(out, eager), (dist, float((out - eager).abs().max()))
+        finally:
+            sk.set_pair_path("auto")
+            plan.close()
+
+
 @pytest.mark.parametrize("case", range(16))
 def test_randomized_shapes_match_oracle(sk, case):
     # seeded random shapes through the default kernel selection: m, n, column lengths (empty,

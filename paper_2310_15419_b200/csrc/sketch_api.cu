@@ -213,7 +213,7 @@ int64_t f4_min_column() {
 // Persistent tensor-core kernel (one CTA per SM walking the items; TMEM / barriers / constant rows set
 // up once, the next item's column scale computed ahead, its first stage produced before the previous
 // item's read-out) whenever there is more than one wave of items: it saves the per-item set-up, scan
-// and pipeline fill.  Measured (scripts/gpu_r2aj.sh, profiles/r02_f4_persistent_sweep.txt), per-item ->
+// and pipeline fill.  Measured (scripts/gpurun/gpu_r2aj.sh, profiles/r02_f4_persistent_sweep.txt), per-item ->
 // persistent: c5 7.234 -> 7.165 ms, its 2-way row shard 3.727 -> 3.635, 8-way 1.088 -> 0.988, 1480
 // items of 8192 nonzeros 0.726 -> 0.672; one item per SM (148 x 131071) 1.019 -> 1.025, so a single
 // wave keeps one CTA per item.  SKETCH_F4_PERSIST = 0 | 1 forces the choice.

@@ -278,8 +278,8 @@ def set_rad_f64_path(path) -> None:
 
 
 def set_f4_persistent(mode) -> None:
-    """Tensor-core columns of plans built from now on: "auto" (persistent kernel when the mean column
-    is short; default), "off" (one CTA per item) or "on" (persistent)."""
+    """Tensor-core columns of plans built from now on: "auto" (persistent kernel when there are more
+    items than SMs; default), "off" (one CTA per item) or "on" (persistent)."""
     m = {"auto": -1, "off": 0, "on": 1}[mode] if isinstance(mode, str) else int(mode)
     _check(load_library().sketch_set_f4_persistent(m), "sketch_set_f4_persistent")
 

@@ -463,6 +463,13 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
 // the same global stage sequence g (ring slot g % 2, phase g / 2); A warps without a tile in an
 // item (T < 6) skip it and wait for its accumulators, and the B warps arrive on the stage barriers
 // in their place.
+// 4 K-steps per smem stage (2 stages of 6 x 16 KB + 4 x 2.5 KB): more independent Philox chains per
+// producer warp between two handshakes (c5 7.155 -> 7.085 ms; the per-item kernel keeps 3, which it
+// measured faster at ptxas -O1: 7.31 vs 7.35 ms)
+constexpr int kF4PSub = 4;
+constexpr int kF4PATileS = kF4PSub * kF4ATile;
+constexpr int kF4PStage = kF4Tiles * kF4PATileS + kF4PSub * kF4BSub;
+constexpr int kF4PJSlots = 2;                       // nonzero-stream ring: one slot = one smem stage
 constexpr int kF4PScanWarp = kF4MmaWarp + 1;
 constexpr int kF4PThreads = (kF4PScanWarp + 1) * 32;
 constexpr int kF4PEpiWarps = kF4AWarps;            // epilogue: the 12 A warps (lane quarter = warp % 4)
@@ -470,14 +477,14 @@ constexpr int kF4PEpiWarps = kF4AWarps;            // epilogue: the 12 A warps (
 struct F4PShared {
   uint64_t full[kF4Stages];
   uint64_t empty[kF4Stages];
-  uint64_t jfull[kF4JSlots];
-  uint64_t jempty[kF4JSlots];
+  uint64_t jfull[kF4PJSlots];
+  uint64_t jempty[kF4PJSlots];
   uint64_t done;                // MMA -> epilogue: one phase per item
   uint64_t tfree;               // epilogue -> MMA: accumulators read out, one phase per item
   uint64_t efull[2];            // scan warp -> B producers / epilogue: E of item k in slot k % 2
   uint64_t eempty[2];
-  uint32_t js[kF4JSlots][64 * kF4Sub];
-  double vs[kF4JSlots][64 * kF4Sub];
+  uint32_t js[kF4PJSlots][64 * kF4PSub];
+  double vs[kF4PJSlots][64 * kF4PSub];
   int64_t item[2];              // item index of the CTA's item k in slot k % 2 (-1: no more items)
   unsigned long long mx0;       // max |a| bits of item 0 (scanned by the whole CTA)
   int32_t E[2];
@@ -504,7 +511,7 @@ __device__ __forceinline__ F4PItem f4p_item(const ApplyArgs& P, const TcItem* it
   r.T = it.ntiles;
   r.pad = it.pad;
   r.nsteps = (int)((r.pe - r.pb + 63) >> 6);
-  r.nsup = (r.nsteps + kF4Sub - 1) / kF4Sub;
+  r.nsup = (r.nsteps + kF4PSub - 1) / kF4PSub;
   return r;
 }
 
@@ -539,7 +546,8 @@ __device__ __forceinline__ unsigned long long f4p_scan(const double* __restrict_
   return r;
 }
 
-static_assert(kF4Stages == 2 && kF4JSlots == 2, "the persistent kernel indexes its rings with g & 1");
+static_assert(kF4Stages == 2 && kF4PJSlots == 2, "the persistent kernel indexes its rings with g & 1");
+static_assert(kF4Stages * kF4PStage + 8192 <= 227 * 1024, "persistent kernel shared memory");
 
 // A wait expected to last long (an item, or the rest of one): poll with explicit sleeps instead of
 // the try_wait loop, whose ~40 ns suspensions cost the producers ~7% of an SMSP per waiting warp.
@@ -560,7 +568,7 @@ __device__ __forceinline__ void f4_arrive_cnt(uint64_t* bar, uint32_t cnt) {
 // One smem stage of S tile t (nonzero half h) for global stage g (as sk_rad_f4_kernel's A loop).
 __device__ __forceinline__ void f4p_a_stage(F4PShared& sh, unsigned char* stages, const PhiloxKeys& keys,
                                             uint64_t row_offset, uint32_t g, uint32_t q, int t, int h, int lane) {
-  constexpr int kMine = kF4Sub;
+  constexpr int kMine = kF4PSub;
   const uint32_t stage = g & 1u, use = g >> 1, jslot = g & 1u;
   const int jl = 32 * h + lane;
   f4_wait(&sh.jfull[jslot], use & 1u);
@@ -577,7 +585,7 @@ __device__ __forceinline__ void f4p_a_stage(F4PShared& sh, unsigned char* stages
   }
   f4_transpose<4 * kMine>(x, lane);
   if (use > 0) f4_wait(&sh.empty[stage], (use - 1) & 1u);
-  const uint32_t tile = s_u32(stages + stage * kF4Stage) + (uint32_t)(t * kF4ATileS) + f4_off(lane, h);
+  const uint32_t tile = s_u32(stages + stage * kF4PStage) + (uint32_t)(t * kF4PATileS) + f4_off(lane, h);
 #pragma unroll
   for (int i = 0; i < kMine; ++i)
 #pragma unroll
@@ -654,14 +662,14 @@ __global__ void __launch_bounds__(kF4PThreads, 1) sk_rad_f4p_kernel(const ApplyA
                                                                      unsigned long long* next_item) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* stages = smem_raw + ((1024u - (s_u32(smem_raw) & 1023u)) & 1023u);
-  F4PShared& sh = *reinterpret_cast<F4PShared*>(stages + kF4Stages * kF4Stage);
+  F4PShared& sh = *reinterpret_cast<F4PShared*>(stages + kF4Stages * kF4PStage);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t G = gridDim.x;
   const double* vals = reinterpret_cast<const double*>(P.vals);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kF4Stages; ++s) { f4_mbar_init(&sh.full[s], kF4AWarps + kF4BWarps); f4_mbar_init(&sh.empty[s], 1); }
-    for (int s = 0; s < kF4JSlots; ++s) { f4_mbar_init(&sh.jfull[s], 32); f4_mbar_init(&sh.jempty[s], kF4AWarps + kF4BWarps); }
+    for (int s = 0; s < kF4PJSlots; ++s) { f4_mbar_init(&sh.jfull[s], 32); f4_mbar_init(&sh.jempty[s], kF4AWarps + kF4BWarps); }
     f4_mbar_init(&sh.done, 1);
     f4_mbar_init(&sh.tfree, kF4PEpiWarps);
     for (int s = 0; s < 2; ++s) { f4_mbar_init(&sh.efull[s], 1); f4_mbar_init(&sh.eempty[s], kF4PEpiWarps + kF4BWarps); }
@@ -673,10 +681,10 @@ __global__ void __launch_bounds__(kF4PThreads, 1) sk_rad_f4p_kernel(const ApplyA
                  :: "r"(s_u32(&sh.tmem_base)), "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  for (int i = threadIdx.x; i < kF4Stages * kF4Sub * 8 * 2; i += blockDim.x) {
-    const int s = i / (16 * kF4Sub), sub = (i / 16) % kF4Sub, row = kF4Ones + (i % 16) / 2, h = i & 1;
+  for (int i = threadIdx.x; i < kF4Stages * kF4PSub * 8 * 2; i += blockDim.x) {
+    const int s = i / (16 * kF4PSub), sub = (i / 16) % kF4PSub, row = kF4Ones + (i % 16) / 2, h = i & 1;
     const uint32_t v = row == kF4Ones ? 0x22222222u : 0u;
-    const uint32_t a = s_u32(stages + s * kF4Stage + kF4Tiles * kF4ATileS + sub * kF4BSub) + f4_off(row, h);
+    const uint32_t a = s_u32(stages + s * kF4PStage + kF4Tiles * kF4PATileS + sub * kF4BSub) + f4_off(row, h);
     asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" :: "r"(a), "r"(v) : "memory");
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -758,17 +766,17 @@ __global__ void __launch_bounds__(kF4PThreads, 1) sk_rad_f4p_kernel(const ApplyA
       const double sc1 = ldexp(1.0, e1), sc2 = ldexp(1.0, 61 - E - e1);
       for (int ss = 0; ss < it.nsup; ++ss, ++g) {
         const uint32_t stage = g & 1u, use = g >> 1, jslot = g & 1u;
-        uint32_t x[2 * kF4Sub];
-        int nval[kF4Sub];
+        uint32_t x[2 * kF4PSub];
+        int nval[kF4PSub];
         f4_wait(&sh.jfull[jslot], use & 1u);
-        double vv[kF4Sub];
+        double vv[kF4PSub];
 #pragma unroll
-        for (int sub = 0; sub < kF4Sub; ++sub) vv[sub] = sh.vs[jslot][64 * sub + 32 * h + lane];
+        for (int sub = 0; sub < kF4PSub; ++sub) vv[sub] = sh.vs[jslot][64 * sub + 32 * h + lane];
         __syncwarp();
         if (lane == 0) f4_arrive_cnt(&sh.jempty[jslot], cnt);
 #pragma unroll
-        for (int sub = 0; sub < kF4Sub; ++sub) {
-          const int ks = kF4Sub * ss + sub;
+        for (int sub = 0; sub < kF4PSub; ++sub) {
+          const int ks = kF4PSub * ss + sub;
           const int64_t c0 = it.pb + (int64_t)ks * 64 + 32 * h;
           nval[sub] = (int)(it.pe - c0 < 0 ? 0 : (it.pe - c0 > 32 ? 32 : it.pe - c0));
           unsigned long long U = 0ull;
@@ -779,11 +787,11 @@ __global__ void __launch_bounds__(kF4PThreads, 1) sk_rad_f4p_kernel(const ApplyA
           x[2 * sub] = ~(uint32_t)U;
           x[2 * sub + 1] = ~(uint32_t)(U >> 32);
         }
-        f4_transpose<2 * kF4Sub>(x, lane);
+        f4_transpose<2 * kF4PSub>(x, lane);
         if (use > 0) f4_wait(&sh.empty[stage], (use - 1) & 1u);
 #pragma unroll
-        for (int sub = 0; sub < kF4Sub; ++sub) {
-          const uint32_t bt = s_u32(stages + stage * kF4Stage + kF4Tiles * kF4ATileS + sub * kF4BSub);
+        for (int sub = 0; sub < kF4PSub; ++sub) {
+          const uint32_t bt = s_u32(stages + stage * kF4PStage + kF4Tiles * kF4PATileS + sub * kF4BSub);
           f4_store_row_masked(bt + f4_off(lane, h), x[2 * sub], nval[sub]);
           f4_store_row_masked(bt + f4_off(32 + lane, h), x[2 * sub + 1], nval[sub]);
           // (the ones row stays all +1.0: the padding's share of D[i, 64] is removed in the read-out)
@@ -804,8 +812,8 @@ __global__ void __launch_bounds__(kF4PThreads, 1) sk_rad_f4p_kernel(const ApplyA
         const uint32_t slot = g & 1u, use = g >> 1;
         if (use > 0) f4_wait(&sh.jempty[slot], (use - 1) & 1u);
 #pragma unroll
-        for (int e = 0; e < 2 * kF4Sub; ++e) {
-          const int64_t p = it.pb + (int64_t)ss * (64 * kF4Sub) + 32 * e + lane;
+        for (int e = 0; e < 2 * kF4PSub; ++e) {
+          const int64_t p = it.pb + (int64_t)ss * (64 * kF4PSub) + 32 * e + lane;
           const bool ok = p < it.pe;
           const int64_t ps = ok ? p : it.pb;
           asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;"
@@ -835,13 +843,13 @@ __global__ void __launch_bounds__(kF4PThreads, 1) sk_rad_f4p_kernel(const ApplyA
           const uint32_t stage = g & 1u;
           f4_wait(&sh.full[stage], (g >> 1) & 1u);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t sb = s_u32(stages + stage * kF4Stage);
-          for (int sub = 0; sub < kF4Sub; ++sub) {
-            const int ks = kF4Sub * ss + sub;
+          const uint32_t sb = s_u32(stages + stage * kF4PStage);
+          for (int sub = 0; sub < kF4PSub; ++sub) {
+            const int ks = kF4PSub * ss + sub;
             if (ks >= it.nsteps) break;
-            const uint64_t bdesc = f4_desc(sb + kF4Tiles * kF4ATileS + sub * kF4BSub);
+            const uint64_t bdesc = f4_desc(sb + kF4Tiles * kF4PATileS + sub * kF4BSub);
             for (int tt = 0; tt < it.T; ++tt) {
-              const uint64_t adesc = f4_desc(sb + tt * kF4ATileS + sub * kF4ATile);
+              const uint64_t adesc = f4_desc(sb + tt * kF4PATileS + sub * kF4ATile);
               asm volatile(
                   "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                   "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}"
@@ -942,7 +950,7 @@ cudaError_t launch_apply_rad_f4(const ApplyArgs& a, const TcItem* items, int64_t
     e = cudaGetLastError();
   }
   if (e == cudaSuccess && persist) {
-    const size_t psmem = (size_t)kF4Stages * kF4Stage + sizeof(F4PShared) + 1024;
+    const size_t psmem = (size_t)kF4Stages * kF4PStage + sizeof(F4PShared) + 1024;
     e = set_max_dynamic_smem((const void*)sk_rad_f4p_kernel, psmem);
     int dev = 0, sms = 148;
     if (e == cudaSuccess) e = cudaGetDevice(&dev);

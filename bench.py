@@ -102,7 +102,7 @@ class ClockSampler:
 
 def launches_per_apply(plan, dist: str, stats: dict) -> int:
     """Kernels of the library one sketch_apply launches.  ±1: the tensor-core kernel with its IEEE fix-up
-    of non-finite columns (and the zeroing of the K-split rows when the plan split its last wave) when columns of 1280 ..
+    of non-finite columns (and the zeroing of the K-split rows when the plan split its last wave) when columns of 896 ..
     131071 nonzeros exist (fp64), the SIMT kernel for the other columns, and for fp32 the IEEE fix-up
     scan.  Uniform / Gaussian: the fused kernel, or Algorithm 4's gather + kernel (+ the finishing sum
     of split column blocks)."""

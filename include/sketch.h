@@ -181,7 +181,8 @@ const char* sketch_version(void);
  * Both compute the same Â within the parity bound |Â - oracle| <= 1e-12 |S||A|.
  *  SK_PATH_TC_FP4 (default): the tcgen05 kind::mxf4 kernel (±1 as e2m1, values as 64 signed binary
  *    digits of a per-column fixed-point scale; exact up to the value rounding <= L 2^-62 max|a| and one
- *    final fp64 rounding) for every column with 1280 .. 131071 nonzeros, and the SIMT kernel,
+ *    final fp64 rounding) for every column with 896 (1280 when the tensor-core items fill at most
+ *    one wave of SMs) .. 131071 nonzeros, and the SIMT kernel,
  *    concurrently on a side stream, for the other columns of the same plan.  A column holding a NaN
  *    or an Inf gets the IEEE result (NaN, or the common sign of its infinite terms), as the SIMT
  *    kernel and the oracle do.

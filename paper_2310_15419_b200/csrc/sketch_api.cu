@@ -187,7 +187,7 @@ std::vector<sk::TcItem> build_tc_schedule(const int64_t* colptr, int64_t d, int6
 
 // Kernel used for ±1 with fp64 values (process-wide, read when a plan is built; results agree
 // within the parity bound): SK_PATH_TC_FP4 (default: the tensor-core kernel for every column of
-// f4_min_column() .. kTcMaxColumn nonzeros, the SIMT kernel for the others, concurrently) or
+// f4_min_column(..) .. kTcMaxColumn nonzeros, the SIMT kernel for the others, concurrently) or
 // SK_PATH_SIMT (the SIMT kernel for every column).  Initialised from SKETCH_RAD_F64_PATH = fp4 | simt.
 std::atomic<int> g_rad_f64_path{-1};
 
@@ -203,11 +203,12 @@ int rad_f64_path() {
 
 // Shortest column the tensor-core kernel takes (shorter ones go to the SIMT kernel, whose CTA has
 // no TMEM / barrier / pipeline fill and drain to amortise): the measured crossover at d = 2000
-// (scripts/f4_threshold_sweep.py, profiles/r02_f4_threshold_sweep.txt: fp4 / SIMT time 1.16 at
-// L = 1024, 0.94 at 1536).  SKETCH_F4_MIN_COL (tuning only) overrides it.
-int64_t f4_min_column() {
-  static const int64_t v = [] { const char* e = getenv("SKETCH_F4_MIN_COL"); return e ? std::max<int64_t>(1, atoll(e)) : 1280; }();
-  return v;
+// (scripts/f4_threshold_sweep.py, profiles/r02_f4_threshold_sweep.txt, tensor-core / SIMT time):
+// persistent kernel 1.08 at L = 768, 0.85 at 1024 -> 896; one CTA per item 1.16 at 1024, 0.94 at
+// 1536 -> 1280.  SKETCH_F4_MIN_COL (tuning only) overrides both.
+int64_t f4_min_column(bool persistent) {
+  static const int64_t v = [] { const char* e = getenv("SKETCH_F4_MIN_COL"); return e ? std::max<int64_t>(1, atoll(e)) : 0; }();
+  return v > 0 ? v : (persistent ? 896 : 1280);
 }
 
 // Persistent tensor-core kernel (one CTA per SM walking the items; TMEM / barriers / constant rows set
@@ -603,16 +604,27 @@ int make_plan(sk_plan_t* out, sk_dtype_t dtype, int64_t d, int64_t m, int64_t n,
       fprintf(stderr, "  make_plan %s: %.3f ms\n", what,
               std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tm0).count());
   };
-  // ±1 x fp64: columns with f4_min_column() .. kTcMaxColumn nonzeros run on the tensor cores, the
+  // ±1 x fp64: columns with f4_min_column(..) .. kTcMaxColumn nonzeros run on the tensor cores, the
   // others on the SIMT kernel (per column, not per matrix; the two launches run concurrently)
   std::vector<sk::TcItem> f4;
   std::vector<int32_t> simt_cols;
   const bool use_f4 = dtype == SK_F64 && rad_f64_path() == SK_PATH_TC_FP4;
   if (use_f4) {
     std::vector<int32_t> tc_cols;
-    for (int64_t k = 0; k < n; ++k) {
-      const int64_t L = h_colptr[k + 1] - h_colptr[k];
-      (L >= f4_min_column() && L <= sk::kTcMaxColumn ? tc_cols : simt_cols).push_back((int32_t)k);
+    auto route = [&](int64_t min_col) {
+      tc_cols.clear();
+      simt_cols.clear();
+      for (int64_t k = 0; k < n; ++k) {
+        const int64_t L = h_colptr[k + 1] - h_colptr[k];
+        (L >= min_col && L <= sk::kTcMaxColumn ? tc_cols : simt_cols).push_back((int32_t)k);
+      }
+    };
+    // the persistent kernel pays from f4_min_column(true) nonzeros on; with a single wave of items
+    // (the per-item kernel) the longer f4_min_column(false)
+    route(f4_min_column(true));
+    if (!tc_cols.empty()) {
+      const int64_t groups = ((d + 127) / 128 + sk::f4_tiles_per_cta() - 1) / sk::f4_tiles_per_cta();
+      if (!f4_use_persistent((int64_t)tc_cols.size() * groups)) route(f4_min_column(false));
     }
     if (!tc_cols.empty()) {
       f4 = build_tc_schedule(h_colptr, d, sk::f4_tiles_per_cta(), tc_cols);

@@ -272,7 +272,8 @@ def sketch_fill_s(seed, dist, i0, i1, j0, j1, dtype="f64", device="cuda", stream
 
 def set_rad_f64_path(path) -> None:
     """Select the kernel for ±1 sketches of fp64 values in plans built from now on: "fp4" (tensor
-    cores for columns of 1280 .. 131071 nonzeros, SIMT for the rest; default) or "simt" (process-wide)."""
+    cores for columns of 896 (1280 for a single wave of items) .. 131071 nonzeros, SIMT for the rest;
+    default) or "simt" (process-wide)."""
     p = RAD_F64_PATHS[path] if isinstance(path, str) else int(path)
     _check(load_library().sketch_set_rad_f64_path(p), "sketch_set_rad_f64_path")
 

@@ -49,8 +49,8 @@ def main():
         t4, n4 = time_path("fp4", A, a.d)
         ts, ns = time_path("simt", A, a.d)
         e = 2.0 * a.d * A.nnz
-        print(f"L {L:6d} n {n:6d}  fp4 {t4:8.3f} ms ({e / t4 / 1e9:8.0f} GF/s, {n4.split(' ')[0]})  "
-              f"simt {ts:8.3f} ms ({e / ts / 1e9:8.0f} GF/s)  fp4/simt {t4 / ts:.3f}", flush=True)
+        print(f"L {L:6d} n {n:6d}  fp4 {t4:8.3f} ms ({e / t4 / 1e9:8.0f} TF/s, {n4.split(' ')[0]})  "
+              f"simt {ts:8.3f} ms ({e / ts / 1e9:8.0f} TF/s)  fp4/simt {t4 / ts:.3f}", flush=True)
     sk.set_rad_f64_path("fp4")
 
 

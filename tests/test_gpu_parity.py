@@ -170,7 +170,7 @@ def test_rad_f64_kernel_paths(sk, path):
     # relative to the rest, unsorted rows with duplicates, explicit zeros and huge / tiny values
     try:
         sk.set_rad_f64_path(path)
-        # (columns of 1280 .. 131071 nonzeros run on the tensor cores, the others on the SIMT kernel)
+        # (columns of 896 / 1280 .. 131071 nonzeros run on the tensor cores, the others on the SIMT kernel)
         cases = [workloads.random_csc(50000, 40, 1300, seed=2),
                  workloads.random_csc(30000, 12, [0, 500, 0, 0, 1640, 1, 0, 3300, 0, 2, 0, 1279], seed=5),
                  workloads.random_csc(200000, 24, [20000] + [10] * 23, seed=6),
@@ -295,7 +295,7 @@ def test_f4_long_columns_next_to_tensor_columns(sk):
     # stream, while every other column stays on sk_rad_f4_kernel; results match the oracle and two
     # runs are bit-identical
     import torch
-    lens = [300000, 131072, 131071, 3000, 1279, 1280, 700, 90]
+    lens = [300000, 131072, 131071, 3000, 1279, 1280, 700, 90]   # (one wave of items: threshold 1280)
     A = workloads.random_csc(400000, len(lens), lens, seed=29)
     plan = sk.Plan(_dev(A.colptr), _dev(A.rowidx), 1300, A.m, "f64")
     try:

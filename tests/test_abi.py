@@ -67,6 +67,22 @@ def test_argument_validation_happens_before_any_device_work(lib):
     assert lib.sketch_plan_stats(None, None) == sk.SK_EINVAL
 
 
+def test_kernel_selectors_validate_on_host(lib):
+    # the process-wide selectors take only their documented values (no device work)
+    from paper_2310_15419_b200 import sketch as sk
+    for bad in (-2, 2, 7):
+        assert lib.sketch_set_f4_persistent(bad) == sk.SK_EINVAL
+    for bad in (1, 2, 4, -1):
+        assert lib.sketch_set_rad_f64_path(bad) == sk.SK_EINVAL
+    for bad in (3, -1):
+        assert lib.sketch_set_pair_path(bad) == sk.SK_EINVAL
+    for good in (-1, 0, 1):
+        assert lib.sketch_set_f4_persistent(good) == sk.SK_OK
+    assert lib.sketch_set_f4_persistent(-1) == sk.SK_OK       # back to auto
+    with pytest.raises(KeyError):
+        sk.set_f4_persistent("sometimes")
+
+
 def test_host_entry_point_validates_colptr_on_host(lib):
     import numpy as np
     from paper_2310_15419_b200 import sketch as sk

@@ -347,6 +347,32 @@ def test_f4_persistent_kernel_matches_per_item_kernel(sk, d):
     _check(outs["on"][:, keep], ref[:, keep], B[:, keep], TOL["f64"])
 
 
+def test_f4_persistent_kernel_with_row_offset(sk):
+    # a row shard (global row keys j + row_offset > 2^32) on the persistent kernel: its read-out
+    # removes the padding's share of the ones row with S[i, row_offset], so a wrong offset there
+    # would show in every column whose length is not a multiple of 64
+    import torch
+    rng = np.random.default_rng(5)
+    lens = [int(x) for x in rng.integers(900, 4000, size=180)]
+    A = workloads.random_csc(70000, len(lens), lens, seed=55)
+    A.row_offset = (1 << 32) + 777
+    try:
+        sk.set_f4_persistent("on")
+        plan = sk.Plan(_dev(A.colptr), _dev(A.rowidx), 1000, A.m, "f64", row_offset=A.row_offset)
+        try:
+            st = plan.stats()
+            assert st["f4_persistent"] == 1 and st["n_cols_f4"] == len(lens)
+            got = plan.apply(_dev(A.vals), 29, "rademacher").T.cpu().numpy()
+            torch.cuda.synchronize()
+        finally:
+            plan.close()
+    finally:
+        sk.set_f4_persistent("auto")
+    ref, B = oracle.sketch(29, "rademacher", 1000, A.m, A.n, A.colptr, A.rowidx, A.vals, row_offset=A.row_offset,
+                           threads=16)
+    _check(got, ref, B, TOL["f64"])
+
+
 def test_f4_persistent_selection(sk):
     # the plan picks the persistent kernel when there is more than one wave of tensor-core items (600
     # items here, c5's 3188) and one CTA per item for a single wave (80 items)

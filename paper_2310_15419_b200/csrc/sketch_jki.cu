@@ -62,9 +62,10 @@ static_assert(kJHdrRing >= 2 * kJDepth && kJDepth >= 2, "ring sizes");
 
 template <typename T>
 struct JSlot {                                   // byte layout of one ring slot
-  static constexpr int desc = 0;                                   // uint32 [kJBatchEnt]
-  static constexpr int vals = desc + kJBatchEnt * 4;               // T [kJBatchEnt]
-  static constexpr int rj = vals + kJBatchEnt * (int)sizeof(T);    // int32 [kJBatch]
+  // entry records [kJBatchEnt]: descriptor at +0, value at +sizeof(T) (one 16-byte load in fp64)
+  static constexpr int ent = 2 * (int)sizeof(T);
+  static constexpr int ents = 0;
+  static constexpr int rj = ents + kJBatchEnt * ent;               // int32 [kJBatch]
   static constexpr int own = rj + kJBatch * 4;                     // uint16 [kJOwnStride]
   static constexpr int bytes = (own + kJOwnStride * 2 + 15) & ~15;
 };
@@ -144,9 +145,10 @@ __global__ void __launch_bounds__(kJThreads, 1) sk_jki_kernel(const ApplyArgs P,
     const JBatch& B = hdr[(x - bt0) % kJHdrRing];
     unsigned char* sl = slot_of(x);
     if (tid < B.nent) {
-      cp_async4(sl + JSlot<T>::desc + 4 * tid, J.ent_desc + B.ent0 + tid);
-      if constexpr (sizeof(T) == 8) cp_async8(sl + JSlot<T>::vals + 8 * tid, vcsr + B.ent0 + tid);
-      else cp_async4(sl + JSlot<T>::vals + 4 * tid, vcsr + B.ent0 + tid);
+      unsigned char* rec = sl + JSlot<T>::ents + JSlot<T>::ent * tid;
+      cp_async4(rec, J.ent_desc + B.ent0 + tid);
+      if constexpr (sizeof(T) == 8) cp_async8(rec + 8, vcsr + B.ent0 + tid);
+      else cp_async4(rec + 4, vcsr + B.ent0 + tid);
     }
     if (tid < B.nrows) cp_async4(sl + JSlot<T>::rj + 4 * tid, J.row_j + B.row0 + tid);
     if (tid < kJOwnStride / 2) cp_async4(sl + JSlot<T>::own + 4 * tid, J.own + (int64_t)x * kJOwnStride + 2 * tid);
@@ -203,17 +205,33 @@ __global__ void __launch_bounds__(kJThreads, 1) sk_jki_kernel(const ApplyArgs P,
     cp_async_commit();
     {                                                              // scatter batch x
       const unsigned char* sl = slot_of(x);
-      const uint32_t* ed = reinterpret_cast<const uint32_t*>(sl + JSlot<T>::desc);
-      const T* ev = reinterpret_cast<const T*>(sl + JSlot<T>::vals);
+      const unsigned char* er = sl + JSlot<T>::ents;
       const uint16_t* own = reinterpret_cast<const uint16_t*>(sl + JSlot<T>::own);
       const char* Sb = reinterpret_cast<const char*>(S + b * (kJBatch * kJQ) + i);
       char* acci = reinterpret_cast<char*>(acc + i);
       const int e1 = own[hw + 1];
+      // an owner's entries come in row order, so consecutive entries of one row reuse the S pair
+      // already in registers (one record load + the accumulator load and store per entry)
+      uint32_t prev = 0xFFFFFFFFu;
+      V2 sv{T(0), T(0)};
       for (int e = own[hw]; e < e1; ++e) {
-        const uint32_t dsc = ed[e];
-        const T a = ev[e];
+        uint32_t dsc;
+        T a;
+        if constexpr (sizeof(T) == 8) {
+          const uint4 r = *reinterpret_cast<const uint4*>(er + 16 * e);
+          dsc = r.x;
+          a = __hiloint2double((int)r.w, (int)r.z);
+        } else {
+          const uint2 r = *reinterpret_cast<const uint2*>(er + 8 * e);
+          dsc = r.x;
+          a = __uint_as_float(r.y);
+        }
         V2* slot = reinterpret_cast<V2*>(acci + (dsc & 0x1FFFFu));
-        const V2 sv = *reinterpret_cast<const V2*>(Sb + (dsc >> 17));
+        const uint32_t soff = dsc >> 17;
+        if (soff != prev) {
+          sv = *reinterpret_cast<const V2*>(Sb + soff);
+          prev = soff;
+        }
         V2 av = *slot;
         av.x = fma(sv.x, a, av.x);
         av.y = fma(sv.y, a, av.y);

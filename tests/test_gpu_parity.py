@@ -347,6 +347,26 @@ def test_f4_persistent_kernel_matches_per_item_kernel(sk, d):
     _check(outs["on"][:, keep], ref[:, keep], B[:, keep], TOL["f64"])
 
 
+@pytest.mark.parametrize("d", [100, 129, 768])
+def test_f4_persistent_kernel_edge_shapes(sk, d):
+    # persistent kernel with 1-tile items (10 idle S warps per item: the digit warps arrive for them),
+    # a ragged last tile, columns at the thresholds (896, 131071), lengths that fill whole K-steps
+    # (no padding) and lengths one past them
+    import torch
+    lens = [896, 131071, 1024, 1025, 4096, 4097, 963] + [900 + 7 * k for k in range(200)]
+    A = workloads.random_csc(400000, len(lens), lens, seed=61)
+    plan = sk.Plan(_dev(A.colptr), _dev(A.rowidx), d, A.m, "f64")
+    try:
+        st = plan.stats()
+        assert st["f4_persistent"] == 1 and st["n_cols_f4"] == len(lens), st
+        got = plan.apply(_dev(A.vals), 31, "rademacher").T.cpu().numpy()
+        torch.cuda.synchronize()
+    finally:
+        plan.close()
+    ref, B = oracle.sketch(31, "rademacher", d, A.m, A.n, A.colptr, A.rowidx, A.vals, threads=16)
+    _check(got, ref, B, TOL["f64"])
+
+
 def test_f4_persistent_kernel_with_row_offset(sk):
     # a row shard (global row keys j + row_offset > 2^32) on the persistent kernel: its read-out
     # removes the padding's share of the ones row with S[i, row_offset], so a wrong offset there

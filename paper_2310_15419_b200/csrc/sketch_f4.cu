@@ -467,6 +467,13 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
 // producer warp between two handshakes (c5 7.155 -> 7.085 ms; the per-item kernel keeps 3, which it
 // measured faster at ptxas -O1: 7.31 vs 7.35 ms)
 constexpr int kF4PSub = 4;
+// The scan warp starts the next item's column scan when the running item has SK_F4P_SCANLEAD stages
+// to go: started an item ahead, the scanned values (148 columns in flight) were evicted from L2
+// before the loader read them, DRAM 699 MB per c5 launch; at 64 stages 627 MB (616 algorithmic) at
+// the same time (scripts/gpurun/gpu_r2bj.sh).  0: scan as soon as the slot is free.
+#ifndef SK_F4P_SCANLEAD
+#define SK_F4P_SCANLEAD 64
+#endif
 constexpr int kF4PATileS = kF4PSub * kF4ATile;
 constexpr int kF4PStage = kF4Tiles * kF4PATileS + kF4PSub * kF4BSub;
 constexpr int kF4PJSlots = 2;                       // nonzero-stream ring: one slot = one smem stage
@@ -487,6 +494,7 @@ struct F4PShared {
   double vs[kF4PJSlots][64 * kF4PSub];
   int64_t item[2];              // item index of the CTA's item k in slot k % 2 (-1: no more items)
   unsigned long long mx0;       // max |a| bits of item 0 (scanned by the whole CTA)
+  uint32_t loaded;              // stages the loader has issued (the scan warp starts item k + 1's scan late)
   int32_t E[2];
   int32_t nonfinite[2];
   uint32_t tmem_base;
@@ -674,6 +682,7 @@ __global__ void __launch_bounds__(kF4PThreads, 1) sk_rad_f4p_kernel(const ApplyA
     f4_mbar_init(&sh.tfree, kF4PEpiWarps);
     for (int s = 0; s < 2; ++s) { f4_mbar_init(&sh.efull[s], 1); f4_mbar_init(&sh.eempty[s], kF4PEpiWarps + kF4BWarps); }
     sh.mx0 = 0ull;
+    sh.loaded = 0u;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kF4MmaWarp) {
@@ -822,6 +831,9 @@ __global__ void __launch_bounds__(kF4PThreads, 1) sk_rad_f4p_kernel(const ApplyA
                        :: "r"(s_u32(&sh.vs[slot][32 * e + lane])), "l"(vals + ps), "r"(ok ? 8 : 0) : "memory");
         }
         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" :: "r"(s_u32(&sh.jfull[slot])) : "memory");
+#if SK_F4P_SCANLEAD
+        if (lane == 0) *reinterpret_cast<volatile uint32_t*>(&sh.loaded) = g + 1;
+#endif
       }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
@@ -872,8 +884,17 @@ __global__ void __launch_bounds__(kF4PThreads, 1) sk_rad_f4p_kernel(const ApplyA
     // ===================== scan warp: the CTA's next item and its column scale E, one item ahead ====
     // Item 0 is blockIdx.x; later items come from a global counter (dynamic: CTAs that drew shorter
     // items take more of them, as the hardware scheduler does for one CTA per item).
+    uint32_t g_start = 0, nsup_prev = 0;           // stage range of item k - 1 (the one running)
     for (int64_t k = 0;; ++k) {
       if (k >= 2) f4_wait_sleep(&sh.eempty[k & 1], (uint32_t)(((k >> 1) - 1) & 1), 2000);
+#if SK_F4P_SCANLEAD
+      // scan item k while item k - 1 has its last SK_F4P_SCANLEAD stages to go (earlier, the scanned
+      // values are evicted from L2 before the loader reads them)
+      if (k >= 1 && nsup_prev > SK_F4P_SCANLEAD) {
+        const uint32_t until = g_start + nsup_prev - SK_F4P_SCANLEAD;
+        while (*reinterpret_cast<volatile uint32_t*>(&sh.loaded) < until) __nanosleep(500);
+      }
+#endif
       int64_t idx = blockIdx.x;
       if (k > 0) {
         unsigned long long v = 0;
@@ -882,9 +903,11 @@ __global__ void __launch_bounds__(kF4PThreads, 1) sk_rad_f4p_kernel(const ApplyA
       }
       if (idx >= n_items) idx = -1;
       unsigned long long mx = k == 0 ? sh.mx0 : 0ull;
-      if (idx >= 0 && k > 0) {
+      if (idx >= 0) {
         const F4PItem it = f4p_item(P, items, idx);
-        mx = f4p_scan(vals, it.pb, it.pe, lane);
+        if (k > 0) mx = f4p_scan(vals, it.pb, it.pe, lane);
+        if (k > 0) g_start += nsup_prev;
+        nsup_prev = (uint32_t)it.nsup;
       }
       if (lane == 0) {
         const double m = __longlong_as_double((long long)mx);

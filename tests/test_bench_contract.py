@@ -91,12 +91,11 @@ def test_traffic_lookup_matches_the_committed_capture():
     assert v == t["c5"]["sk_rad_f4_kernel"]
     vp = bench.load_profile_traffic("c5", "sk_rad_f4p_kernel (tcgen05 kind::mxf4, persistent)")
     assert vp == t["c5"]["sk_rad_f4p_kernel"]
-    # the per-item kernel reads A once (DRAM traffic within 2% of the algorithmic bytes); the persistent
-    # one re-reads ~12% (its scan warp reads the next item's column while 148 columns are in flight:
-    # ~148 MB of working set against the 126 MB L2)
+    # both tensor-core kernels read A once: DRAM traffic within 2% (per-item) / 3% (persistent, whose
+    # scan warp reads the next item's column shortly before the loader does)
     alg = algorithmic_bytes(2000, 1000, 50_000_000, 8)
     assert abs(v - alg) / alg < 0.02
-    assert 0 <= (vp - alg) / alg < 0.15
+    assert abs(vp - alg) / alg < 0.03
 
 
 def test_metric_and_bytes_arithmetic():

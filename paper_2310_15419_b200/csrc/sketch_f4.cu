@@ -455,9 +455,11 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
 }
 
 // ============================================================================================
-// Persistent variant (SKETCH_F4_PERSIST=1): one CTA per SM walks the items blockIdx.x + k gridDim.x.
-// TMEM, the barriers, the constant B rows and the scale factors are set up once; a scan warp
-// computes the next item's column scale E while the current item runs (2-slot ring); the A
+// Persistent variant (the default when the items fill more than one wave; sketch_set_f4_persistent /
+// SKETCH_F4_PERSIST): one CTA per SM; its first item is blockIdx.x, the next ones come from a global
+// counter claimed by the scan warp (dynamic, like the hardware scheduler).  TMEM, the barriers, the
+// constant B rows and the scale factors are set up once; the scan warp computes the next item's
+// column scale E while the current item runs (2-slot ring; the whole CTA scans item 0); the A
 // producers produce the first stage of item k before they read out item k-1's accumulators, so the
 // MMA warp restarts as soon as TMEM is free (tfree) with a stage already waiting.  All roles walk
 // the same global stage sequence g (ring slot g % 2, phase g / 2); A warps without a tile in an

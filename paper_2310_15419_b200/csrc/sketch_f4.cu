@@ -122,13 +122,13 @@ __host__ __device__ constexpr uint32_t f4_idesc() {
 // LOP3 (the partner's word arrives already aligned): 2 + 5 ALU ops per word instead of 5 x 2.
 // Stage s (distance j = 16 >> s) keeps rot(m_j, lane) in the lower lane of a pair, the
 // complement in the upper lane.
-template <int NW>
+template <int NW, int NS = 5>
 __device__ __forceinline__ void f4_transpose(uint32_t (&x)[NW], int lane) {
   const uint32_t m[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
 #pragma unroll
   for (int k = 0; k < NW; ++k) x[k] = __funnelshift_l(x[k], x[k], lane);
 #pragma unroll
-  for (int s = 0; s < 5; ++s) {
+  for (int s = 0; s < NS; ++s) {
     const uint32_t rm = __funnelshift_l(m[s], m[s], lane);
     const uint32_t keep = (lane & (16 >> s)) ? ~rm : rm;
     uint32_t y[NW];
@@ -469,6 +469,29 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
 // producer warp between two handshakes (c5 7.155 -> 7.085 ms; the per-item kernel keeps 3, which it
 // measured faster at ptxas -O1: 7.31 vs 7.35 ms)
 constexpr int kF4PSub = 4;
+#ifndef SK_F4P_T4
+#define SK_F4P_T4 1                                 // c5 7.10 -> 7.00 ms (scripts/gpurun/gpu_r2bo.sh)
+#endif
+// SK_F4P_T4: the S transpose stops one butterfly stage early.  Lane r then holds row r's bits at the
+// positions of r's parity and row r^1's at the others (bit c <-> nonzero c, or c^1 for the other row),
+// so each lane stores two 8-byte halves: the even-nonzero half of row pair k = lane/2 comes from the
+// even lane, the odd half from the odd lane.  The 16-byte K chunk of a row holds its nibble words in
+// the order c0, c2, c1, c3 (word c nibble n = nonzero 4n + c), for the digits operand too, and the
+// logical rows 2k, 2k+1 sit in physical rows k, 16 + k of their 32-row group, so each 8-byte store of
+// the warp fills 16 whole rows of two core matrices (no bank conflicts); the read-out maps TMEM lane
+// l back to row 2l (l < 16) or 2(l - 16) + 1.
+// digits rows in the chunk word order c0, c2, c1, c3 (SK_F4P_T4)
+__device__ __forceinline__ void f4p_store_row_masked_perm(uint32_t addr, uint32_t y, int nvalid) {
+  uint32_t w0 = f4_nib(y << 3), w1 = f4_nib(y << 2), w2 = f4_nib(y << 1), w3 = f4_nib(y);
+  if (nvalid < 32) {
+    w0 &= f4_valid_mask(0, nvalid);
+    w1 &= f4_valid_mask(1, nvalid);
+    w2 &= f4_valid_mask(2, nvalid);
+    w3 &= f4_valid_mask(3, nvalid);
+  }
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" :: "r"(addr), "r"(w0), "r"(w2), "r"(w1), "r"(w3) : "memory");
+}
+__device__ __forceinline__ int f4p_row_of_lane(int l) { return SK_F4P_T4 ? (l < 16 ? 2 * l : 2 * (l - 16) + 1) : l; }
 // The scan warp starts the next item's column scan when the running item has SK_F4P_SCANLEAD stages
 // to go: started an item ahead, the scanned values (148 columns in flight) were evicted from L2
 // before the loader read them, DRAM 699 MB per c5 launch; at 64 stages 627 MB (616 algorithmic) at
@@ -593,6 +616,20 @@ __device__ __forceinline__ void f4p_a_stage(F4PShared& sh, unsigned char* stages
     const uint4 xb = s_block(q, row_offset + jv[i], keys);
     x[4 * i + 0] = xb.x; x[4 * i + 1] = xb.y; x[4 * i + 2] = xb.z; x[4 * i + 3] = xb.w;
   }
+#if SK_F4P_T4
+  f4_transpose<4 * kMine, 4>(x, lane);
+  if (use > 0) f4_wait(&sh.empty[stage], (use - 1) & 1u);
+  const uint32_t base = s_u32(stages + stage * kF4PStage) + (uint32_t)(t * kF4PATileS) + 8u * (uint32_t)(lane & 1);
+  const uint32_t ra = base + f4_off(lane >> 1, h), rb = base + f4_off(16 + (lane >> 1), h);
+#pragma unroll
+  for (int i = 0; i < kMine; ++i)
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq) {
+      const uint32_t y = x[4 * i + qq], o = (uint32_t)(i * kF4ATile + qq * 4 * 256);
+      asm volatile("st.shared.v2.b32 [%0], {%1, %2};" :: "r"(ra + o), "r"(f4_nib(y << 3)), "r"(f4_nib(y << 1)) : "memory");
+      asm volatile("st.shared.v2.b32 [%0], {%1, %2};" :: "r"(rb + o), "r"(f4_nib(y << 2)), "r"(f4_nib(y)) : "memory");
+    }
+#else
   f4_transpose<4 * kMine>(x, lane);
   if (use > 0) f4_wait(&sh.empty[stage], (use - 1) & 1u);
   const uint32_t tile = s_u32(stages + stage * kF4PStage) + (uint32_t)(t * kF4PATileS) + f4_off(lane, h);
@@ -601,6 +638,7 @@ __device__ __forceinline__ void f4p_a_stage(F4PShared& sh, unsigned char* stages
 #pragma unroll
     for (int qq = 0; qq < 4; ++qq)
       f4_store_row(tile + (uint32_t)(i * kF4ATile + qq * 4 * 256), x[4 * i + qq]);
+#endif
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncwarp();
   if (lane == 0) f4_arrive(&sh.full[stage]);
@@ -641,12 +679,13 @@ __device__ __forceinline__ void f4p_epilogue(F4PShared& sh, const ApplyArgs& P, 
         }
       }
     }
-    const int64_t row = (int64_t)(it.tile0 + tt) * 128 + 32 * qw + lane;
+    const int lrow = f4p_row_of_lane(lane);
+    const int64_t row = (int64_t)(it.tile0 + tt) * 128 + 32 * qw + lrow;
     const int pad = it.nsteps * 64 - (int)(it.pe - it.pb);
     if (pad > 0) {
       const uint4 x0 = s_block((uint32_t)(it.tile0 + tt), (uint64_t)P.row_offset, P.keys);
       const uint32_t w = qw == 0 ? x0.x : qw == 1 ? x0.y : qw == 2 ? x0.z : x0.w;
-      ones -= ((w >> lane) & 1u) ? -(long long)pad : (long long)pad;   // bit 1 -> S = -1
+      ones -= ((w >> lrow) & 1u) ? -(long long)pad : (long long)pad;   // bit 1 -> S = -1
     }
     if (row < P.d) {
       const double v = scalbn((double)hi * 4294967296.0 + (double)(lo - ones), E - 62);
@@ -803,8 +842,13 @@ __global__ void __launch_bounds__(kF4PThreads, 1) sk_rad_f4p_kernel(const ApplyA
 #pragma unroll
         for (int sub = 0; sub < kF4PSub; ++sub) {
           const uint32_t bt = s_u32(stages + stage * kF4PStage + kF4Tiles * kF4PATileS + sub * kF4BSub);
+#if SK_F4P_T4
+          f4p_store_row_masked_perm(bt + f4_off(lane, h), x[2 * sub], nval[sub]);
+          f4p_store_row_masked_perm(bt + f4_off(32 + lane, h), x[2 * sub + 1], nval[sub]);
+#else
           f4_store_row_masked(bt + f4_off(lane, h), x[2 * sub], nval[sub]);
           f4_store_row_masked(bt + f4_off(32 + lane, h), x[2 * sub + 1], nval[sub]);
+#endif
           // (the ones row stays all +1.0: the padding's share of D[i, 64] is removed in the read-out)
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

@@ -469,6 +469,9 @@ __global__ void __launch_bounds__(kF4Threads, 1) sk_rad_f4_kernel(const ApplyArg
 // producer warp between two handshakes (c5 7.155 -> 7.085 ms; the per-item kernel keeps 3, which it
 // measured faster at ptxas -O1: 7.31 vs 7.35 ms)
 constexpr int kF4PSub = 4;
+#ifndef SK_F4P_OFFSPEC
+#define SK_F4P_OFFSPEC 1                            // separate S-producer loop for row_offset == 0 (c5 7.00 -> 6.98 ms)
+#endif
 #ifndef SK_F4P_T4
 #define SK_F4P_T4 1                                 // c5 7.10 -> 7.00 ms (scripts/gpurun/gpu_r2bo.sh)
 #endif
@@ -599,6 +602,8 @@ __device__ __forceinline__ void f4_arrive_cnt(uint64_t* bar, uint32_t cnt) {
 }
 
 // One smem stage of S tile t (nonzero half h) for global stage g (as sk_rad_f4_kernel's A loop).
+// kOff: the plan has a row offset (a row shard); without one the Philox counter's high word is 0
+template <bool kOff>
 __device__ __forceinline__ void f4p_a_stage(F4PShared& sh, unsigned char* stages, const PhiloxKeys& keys,
                                             uint64_t row_offset, uint32_t g, uint32_t q, int t, int h, int lane) {
   constexpr int kMine = kF4PSub;
@@ -613,7 +618,7 @@ __device__ __forceinline__ void f4p_a_stage(F4PShared& sh, unsigned char* stages
   uint32_t x[4 * kMine];
 #pragma unroll
   for (int i = 0; i < kMine; ++i) {
-    const uint4 xb = s_block(q, row_offset + jv[i], keys);
+    const uint4 xb = s_block(q, kOff ? row_offset + jv[i] : (uint64_t)jv[i], keys);
     x[4 * i + 0] = xb.x; x[4 * i + 1] = xb.y; x[4 * i + 2] = xb.z; x[4 * i + 3] = xb.w;
   }
 #if SK_F4P_T4
@@ -786,11 +791,15 @@ __global__ void __launch_bounds__(kF4PThreads, 1) sk_rad_f4p_kernel(const ApplyA
         const uint32_t q = (uint32_t)(it.tile0 + t);
         int ss = 0;
         if (it.nsup > 0) {   // the first stage of item k before item k-1's epilogue
-          f4p_a_stage(sh, stages, keys, row_offset, g, q, t, h, lane);
+          if (SK_F4P_OFFSPEC && row_offset == 0) f4p_a_stage<false>(sh, stages, keys, row_offset, g, q, t, h, lane);
+          else f4p_a_stage<true>(sh, stages, keys, row_offset, g, q, t, h, lane);
           ++ss;
         }
         if (pending) f4p_epilogue(sh, P, prev, k - 1, tmem, warp, lane);
-        for (; ss < it.nsup; ++ss) f4p_a_stage(sh, stages, keys, row_offset, g + (uint32_t)ss, q, t, h, lane);
+        if (SK_F4P_OFFSPEC && row_offset == 0)
+          for (; ss < it.nsup; ++ss) f4p_a_stage<false>(sh, stages, keys, row_offset, g + (uint32_t)ss, q, t, h, lane);
+        else
+          for (; ss < it.nsup; ++ss) f4p_a_stage<true>(sh, stages, keys, row_offset, g + (uint32_t)ss, q, t, h, lane);
         pending = true;
       } else {
         if (pending) f4p_epilogue(sh, P, prev, k - 1, tmem, warp, lane);
